@@ -1,0 +1,460 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: DC loadflows/s of the batched topology screen on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config g118] [--impl ours|reference]
+
+One step = one ``bdc_solve`` over one batch of synthetic topology tasks (the
+BASELINE config: by default configs[1], a 118-bus-sized synthetic grid,
+65,536 topologies x 64 injection candidates, k=3 busbar splits, full N-1).
+A loadflow is one flow vector (topology, injection candidate, case), counted
+exactly as the reference counts it: T * (1 + feasible cases) per feasible
+task (`solver.py:881-883`).
+
+Reported (one JSON line on rank 0):
+  value     whole-job loadflows/s with inputs resident in HBM, device-timed with
+            CUDA events on the solve stream, L2 flushed between steps, max over ranks
+  e2e       the same metric through the public session API with host (pinned)
+            inputs and host outputs, copies inside the timed region (wall clock)
+  roofline  the dominant kernel (single-branch N-1 screen, k_single) against the
+            FP32 issue rate: 148 SMs x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)
+  cpu_baseline  the CPU oracle port (reference algorithm, metric_first) on the
+            host cores, bounded sample of the same workload (rank 0, N=1 only)
+
+`--impl reference` times the reference algorithm on the CPU instead (the oracle
+port, all host cores).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    # name: (grid spec, tasks per GPU per step, candidates, splits, disconnections)
+    "g14": ("g14", 1024, 16, 2, 0),
+    "g118": ("g118", 65536, 64, 3, 0),
+    "g1k": ("g1k", 8192, 128, 3, 0),
+    "g3k": ("g3k", 1024, 32, 8, 0),
+    "g10k": ("g10k", 64, 64, 3, 0),
+}
+DESCR = {
+    "g14": "IEEE-14-sized synthetic grid, 1024 topologies x 16 injections, 2 splits, full N-1",
+    "g118": "IEEE-118-sized synthetic grid, 65536 topologies x 64 injections, 3 splits, full N-1",
+    "g1k": "1000-bus synthetic grid, topologies x 128 injections, 3 splits, full N-1",
+    "g3k": "3000-bus synthetic grid, multi-split (k=8) topologies x 32 injections, full N-1",
+    "g10k": "10k-bus synthetic grid, topologies x 64 injections, 3 splits, full N-1",
+}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[6]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+            "power_w_max": max(power) if power else None,
+        }
+
+
+def make_workload(name, rank, n_tasks=None):
+    from paper_2501_17529_b200 import synth
+
+    spec, tasks, T, k, d = WORKLOADS[name]
+    if n_tasks is not None:
+        tasks = n_tasks
+    grid = synth.make_grid(spec, seed=0)
+    splits, discos, inj = synth.random_task_arrays(grid, tasks, T, k, seed=1000 + rank, n_disconnections=d)
+    return grid, splits, discos, inj
+
+
+# ---------------------------------------------------------------------------- CPU legs
+def _port_worker(args):
+    grid_doc, splits, discos, inj = args
+    from oracle import port
+    from paper_2501_17529_b200.io import grid_from_dict
+    from paper_2501_17529_b200.ptdf import prepare_base_ptdf
+    from paper_2501_17529_b200.solver import SolveConfig
+
+    grid = grid_from_dict(grid_doc)
+    base = prepare_base_ptdf(grid)
+    cfg = SolveConfig(mode="metric_first")
+    canons = port.decode_arrays(grid, splits, discos, inj)
+    t0 = time.perf_counter()
+    lf = 0
+    for c in canons:
+        r = port.solve_one(grid, base, c, cfg)
+        if r.feasible:
+            lf += c.rows.shape[0] * (1 + r.n_feasible_cases)
+    return lf, time.perf_counter() - t0, len(canons)
+
+
+def cpu_port_rate(name, budget_s=12.0, cores=None, rank=0):
+    """The reference algorithm (oracle port, metric_first) on host cores; solve-only time."""
+    import multiprocessing as mp
+
+    from paper_2501_17529_b200 import synth
+    from paper_2501_17529_b200.io import grid_to_dict
+
+    spec, _tasks, T, k, d = WORKLOADS[name]
+    cores = cores or os.cpu_count() or 1
+    grid = synth.make_grid(spec, seed=0)
+    doc = grid_to_dict(grid)
+    # calibrate the per-task cost on one core, then size the sample to ~budget_s
+    s, dd, i = synth.random_task_arrays(grid, 4, T, k, seed=77 + rank, n_disconnections=d)
+    lf0, t_0, n0 = _port_worker((doc, s, dd, i))
+    per_task = max(t_0 / n0, 1e-4)
+    n_total = int(max(cores, min(200000, budget_s * cores / per_task)))
+    per = (n_total + cores - 1) // cores
+    s, dd, i = synth.random_task_arrays(grid, per * cores, T, k, seed=99 + rank, n_disconnections=d)
+    jobs = [(doc, s[c * per:(c + 1) * per], dd[c * per:(c + 1) * per], i[c * per:(c + 1) * per]) for c in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_port_worker, jobs)
+    lf = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {
+        "value": lf / wall,
+        "unit": "loadflows/s",
+        "cores": cores,
+        "kind": "port",
+        "sample": f"{per * cores} tasks of the {name} workload ({T} candidates, k={k}), metric_first, "
+        f"{cores} processes x {per} tasks, solve-only wall {wall:.1f}s",
+        "loadflows": lf,
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    steps = []
+    last = None
+    for it in range(args.warmup + args.steps):
+        r = cpu_port_rate(args.config, budget_s=args.cpu_budget, rank=it)
+        if it >= args.warmup:
+            steps.append(r)
+        last = r
+    lf = sum(r["loadflows"] for r in steps)
+    val = statistics.mean(r["value"] for r in steps)
+    spec, tasks, T, k, d = WORKLOADS[args.config]
+    line = {
+        "impl": "reference",
+        "metric": "DC loadflows/sec (topo x inj x N-1)",
+        "value": val,
+        "unit": "loadflows/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": None,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (scaled make_fixtures recipe, random_tasks semantics)",
+        "config": {"workload": DESCR[args.config], "grid": spec, "candidates": T, "splits": k},
+        "cpu_baseline": {k2: last[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": val, "unit": "loadflows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    line["cpu_baseline"]["value"] = val
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2501_17529_b200.engine import MAX_TOPK
+    from paper_2501_17529_b200.session import session_open, solve_batch_output
+
+    spec, tasks, T, k, d = WORKLOADS[args.config]
+    if args.tasks:
+        tasks = args.tasks
+    grid, splits, discos, inj = make_workload(args.config, rank, tasks)
+    sess = session_open(grid, device=local)
+    eng = sess.engine
+    kk, dd = eng.task_ranks(splits, discos)
+    max_rank = eng.check_limits(splits, kk, dd)
+    B = splits.shape[0]
+    dev = torch.device("cuda", local)
+    t_spl = torch.from_numpy(splits.view(np.uint8)).to(dev)
+    t_dis = torch.from_numpy(discos).to(dev)
+    t_inj = torch.from_numpy(inj.view(np.uint8)).to(dev)
+    kg = sess.config.topk_global
+    ncw = max(1, (len(grid.contingencies) + 31) // 32)
+    outs = {
+        "metric": torch.empty(B, dtype=torch.float64, device=dev),
+        "best": torch.empty(B, dtype=torch.int64, device=dev),
+        "feasible": torch.empty(B, dtype=torch.uint8, device=dev),
+        "status": torch.empty(B, dtype=torch.int32, device=dev),
+        "status_arg": torch.empty(B, dtype=torch.int32, device=dev),
+        "n_islanded": torch.empty(B, dtype=torch.int32, device=dev),
+        "islanded_bits": torch.empty(B, ncw, dtype=torch.int32, device=dev),
+        "n0_count": torch.empty(B, dtype=torch.int32, device=dev),
+        "n0_pos": torch.empty(B, kg, dtype=torch.int32, device=dev),
+        "n0_flow": torch.empty(B, kg, dtype=torch.float64, device=dev),
+        "n0_rel": torch.empty(B, kg, dtype=torch.float64, device=dev),
+        "n1_count": torch.empty(B, dtype=torch.int32, device=dev),
+        "n1_case": torch.empty(B, kg, dtype=torch.int32, device=dev),
+        "n1_pos": torch.empty(B, kg, dtype=torch.int32, device=dev),
+        "n1_flow": torch.empty(B, kg, dtype=torch.float64, device=dev),
+        "n1_rel": torch.empty(B, kg, dtype=torch.float64, device=dev),
+    }
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return eng.solve_device(t_spl, t_dis, t_inj, outs, stream.cuda_stream, max_rank)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    elapsed_ms = 0.0
+    lf_total = 0
+    stage = [0.0] * 8
+    launches = 0
+    waves = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        st, wv, nl, lf = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        elapsed_ms += e0.elapsed_time(e1)
+        lf_total += lf
+        stage = [a + b for a, b in zip(stage, st)]
+        launches += nl
+        waves = wv
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if ws > 1:
+        dist.barrier()
+        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        lt = torch.tensor([lf_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        elapsed_max, lf_all = float(tt.item()), float(lt.item())
+    else:
+        elapsed_max, lf_all = elapsed_ms, float(lf_total)
+    value = lf_all / (elapsed_max / 1e3)
+
+    # ---- e2e: host pinned inputs -> public session API -> host outputs, wall clock
+    pin_s = torch.from_numpy(splits).pin_memory().numpy()
+    pin_d = torch.from_numpy(discos).pin_memory().numpy()
+    pin_i = torch.from_numpy(inj).pin_memory().numpy()
+    solve_batch_output(sess, pin_s, pin_d, pin_i)  # warm
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e2e_s = 0.0
+    e2e_lf = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        out = solve_batch_output(sess, pin_s, pin_d, pin_i)
+        e2e_s += time.perf_counter() - t0
+        e2e_lf += out.loadflows
+    if ws > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        lt = torch.tensor([e2e_lf], dtype=torch.float64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        e2e_s, e2e_lf = float(tt.item()), float(lt.item())
+    e2e_val = e2e_lf / e2e_s
+    h2d = splits.nbytes + discos.nbytes + inj.nbytes
+    d2h = sum(getattr(out, n).nbytes for n in (
+        "metric", "best", "feasible", "status", "status_arg", "n_islanded", "islanded_bits",
+        "n0_count", "n0_pos", "n0_flow", "n0_rel", "n1_count", "n1_case", "n1_pos", "n1_flow", "n1_rel"))
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (k_single), live from the engine's CUDA events
+    tb = eng.tables
+    fe = out.feasible.astype(bool)
+    single_orders = set(int(x) for x in tb.sc_order)
+    isl_single = np.zeros(B, dtype=np.int64)
+    for b in np.flatnonzero(out.n_islanded > 0):
+        isl_single[b] = sum(1 for o in out.islanded_orders(int(b)) if o in single_orders)
+    pairs = float(((tb.N1 - isl_single) * fe).sum()) * T  # feasible (case, candidate) pairs per step
+    ops_per_launch_set = 2.0 * tb.M * pairs  # FFMA + FMNMX per monitored row
+    single_ms = stage[3] / args.steps
+    peaks, src = _peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_ops = 148 * 128 * sm_mhz * 1e6
+    achieved = ops_per_launch_set / (single_ms / 1e3)
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "k_single_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as fh:
+                tj = json.load(fh)
+            if tj.get("workload") == args.config:
+                traffic = tj.get("dram_bytes_per_task", 0) * B / max(1, waves)
+        except (OSError, ValueError):
+            traffic = None
+    step_ms = elapsed_max / args.steps
+    line = {
+        "metric": "DC loadflows/sec (topo x inj x N-1)",
+        "value": value,
+        "unit": "loadflows/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 N-1 scan / f64 updates + winner re-score",
+        "data": "synthetic (scaled make_fixtures recipe, random_tasks semantics, seeded per rank)",
+        "config": {
+            "workload": DESCR[args.config],
+            "grid": spec,
+            "tasks_per_gpu": int(B),
+            "candidates": T,
+            "splits": k,
+            "disconnections": d,
+            "rows": tb.R,
+            "monitored": tb.M,
+            "cases": len(grid.contingencies),
+            "parallelism": f"topology-sharded dp{ws} (no collective in the solve)",
+            "l2": "flushed between steps (256 MB write, outside the timed events)",
+        },
+        "e2e": {"value": e2e_val, "unit": "loadflows/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "how": "session API solve_batch_output, pinned host arrays in, host arrays out, wall clock, max over ranks"},
+        "roofline": {
+            "kernel": "k_single (fused single-branch N-1 screen)",
+            "bound": "alu",
+            "achieved": achieved / 1e9,
+            "peak": peak_ops / 1e9,
+            "unit": "Gop/s",
+            "frac": achieved / peak_ops,
+            "traffic": traffic,
+            "ops_definition": "2 lane-ops (FFMA + FMNMX) per monitored row per feasible (task, candidate, single case)",
+            "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz {sm_mhz:.0f} ({src} MEASURED_PEAKS.json)",
+            "kernel_ms_per_step": single_ms,
+        },
+        "stage_ms_per_step": {
+            n: v / args.steps for n, v in zip(["h2d", "update", "n0", "single_n1", "other_n1", "select", "report", "d2h"], stage)
+        },
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "loadflows_per_step": lf_all / args.steps,
+        "feasible_tasks": int(fe.sum()),
+    }
+    if ws == 1 and not args.no_cpu:
+        try:
+            cb = cpu_port_rate(args.config, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the baseline is reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": "loadflows/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="g118", choices=sorted(WORKLOADS))
+    ap.add_argument("--tasks", type=int, default=0, help="override tasks per GPU per step")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

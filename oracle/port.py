@@ -670,3 +670,32 @@ def decode_arrays(grid: Grid, splits, discos, inj):
 
 def solve_arrays(grid: Grid, base, splits, discos, inj, cfg) -> list[PortResult]:
     return [solve_one(grid, base, c, cfg) for c in decode_arrays(grid, splits, discos, inj)]
+
+
+def evaluate(grid: Grid, base, canon: Canon, cfg, winner: Optional[int] = None):
+    """Brute-force per-candidate metrics (every feasible case, like `symmetric`,
+    solver.py:826-842) and the winner report of candidate ``winner`` (default:
+    first argmin).  Returns None for infeasible tasks, else
+    (metrics (T,), winner, n0_worst, n1_worst, islanded)."""
+    st = _State.of(base)
+    try:
+        for si, bits in canon.splits:
+            st = _split(st, grid, si, bits)
+    except _SplitFail:
+        return None
+    ctx = _branch(grid, st, canon.discos, cfg)
+    if not ctx.feasible:
+        return None
+    rows = canon.rows
+    n0 = _n0_block(ctx, rows)
+    ccols = _inj_cols(ctx, rows)
+    metrics = _rel_max(ctx, n0)
+    for ce in ctx.cases:
+        if ce.feasible:
+            fl = _case_flows(ctx, ce, n0, ccols.get(ce.order), slice(None))
+            np.maximum(metrics, _rel_max(ctx, fl), out=metrics)
+    if ctx.islanded:
+        np.maximum(metrics, cfg.islanding_penalty, out=metrics)
+    w = int(np.argmin(metrics)) if winner is None else int(winner)
+    n0e, n1e = _report_winner(grid, ctx, cfg, n0, ccols, w)
+    return metrics, w, n0e, n1e, tuple(sorted(ctx.islanded))

@@ -1,0 +1,57 @@
+"""Build libbdc.so in-tree for sm_100a (nvcc; no JIT cache, so it travels with the repo)."""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SOURCES = ["bdc_update.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_capi.cu"]
+TARGET = os.path.join(HERE, "libbdc.so")
+FLAGS = [
+    "-std=c++17",
+    "-O3",
+    "-lineinfo",
+    "-gencode",
+    "arch=compute_100a,code=sm_100a",
+    "-shared",
+    "-Xcompiler",
+    "-fPIC",
+    "-Xcompiler",
+    "-O3",
+]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def stale() -> bool:
+    if not os.path.exists(TARGET):
+        return True
+    t = os.path.getmtime(TARGET)
+    deps = [os.path.join(HERE, "csrc", s) for s in SOURCES + ["bdc_device.cuh"]]
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "bdc.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return TARGET
+    srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES]
+    tmp = TARGET + ".tmp"
+    cmd = [nvcc()] + FLAGS + ["-o", tmp] + srcs
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, TARGET)
+    return TARGET
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

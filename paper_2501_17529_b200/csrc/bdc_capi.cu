@@ -1,0 +1,444 @@
+// bdc_capi.cu -- the C ABI (include/bdc.h): session lifetime, wave scheduling,
+// host<->device staging.  No exceptions cross the boundary; every entry point
+// returns a status and leaves a thread-local message for bdc_last_error().
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bdc_device.cuh"
+
+using namespace bdc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(BDC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class T>
+cudaError_t upload(const T* src, size_t n, const T** dst, std::vector<void*>& owned) {
+  *dst = nullptr;
+  if (n == 0) return cudaSuccess;
+  T* p = nullptr;
+  cudaError_t e = cudaMalloc((void**)&p, n * sizeof(T));
+  if (e != cudaSuccess) return e;
+  owned.push_back(p);
+  *dst = p;
+  if (src) return cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice);
+  return cudaMemset(p, 0, n * sizeof(T));
+}
+
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct BdcSession {
+  int device = 0;
+  DevGrid g{};
+  DevCfg cfg{};
+  std::vector<void*> owned;
+  int64_t wave_cap = 0;
+};
+
+extern "C" {
+
+const char* bdc_version(void) { return "bdc-b200 0.1.0 (sm_100a)"; }
+
+const char* bdc_last_error(void) { return g_err.c_str(); }
+
+int bdc_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(BDC_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *count = n;
+  return BDC_OK;
+}
+
+int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSession** out) {
+  if (!G || !C || !out) return fail(BDC_EINVAL, "null argument");
+  *out = nullptr;
+  if (G->E > EMAX) return fail(BDC_ELIMIT, "substation has more than 32 branch elements");
+  if (C->topk_per_case < 1 || C->topk_global < 1)
+    return fail(BDC_EINVAL, "top-k limits must be >= 1");
+  if (C->topk_per_case > KMAX || C->topk_global > KMAX)
+    return fail(BDC_ELIMIT, "top-k limits above 32 are not supported by the engine");
+  for (int q = 0; q < G->NM; ++q)
+    if (G->mc_start[q + 1] - G->mc_start[q] > MMAX)
+      return fail(BDC_ELIMIT, "multi-branch contingency with more than 8 branches");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(BDC_EINVAL, "device index out of range");
+  CK(cudaSetDevice(device));
+  auto* s = new BdcSession();
+  s->device = device;
+  DevGrid& g = s->g;
+  g.R = G->R; g.C0 = G->C0; g.M = G->M; g.S = G->S; g.E = G->E; g.K = G->K;
+  g.N1 = G->N1; g.NM = G->NM; g.NMB = G->NMB; g.NI = G->NI; g.NC = G->NC; g.NBR = G->NBR;
+  g.static_col = G->static_col;
+  std::vector<double> inv(G->M);
+  for (int i = 0; i < G->M; ++i) inv[i] = 1.0 / G->rating[i];
+  cudaError_t e = cudaSuccess;
+  auto& o = s->owned;
+#define UP(field, n) if (e == cudaSuccess) e = upload(G->field, (size_t)(n), &g.field, o)
+  UP(P0, (size_t)G->R * G->C0);
+  UP(P0T, (size_t)G->R * G->C0);
+  UP(row_from, G->R);
+  UP(row_to, G->R);
+  UP(branch_row, G->NBR);
+  UP(f0, G->R);
+  UP(p_base, G->C0);
+  UP(mon_row, G->M);
+  UP(rating, G->M);
+  UP(row_mon_pos, G->R);
+  UP(sub_col, G->S);
+  UP(sub_count, G->S);
+  UP(sub_elem_row, (size_t)G->S * G->E);
+  UP(sub_elem_b, (size_t)G->S * G->E);
+  UP(slot_sub, G->K);
+  UP(slot_col, G->K);
+  UP(slot_sp, G->K);
+  UP(sc_row, G->N1);
+  UP(sc_order, G->N1);
+  UP(sc_delta, G->N1);
+  UP(D64, (size_t)G->N1 * G->R);
+  UP(D32, (size_t)G->N1 * G->M);
+  UP(mc_start, G->NM + 1);
+  UP(mc_order, G->NM);
+  UP(mb_row, G->NMB);
+  UP(Dm64, (size_t)G->NMB * G->R);
+  UP(ic_slot, G->NI);
+  UP(ic_col, G->NI);
+  UP(ic_sp, G->NI);
+  UP(ic_order, G->NI);
+#undef UP
+  if (e == cudaSuccess) e = upload((const double*)inv.data(), inv.size(), &g.inv_rating, o);
+  if (e != cudaSuccess) {
+    for (void* p : o) cudaFree(p);
+    delete s;
+    return fail(BDC_ECUDA, std::string("session upload: ") + cudaGetErrorString(e));
+  }
+  s->cfg.kc = C->topk_per_case;
+  s->cfg.kg = C->topk_global;
+  s->cfg.policy = C->islanding_policy;
+  s->cfg.method = C->multi_outage_method;
+  s->cfg.maxout = C->max_simultaneous_outages;
+  s->cfg.penalty = C->islanding_penalty;
+  // keep freed workspace in the stream-ordered pool between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = s;
+  return BDC_OK;
+}
+
+int bdc_session_destroy(BdcSession* s) {
+  if (!s) return BDC_OK;
+  cudaSetDevice(s->device);
+  for (void* p : s->owned) cudaFree(p);
+  delete s;
+  return BDC_OK;
+}
+
+int bdc_session_set_wave(BdcSession* s, int64_t cap) {
+  if (!s) return fail(BDC_EINVAL, "null session");
+  s->wave_cap = cap;
+  return BDC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Layout {
+  size_t off[64];
+  int n = 0;
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    size_t o = total;
+    off[n++] = o;
+    total += al(bytes);
+    return o;
+  }
+};
+
+// Carve one allocation into the wave workspace; returns bytes needed.
+size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base, Work* w) {
+  Layout L;
+  const size_t B = Wb;
+  const int Cs = g.C0 + rs;
+  const int NCw = (g.NC + 31) / 32 > 0 ? (g.NC + 31) / 32 : 1;
+  size_t o_spl = L.add(B * g.S * Ein), o_dis = L.add(B * (D > 0 ? D : 1) * 8), o_inj = L.add(B * T * (g.K > 0 ? g.K : 1));
+  size_t o_tc = L.add(B * 4);
+  size_t o_st = L.add(B * 4), o_sa = L.add(B * 4), o_rk = L.add(B * 4), o_ns = L.add(B * 4), o_nd = L.add(B * 4);
+  size_t o_dead = L.add(B * RMAX * 4), o_ss = L.add(B * RMAX * 4), o_ni = L.add(B * 4), o_isl = L.add(B * NCw * 4);
+  size_t o_B = L.add(B * rs * g.R * 8), o_C = L.add(B * rs * Cs * 8);
+  size_t o_W = L.add(B * g.N1 * rs * 8), o_den = L.add(B * g.N1 * 8), o_ok = L.add(B * g.N1);
+  size_t o_Wm = L.add(B * g.NMB * rs * 8), o_mi = L.add(B * g.NM * MMAX * MMAX * 8), o_mo = L.add(B * g.NM);
+  size_t o_ca = L.add(B * g.NI * rs * 8), o_cb = L.add(B * g.NI * rs * 8);
+  size_t o_Y = L.add(B * rs * T * 8), o_n0 = L.add(B * g.R * T * 8), o_n0s = L.add(B * g.M * T * 4);
+  size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
+  size_t o_met = L.add(B * 8), o_best = L.add(B * 8), o_fe = L.add(B);
+  size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
+  size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
+  size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
+  size_t o_lf = L.add(16), o_bs = L.add(16);
+  if (!base) return L.total;
+  Work& x = *w;
+  x.Wb = Wb; x.T = T; x.D = D; x.Ein = Ein; x.rs = rs; x.Cs = Cs; x.NCw = NCw;
+  x.splits = (const uint8_t*)(base + o_spl);
+  x.discos = (const int64_t*)(base + o_dis);
+  x.inj = (const uint8_t*)(base + o_inj);
+  x.tcount = (const int*)(base + o_tc);
+  x.status = (int*)(base + o_st); x.sarg = (int*)(base + o_sa); x.rank = (int*)(base + o_rk);
+  x.nsplit = (int*)(base + o_ns); x.ndead = (int*)(base + o_nd); x.dead = (int*)(base + o_dead);
+  x.splitsub = (int*)(base + o_ss); x.nisl = (int*)(base + o_ni); x.isl = (uint32_t*)(base + o_isl);
+  x.Bm = (double*)(base + o_B); x.Cm = (double*)(base + o_C);
+  x.Wsc = (double*)(base + o_W); x.den = (double*)(base + o_den); x.sc_ok = (uint8_t*)(base + o_ok);
+  x.Wm = (double*)(base + o_Wm); x.minv = (double*)(base + o_mi); x.mc_ok = (uint8_t*)(base + o_mo);
+  x.cia = (double*)(base + o_ca); x.cib = (double*)(base + o_cb);
+  x.Y = (double*)(base + o_Y); x.n0 = (double*)(base + o_n0); x.n0s = (float*)(base + o_n0s);
+  x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b);
+  x.metric = (double*)(base + o_met); x.best = (int64_t*)(base + o_best); x.feasible = (uint8_t*)(base + o_fe);
+  x.n0cnt = (int*)(base + o_n0c); x.n0pos = (int*)(base + o_n0p); x.n0flow = (double*)(base + o_n0f);
+  x.n0rel = (double*)(base + o_n0r);
+  x.n1cnt = (int*)(base + o_n1c); x.n1case = (int*)(base + o_n1k); x.n1pos = (int*)(base + o_n1p);
+  x.n1flow = (double*)(base + o_n1f); x.n1rel = (double*)(base + o_n1r);
+  x.lf = (unsigned long long*)(base + o_lf); x.bsdf = (unsigned long long*)(base + o_bs);
+  return L.total;
+}
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  bool own = false;
+  ~StreamGuard() {
+    if (own && s) cudaStreamDestroy(s);
+  }
+};
+
+// Device-to-host (or device-to-device) copy of a wave's slice of one output.
+template <class T>
+cudaError_t out_copy(T* dst, const T* src, size_t n, int64_t off, bool on_dev, cudaStream_t st) {
+  if (!dst || n == 0) return cudaSuccess;
+  return cudaMemcpyAsync(dst + off, src, n * sizeof(T),
+                         on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
+}
+
+}  // namespace
+
+extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
+  if (!s || !bt) return fail(BDC_EINVAL, "null argument");
+  const DevGrid& g = s->g;
+  const int64_t B = bt->B;
+  const int T = bt->T, D = bt->D, Ein = g.E > 0 ? g.E : 1;
+  for (int i = 0; i < 8; ++i) bt->stage_ms[i] = 0.f;
+  bt->waves = 0;
+  bt->kernel_launches = 0;
+  if (B < 0 || T < 1 || D < 0) return fail(BDC_EINVAL, "bad batch dimensions");
+  if (B == 0) {
+    if (bt->loadflows) *bt->loadflows = 0;
+    return BDC_OK;
+  }
+  if (!bt->splits || !bt->inj || (D > 0 && !bt->discos) || !bt->metric || !bt->best ||
+      !bt->feasible || !bt->status)
+    return fail(BDC_EINVAL, "missing required input or output pointer");
+  if (T > 65535 * 128) return fail(BDC_ELIMIT, "too many candidates per task");
+  const int rs = bt->max_rank > 0 ? (bt->max_rank < RMAX ? bt->max_rank : RMAX) : RMAX;
+  CK(cudaSetDevice(s->device));
+  StreamGuard sg;
+  if (bt->stream) {
+    sg.s = (cudaStream_t)bt->stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    sg.own = true;
+  }
+  cudaStream_t st = sg.s;
+
+  // wave size: bounded by a workspace budget, the grid-z limit and the user cap
+  size_t per = carve(g, 1, T, D, Ein, rs, nullptr, nullptr);
+  size_t freeb = 0, totb = 0;
+  CK(cudaMemGetInfo(&freeb, &totb));
+  size_t budget = std::min<size_t>(freeb / 3, (size_t)16 << 30);
+  int64_t Wb = (int64_t)(budget / per);
+  if (Wb < 1) return fail(BDC_ELIMIT, "one task does not fit in device memory");
+  Wb = std::min<int64_t>(Wb, 32768);
+  if (s->wave_cap > 0) Wb = std::min<int64_t>(Wb, s->wave_cap);
+  Wb = std::min<int64_t>(Wb, B);
+  Work w{};
+  size_t bytes = carve(g, (int)Wb, T, D, Ein, rs, nullptr, nullptr);
+  char* ws = nullptr;
+  CK(cudaMallocAsync((void**)&ws, bytes, st));
+  carve(g, (int)Wb, T, D, Ein, rs, ws, &w);
+  CK(cudaMemsetAsync(w.lf, 0, 32, st));
+
+  const int nwaves = (int)((B + Wb - 1) / Wb);
+  std::vector<cudaEvent_t> ev((size_t)nwaves * 9);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  const bool ondev_in = bt->inputs_on_device != 0, ondev_out = bt->outputs_on_device != 0;
+  const int kg = s->cfg.kg, NCw = w.NCw;
+  int launches = 0;
+  cudaError_t err = cudaSuccess;
+  for (int wv = 0; wv < nwaves && err == cudaSuccess; ++wv) {
+    const int64_t b0 = (int64_t)wv * Wb;
+    const int nb = (int)std::min<int64_t>(Wb, B - b0);
+    Work x = w;
+    x.Wb = nb;
+    cudaEvent_t* E = &ev[(size_t)wv * 9];
+    cudaEventRecord(E[0], st);
+    const cudaMemcpyKind hk = ondev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const size_t sz_spl = (size_t)g.S * Ein, sz_inj = (size_t)T * g.K;
+    if (sz_spl) err = cudaMemcpyAsync((void*)x.splits, bt->splits + b0 * sz_spl, nb * sz_spl, hk, st);
+    if (err == cudaSuccess && D > 0)
+      err = cudaMemcpyAsync((void*)x.discos, bt->discos + b0 * D, (size_t)nb * D * 8, hk, st);
+    if (err == cudaSuccess && sz_inj)
+      err = cudaMemcpyAsync((void*)x.inj, bt->inj + b0 * sz_inj, nb * sz_inj, hk, st);
+    if (err == cudaSuccess && bt->t_count)
+      err = cudaMemcpyAsync((void*)x.tcount, bt->t_count + b0, (size_t)nb * 4, hk, st);
+    if (!bt->t_count) x.tcount = nullptr;
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
+    if (err != cudaSuccess) break;
+    cudaEventRecord(E[1], st);
+    launch_update(g, s->cfg, x, st);
+    cudaEventRecord(E[2], st);
+    launch_n0(g, x, st);
+    cudaEventRecord(E[3], st);
+    launch_single(g, x, st);
+    cudaEventRecord(E[4], st);
+    launch_other(g, x, st);
+    cudaEventRecord(E[5], st);
+    launch_select(g, s->cfg, x, st);
+    cudaEventRecord(E[6], st);
+    launch_report(g, s->cfg, x, st);
+    cudaEventRecord(E[7], st);
+    launches += kernels_per_wave(g);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) break;
+    // outputs
+    cudaError_t e2 = cudaSuccess;
+    auto chk = [&](cudaError_t e) { if (e2 == cudaSuccess) e2 = e; };
+    chk(out_copy(bt->metric, x.metric, nb, b0, ondev_out, st));
+    chk(out_copy(bt->best, x.best, nb, b0, ondev_out, st));
+    chk(out_copy(bt->feasible, x.feasible, nb, b0, ondev_out, st));
+    chk(out_copy(bt->status, x.status, nb, b0, ondev_out, st));
+    chk(out_copy(bt->status_arg, x.sarg, nb, b0, ondev_out, st));
+    chk(out_copy(bt->n_islanded, x.nisl, nb, b0, ondev_out, st));
+    chk(out_copy(bt->islanded_bits, x.isl, (size_t)nb * NCw, b0 * NCw, ondev_out, st));
+    chk(out_copy(bt->n0_count, x.n0cnt, nb, b0, ondev_out, st));
+    chk(out_copy(bt->n1_count, x.n1cnt, nb, b0, ondev_out, st));
+    // report entries are stored with stride KMAX on device; copy with the user's stride kg
+    auto strided = [&](auto* dst, const auto* src, size_t elem) {
+      if (!dst) return;
+      chk(cudaMemcpy2DAsync(dst + b0 * kg, kg * elem, src, (size_t)kg * elem, (size_t)kg * elem, nb,
+                            ondev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    };
+    strided(bt->n0_pos, x.n0pos, 4);
+    strided(bt->n0_flow, x.n0flow, 8);
+    strided(bt->n0_rel, x.n0rel, 8);
+    strided(bt->n1_case, x.n1case, 4);
+    strided(bt->n1_pos, x.n1pos, 4);
+    strided(bt->n1_flow, x.n1flow, 8);
+    strided(bt->n1_rel, x.n1rel, 8);
+    if (bt->cand_metric)
+      chk(cudaMemcpyAsync(bt->cand_metric + b0 * T, x.m32, (size_t)nb * T * 4,
+                          ondev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    cudaEventRecord(E[8], st);
+    err = e2;
+  }
+  unsigned long long counters[2] = {0, 0};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 16, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(ws, st);
+  cudaError_t es = cudaStreamSynchronize(st);
+  if (err == cudaSuccess) err = es;
+  if (err == cudaSuccess) {
+    for (int wv = 0; wv < nwaves; ++wv) {
+      cudaEvent_t* E = &ev[(size_t)wv * 9];
+      for (int k = 0; k < 8; ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, E[k], E[k + 1]) == cudaSuccess) {
+          // stage_ms: 0 h2d, 1 update, 2 n0, 3 single N-1, 4 other N-1, 5 select, 6 report, 7 d2h
+          bt->stage_ms[k] += ms;
+        }
+      }
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (err != cudaSuccess) return fail(BDC_ECUDA, std::string("bdc_solve: ") + cudaGetErrorString(err));
+  if (bt->loadflows) *bt->loadflows = (int64_t)counters[0];
+  if (bt->bsdf_applications) *bt->bsdf_applications = (int64_t)counters[1];
+  bt->waves = nwaves;
+  bt->kernel_launches = launches;
+  return BDC_OK;
+}
+
+extern "C" int bdc_probe_flows(BdcSession* s, const uint8_t* splits, const int64_t* discos,
+                               int32_t D, const uint8_t* inj, int32_t T, double* n0, double* n1,
+                               uint8_t* case_ok, int32_t* status, int32_t* status_arg) {
+  if (!s || !splits || !inj || !n0 || !n1 || !case_ok || !status || T < 1)
+    return fail(BDC_EINVAL, "bad probe arguments");
+  const DevGrid& g = s->g;
+  const int Ein = g.E > 0 ? g.E : 1;
+  CK(cudaSetDevice(s->device));
+  StreamGuard sg;
+  CK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  sg.own = true;
+  cudaStream_t st = sg.s;
+  Work w{};
+  size_t bytes = carve(g, 1, T, D, Ein, RMAX, nullptr, nullptr);
+  char* ws = nullptr;
+  double *dn0 = nullptr, *dn1 = nullptr;
+  uint8_t* dok = nullptr;
+  const size_t n1n = (size_t)g.NC * g.R * T;
+  CK(cudaMalloc(&ws, bytes));
+  carve(g, 1, T, D, Ein, RMAX, ws, &w);
+  w.tcount = nullptr;
+  cudaError_t e = cudaMalloc(&dn0, (size_t)g.R * T * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dn1, n1n * 8 + 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dok, g.NC + 1);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.lf, 0, 32, st);
+  if (e == cudaSuccess && g.S) e = cudaMemcpyAsync((void*)w.splits, splits, (size_t)g.S * Ein, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && D) e = cudaMemcpyAsync((void*)w.discos, discos, (size_t)D * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && g.K) e = cudaMemcpyAsync((void*)w.inj, inj, (size_t)T * g.K, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.m32, 0, (size_t)T * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dok, 0, g.NC + 1, st);
+  int hs[2] = {0, 0};
+  if (e == cudaSuccess) {
+    launch_update(g, s->cfg, w, st);
+    e = cudaMemcpyAsync(hs, w.status, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs + 1, w.sarg, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  if (e == cudaSuccess && hs[0] == 0) {
+    launch_n0(g, w, st);
+    launch_probe(g, w, dn0, dn1, dok, st);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(n0, dn0, (size_t)g.R * T * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && n1n) e = cudaMemcpyAsync(n1, dn1, n1n * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && g.NC) e = cudaMemcpyAsync(case_ok, dok, g.NC, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  cudaFree(ws);
+  cudaFree(dn0);
+  cudaFree(dn1);
+  cudaFree(dok);
+  if (e != cudaSuccess) return fail(BDC_ECUDA, std::string("bdc_probe_flows: ") + cudaGetErrorString(e));
+  *status = hs[0];
+  if (status_arg) *status_arg = hs[1];
+  return BDC_OK;
+}

@@ -1,0 +1,171 @@
+// bdc_device.cuh -- device-side data structures and small helpers shared by
+// the engine's kernels.  See DESIGN.md for the data layout in HBM.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/bdc.h"
+
+namespace bdc {
+
+constexpr int RMAX = BDC_MAX_RANK;        // rank k+d per task
+constexpr int EMAX = BDC_MAX_ELEMENTS;    // branch elements per substation
+constexpr int MMAX = BDC_MAX_MULTI;       // branches per multi-branch case
+constexpr int KMAX = BDC_MAX_TOPK;        // top-k limits
+constexpr int ACTMAX = 64;                // active slots (slots at split substations) per task
+constexpr int RHMAX = RMAX * EMAX;        // re-homed branch ends per task
+constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors.py:48-49)
+
+// Grid tables, device-resident for the session lifetime.
+struct DevGrid {
+  int R, C0, M, S, E, K, N1, NM, NMB, NI, NC, NBR, static_col;
+  const double *P0, *P0T, *f0, *p_base, *rating, *inv_rating, *sub_elem_b, *slot_sp;
+  const double *sc_delta, *D64, *Dm64, *ic_sp;
+  const float* D32;
+  const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;
+  const int *sub_elem_row, *slot_sub, *slot_col, *sc_row, *sc_order, *mc_start, *mc_order;
+  const int *mb_row, *ic_slot, *ic_col, *ic_order;
+};
+
+struct DevCfg {
+  int kc, kg, policy, method, maxout;
+  double penalty;
+};
+
+// One wave of tasks: inputs, per-task factor workspace, outputs.
+struct Work {
+  int Wb;         // tasks in the wave
+  int T, D, Ein;  // candidates, disconnection columns, split-array width
+  int rs;         // rank stride (max k+d in the batch, >= 1)
+  int Cs;         // column stride of the coupler rows = C0 + rs
+  int NCw;        // 32-bit words of the islanded bitmap
+  // inputs (device)
+  const uint8_t* splits;   // (Wb, S, Ein)
+  const int64_t* discos;   // (Wb, D)
+  const uint8_t* inj;      // (Wb, T, K)
+  const int* tcount;       // (Wb) or null
+  // per-task scalars
+  int* status; int* sarg; int* rank; int* nsplit; int* ndead; int* dead;  // dead: (Wb, RMAX)
+  int* splitsub;  // (Wb, RMAX) substation of split j
+  int* nisl;      // (Wb)
+  uint32_t* isl;  // (Wb, NCw)
+  // factors (FP64)
+  double* Bm;     // (Wb, rs, R)   column j of B'' contiguous over rows
+  double* Cm;     // (Wb, rs, Cs)  coupler / outage row j over logical columns
+  double* Wsc;    // (Wb, N1, rs)  W(c, j) = C[j][f'_c] - C[j][t'_c]
+  double* den;    // (Wb, N1)      1 - D''(r_c, c)
+  uint8_t* sc_ok; // (Wb, N1)
+  double* Wm;     // (Wb, NMB, rs)
+  double* minv;   // (Wb, NM, MMAX*MMAX) inverse of the m x m inner system
+  uint8_t* mc_ok; // (Wb, NM)
+  double* cia; double* cib;  // (Wb, NI, rs) coupler coefficients of the injection column
+  double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
+  double* n0;     // (Wb, R, T)    N-0 flows, FP64, dead rows exactly 0
+  float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
+  uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
+  double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
+  // outputs (device)
+  double* metric; int64_t* best; uint8_t* feasible;
+  int* n0cnt; int* n0pos; double* n0flow; double* n0rel;
+  int* n1cnt; int* n1case; int* n1pos; double* n1flow; double* n1rel;
+  unsigned long long* lf;     // loadflow counter
+  unsigned long long* bsdf;   // split applications counter
+};
+
+__device__ __forceinline__ bool is_dead(const int* dead, int nd, int row) {
+  for (int i = 0; i < nd; ++i)
+    if (dead[i] == row) return true;
+  return false;
+}
+
+__device__ __forceinline__ void atomic_max_pos(uint32_t* addr, float v) {
+  // v >= 0: IEEE order of non-negative floats equals unsigned order of their bits
+  atomicMax(addr, __float_as_uint(v));
+}
+
+// One-sided Jacobi SVD (Hestenes) of an n x n matrix (row-major, n <= MMAX):
+// returns the largest and smallest singular values.  Accurate to eps*sigma_max,
+// which the islanding test sigma_min < 1e-8 max(1, sigma_max) needs
+// (factors.py:398-399); an eigen-decomposition of A^T A would square the
+// condition number and blur exactly that threshold.
+__device__ inline void svd_minmax(const double* A, int n, double& smax, double& smin) {
+  double U[MMAX * MMAX];
+  for (int i = 0; i < n * n; ++i) U[i] = A[i];
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        double al = 0, be = 0, ga = 0;
+        for (int i = 0; i < n; ++i) {
+          double x = U[i * n + p], y = U[i * n + q];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        if (ga == 0.0 || fabs(ga) <= 1e-17 * sqrt(al * be)) continue;
+        rotated = true;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int i = 0; i < n; ++i) {
+          double x = U[i * n + p], y = U[i * n + q];
+          U[i * n + p] = c * x - s * y;
+          U[i * n + q] = s * x + c * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  smax = 0.0; smin = 1e300;
+  for (int j = 0; j < n; ++j) {
+    double nrm = 0;
+    for (int i = 0; i < n; ++i) nrm += U[i * n + j] * U[i * n + j];
+    nrm = sqrt(nrm);
+    smax = fmax(smax, nrm);
+    smin = fmin(smin, nrm);
+  }
+}
+
+// Gauss-Jordan inverse with partial pivoting (n <= MMAX).  Returns false if a
+// pivot vanishes (callers only invert systems that passed svd_minmax).
+__device__ inline bool invert_small(const double* A, int n, double* Ainv) {
+  double M[MMAX * 2 * MMAX];
+  const int w = 2 * n;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      M[i * w + j] = A[i * n + j];
+      M[i * w + n + j] = (i == j) ? 1.0 : 0.0;
+    }
+  for (int c = 0; c < n; ++c) {
+    int p = c;
+    for (int i = c + 1; i < n; ++i)
+      if (fabs(M[i * w + c]) > fabs(M[p * w + c])) p = i;
+    if (M[p * w + c] == 0.0) return false;
+    if (p != c)
+      for (int j = 0; j < w; ++j) {
+        double t = M[c * w + j]; M[c * w + j] = M[p * w + j]; M[p * w + j] = t;
+      }
+    double inv = 1.0 / M[c * w + c];
+    for (int j = 0; j < w; ++j) M[c * w + j] *= inv;
+    for (int i = 0; i < n; ++i) {
+      if (i == c) continue;
+      double f = M[i * w + c];
+      if (f != 0.0)
+        for (int j = 0; j < w; ++j) M[i * w + j] -= f * M[c * w + j];
+    }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) Ainv[i * n + j] = M[i * w + n + j];
+  return true;
+}
+
+// Kernel launchers (bdc_kernels.cu).
+void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_single(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
+                  cudaStream_t s);
+int kernels_per_wave(const DevGrid& g);
+
+}  // namespace bdc

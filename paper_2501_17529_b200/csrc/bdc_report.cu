@@ -1,0 +1,383 @@
+// bdc_report.cu -- Kernel 5: the winner's sparse report and FP64 metric, and the
+// flow probe used by the parity tests.
+//
+// k_report re-evaluates the winning candidate only, in FP64 (metric_first's
+// second pass, PAPER step "recompute p_n0/p_n1 for t_i^*", solver.py:652-713):
+//   * the FP64 metric max(N-0, every feasible case, penalty)   (agg_m, solver.py:235-252)
+//   * N-0 top-kg over reportable monitored rows               (_top_rows, :287-299)
+//   * per case stable top-kc, merged by (-rel, case, position) (_merge_entries, :302-318)
+// One CTA per task; each warp owns a strided subset of the cases and keeps
+// its own top-kg list; a case entry below the warp's current kg-th loading
+// cannot reach the final report, so it is skipped (the same exact pruning the
+// reference's bound-stop implements, solver.py:686-695).
+#include "bdc_device.cuh"
+
+#include <climits>
+
+namespace bdc {
+
+namespace {
+
+constexpr int RT = 256;
+constexpr int RW = RT / 32;
+
+__device__ __forceinline__ bool better(double r1, int p1, double r2, int p2) {
+  return r1 > r2 || (r1 == r2 && p1 < p2);
+}
+__device__ __forceinline__ bool better3(double r1, int c1, int p1, double r2, int c2, int p2) {
+  return r1 > r2 || (r1 == r2 && (c1 < c2 || (c1 == c2 && p1 < p2)));
+}
+
+template <int KC>
+struct LaneTop {
+  double rel[KC], flow[KC];
+  int pos[KC];
+  __device__ void clear() {
+#pragma unroll
+    for (int i = 0; i < KC; ++i) { rel[i] = -1.0; flow[i] = 0.0; pos[i] = INT_MAX; }
+  }
+  __device__ void insert(double r, int p, double f) {
+    if (!better(r, p, rel[KC - 1], pos[KC - 1])) return;
+#pragma unroll
+    for (int i = KC - 1; i > 0; --i) {
+      if (better(r, p, rel[i - 1], pos[i - 1])) {
+        rel[i] = rel[i - 1]; pos[i] = pos[i - 1]; flow[i] = flow[i - 1];
+      } else {
+        rel[i] = r; pos[i] = p; flow[i] = f;
+        return;
+      }
+    }
+    rel[0] = r; pos[0] = p; flow[0] = f;
+  }
+  __device__ void pop() {
+#pragma unroll
+    for (int i = 0; i < KC - 1; ++i) { rel[i] = rel[i + 1]; pos[i] = pos[i + 1]; flow[i] = flow[i + 1]; }
+    rel[KC - 1] = -1.0; pos[KC - 1] = INT_MAX; flow[KC - 1] = 0.0;
+  }
+};
+
+struct WarpList {
+  double rel[KMAX], flow[KMAX];
+  int cs[KMAX], pos[KMAX];
+  int n;
+};
+
+// lane 0 only
+__device__ void wl_insert(WarpList& L, int kg, double r, int c, int p, double f) {
+  if (L.n == kg && !better3(r, c, p, L.rel[kg - 1], L.cs[kg - 1], L.pos[kg - 1])) return;
+  int i = L.n < kg ? L.n : kg - 1;
+  while (i > 0 && better3(r, c, p, L.rel[i - 1], L.cs[i - 1], L.pos[i - 1])) {
+    L.rel[i] = L.rel[i - 1]; L.cs[i] = L.cs[i - 1]; L.pos[i] = L.pos[i - 1]; L.flow[i] = L.flow[i - 1];
+    --i;
+  }
+  L.rel[i] = r; L.cs[i] = c; L.pos[i] = p; L.flow[i] = f;
+  if (L.n < kg) ++L.n;
+}
+
+// Merge each lane's list into the warp list: kc rounds of warp argmax.
+template <int KC>
+__device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int case_order) {
+  const int lane = threadIdx.x & 31;
+  for (int round = 0; round < kc; ++round) {
+    double r = lt.rel[0];
+    int p = lt.pos[0], src = lane;
+    for (int o = 16; o; o >>= 1) {
+      const double orr = __shfl_xor_sync(0xffffffffu, r, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      const int os = __shfl_xor_sync(0xffffffffu, src, o);
+      if (better(orr, op, r, p)) { r = orr; p = op; src = os; }
+    }
+    if (r < 0.0) break;  // every lane empty
+    const double f = __shfl_sync(0xffffffffu, lt.flow[0], src);
+    if (lane == src) lt.pop();
+    if (lane == 0) wl_insert(L, kg, r, case_order, p, f);
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ double warp_thresh(const WarpList& L, int kg) {
+  return L.n == kg ? L.rel[kg - 1] : -1.0;
+}
+
+}  // namespace
+
+template <int KC>
+__global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
+  const int b = blockIdx.x;
+  if (w.status[b] != 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = g.R, M = g.M, T = w.T, rs = w.rs, rt = w.rank[b];
+  const int best = (int)w.best[b];
+  const int kc = cfg.kc, kg = cfg.kg;
+  double* n0b = w.n0b + (size_t)b * R;
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  __shared__ WarpList wl[RW];
+  __shared__ int sdead[RMAX];
+  __shared__ double sred[RW];
+  __shared__ double sbr[RW];
+  __shared__ int sbp[RW];
+  __shared__ double sWc[RW][RMAX];
+  __shared__ double sMinv[RW][MMAX * MMAX];
+  __shared__ int sN0pos[KMAX];
+  const int nd = w.ndead[b];
+  for (int r = tid; r < R; r += RT) n0b[r] = w.n0[((size_t)b * R + r) * T + best];
+  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  if (lane == 0) wl[wid].n = 0;
+  __syncthreads();
+
+  double mymax = 0.0;
+  // ---- N-0 report: kg rounds of block argmax over reportable positions ----------------
+  {
+    double pr = 1e300;
+    int pp = -1;
+    int n0n = 0;
+    for (int round = 0; round < kg; ++round) {
+      double br = -1.0;
+      int bp = INT_MAX;
+      for (int p = tid; p < M; p += RT) {
+        const int row = g.mon_row[p];
+        const double f = n0b[row];
+        const double rel = fabs(f) / g.rating[p];
+        if (round == 0) mymax = fmax(mymax, rel);
+        if (is_dead(sdead, nd, row)) continue;
+        // next entry in (rel desc, pos asc) order after the previous pick
+        if (!(rel < pr || (rel == pr && p > pp))) continue;
+        if (better(rel, p, br, bp)) { br = rel; bp = p; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (better(orr, op, br, bp)) { br = orr; bp = op; }
+      }
+      if (lane == 0) { sbr[wid] = br; sbp[wid] = bp; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int i = 1; i < RW; ++i)
+          if (better(sbr[i], sbp[i], sbr[0], sbp[0])) { sbr[0] = sbr[i]; sbp[0] = sbp[i]; }
+      }
+      __syncthreads();
+      br = sbr[0]; bp = sbp[0];
+      __syncthreads();
+      if (br < 0.0) break;
+      if (tid == 0) sN0pos[round] = bp;
+      pr = br; pp = bp;
+      ++n0n;
+    }
+    if (tid == 0) {
+      w.n0cnt[b] = n0n;
+      for (int i = 0; i < n0n; ++i) {
+        const int p = sN0pos[i];
+        const double f = n0b[g.mon_row[p]];
+        w.n0pos[(size_t)b * kg + i] = p;
+        w.n0flow[(size_t)b * kg + i] = f;
+        w.n0rel[(size_t)b * kg + i] = fabs(f) / g.rating[p];
+      }
+    }
+  }
+
+  // ---- every feasible contingency of the winner ------------------------------------------
+  LaneTop<KC> lt;
+  const int ncase = g.N1 + g.NM + g.NI;
+  for (int ci = wid; ci < ncase; ci += RW) {
+    int order, kind = 0, q = ci;
+    if (ci < g.N1) {
+      if (!w.sc_ok[(size_t)b * g.N1 + ci]) continue;
+      order = g.sc_order[ci];
+    } else if (ci < g.N1 + g.NM) {
+      kind = 1; q = ci - g.N1;
+      if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
+      order = g.mc_order[q];
+    } else {
+      kind = 2; q = ci - g.N1 - g.NM;
+      order = g.ic_order[q];
+    }
+    lt.clear();
+    const double thresh = warp_thresh(wl[wid], kg);
+    if (kind == 0) {
+      const int rowc = g.sc_row[q];
+      const double sc = n0b[rowc];
+      const double den = w.den[(size_t)b * g.N1 + q];
+      for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * g.N1 + q) * rs + j];
+      __syncwarp();
+      const double* Dc = g.D64 + (size_t)q * R;
+      for (int p = lane; p < M; p += 32) {
+        const int row = g.mon_row[p];
+        if (is_dead(sdead, nd, row)) continue;  // flow exactly 0: neither metric nor report
+        double f;
+        if (row == rowc) {
+          f = n0b[row] + (-1.0) * sc;
+        } else {
+          double dv = Dc[row];
+          for (int j = 0; j < rt; ++j) dv = fma(Bm[(size_t)j * R + row], sWc[wid][j], dv);
+          f = n0b[row] + (dv / den) * sc;
+        }
+        const double rel = fabs(f) / g.rating[p];
+        mymax = fmax(mymax, rel);
+        if (row != rowc && rel >= thresh) lt.insert(rel, p, f);
+      }
+    } else if (kind == 1) {
+      const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+      for (int i = lane; i < m * m; i += 32) sMinv[wid][i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
+      __syncwarp();
+      double sv[MMAX];
+      for (int j = 0; j < m; ++j) sv[j] = n0b[g.mb_row[st + j]];
+      for (int p = lane; p < M; p += 32) {
+        const int row = g.mon_row[p];
+        if (is_dead(sdead, nd, row)) continue;
+        int own = -1;
+        for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+        double f = n0b[row];
+        if (own >= 0) {
+          for (int j = 0; j < m; ++j) f += (j == own ? -1.0 : 0.0) * sv[j];
+        } else {
+          double Dv[MMAX];
+          for (int i = 0; i < m; ++i) {
+            double v = g.Dm64[(size_t)(st + i) * R + row];
+            const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+            for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+            Dv[i] = v;
+          }
+          for (int j = 0; j < m; ++j) {
+            double l = 0.0;
+            for (int i = 0; i < m; ++i) l += Dv[i] * sMinv[wid][i * m + j];
+            f += l * sv[j];
+          }
+        }
+        const double rel = fabs(f) / g.rating[p];
+        mymax = fmax(mymax, rel);
+        if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
+      }
+    } else {
+      const int sl = g.ic_slot[q];
+      const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
+      const bool bit = sl >= 0 && w.inj[((size_t)b * T + best) * g.K + sl];
+      const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * g.NI + q) * rs;
+      const double sp = g.ic_sp[q];
+      for (int p = lane; p < M; p += 32) {
+        const int row = g.mon_row[p];
+        if (is_dead(sdead, nd, row)) continue;
+        double pc = g.P0T[(size_t)ca * R + row];
+        for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
+        const double f = n0b[row] - pc * sp;
+        const double rel = fabs(f) / g.rating[p];
+        mymax = fmax(mymax, rel);
+        if (rel >= thresh) lt.insert(rel, p, f);
+      }
+    }
+    warp_merge<KC>(lt, kc, wl[wid], kg, order);
+    __syncwarp();
+  }
+
+  // ---- FP64 metric and final merge --------------------------------------------------------
+  for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  if (lane == 0) sred[wid] = mymax;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < RW; ++i) mx = fmax(mx, sred[i]);
+    if (w.nisl[b] > 0) mx = fmax(mx, cfg.penalty);
+    w.metric[b] = mx;
+    WarpList& F = wl[0];
+    for (int i = 1; i < RW; ++i)
+      for (int e = 0; e < wl[i].n; ++e)
+        wl_insert(F, kg, wl[i].rel[e], wl[i].cs[e], wl[i].pos[e], wl[i].flow[e]);
+    w.n1cnt[b] = F.n;
+    for (int e = 0; e < F.n; ++e) {
+      w.n1case[(size_t)b * kg + e] = F.cs[e];
+      w.n1pos[(size_t)b * kg + e] = F.pos[e];
+      w.n1flow[(size_t)b * kg + e] = F.flow[e];
+      w.n1rel[(size_t)b * kg + e] = F.rel[e];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ probe
+// Every flow of one task (b = 0) in FP64: n0 (R,T) and n1 (NC,R,T) in contingency
+// order, NaN for islanded cases (candidate_case_flows, solver.py:919-958).
+__global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok) {
+  const int ci = blockIdx.y;  // local case index over N1, NM, NI; ci == ncase -> N-0
+  const int ncase = g.N1 + g.NM + g.NI;
+  const int R = g.R, T = w.T, rs = w.rs, rt = w.rank[0];
+  const double* Bm = w.Bm;
+  const int nd = w.ndead[0];
+  const int* dead = w.dead;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)R * T;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / T), t = (int)(idx % T);
+    const double n0v = w.n0[(size_t)row * T + t];
+    if (ci == ncase) { n0o[idx] = n0v; continue; }
+    const bool drow = is_dead(dead, nd, row);
+    int order;
+    double f = nan;
+    if (ci < g.N1) {
+      order = g.sc_order[ci];
+      if (w.sc_ok[ci]) {
+        const int rowc = g.sc_row[ci];
+        const double sc = w.n0[(size_t)rowc * T + t];
+        if (drow) f = 0.0;
+        else if (row == rowc) f = n0v - sc;
+        else {
+          double dv = g.D64[(size_t)ci * R + row];
+          for (int j = 0; j < rt; ++j) dv = fma(Bm[(size_t)j * R + row], w.Wsc[(size_t)ci * rs + j], dv);
+          f = n0v + (dv / w.den[ci]) * sc;
+        }
+      }
+    } else if (ci < g.N1 + g.NM) {
+      const int q = ci - g.N1;
+      order = g.mc_order[q];
+      if (w.mc_ok[q]) {
+        const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+        if (drow) f = 0.0;
+        else {
+          int own = -1;
+          for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+          f = n0v;
+          for (int j = 0; j < m; ++j) {
+            double l = 0.0;
+            if (own >= 0) l = (j == own) ? -1.0 : 0.0;
+            else
+              for (int i = 0; i < m; ++i) {
+                double v = g.Dm64[(size_t)(st + i) * R + row];
+                for (int jj = 0; jj < rt; ++jj) v = fma(Bm[(size_t)jj * R + row], w.Wm[(size_t)(st + i) * rs + jj], v);
+                l += v * w.minv[(size_t)q * MMAX * MMAX + i * m + j];
+              }
+            f += l * w.n0[(size_t)g.mb_row[st + j] * T + t];
+          }
+        }
+      }
+    } else {
+      const int q = ci - g.N1 - g.NM;
+      order = g.ic_order[q];
+      const int sl = g.ic_slot[q];
+      const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
+      const bool bit = sl >= 0 && w.inj[(size_t)t * g.K + sl];
+      const double* coef = (bit ? w.cib : w.cia) + (size_t)q * rs;
+      double pc = g.P0T[(size_t)ca * R + row];
+      for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
+      f = drow ? 0.0 : n0v - pc * g.ic_sp[q];
+    }
+    n1o[((size_t)order * R + row) * T + t] = f;
+    if (idx == 0) ok[order] = (f == f);
+  }
+}
+
+void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  if (c.kc <= 5) k_report<5><<<w.Wb, RT, 0, s>>>(g, c, w);
+  else if (c.kc <= 8) k_report<8><<<w.Wb, RT, 0, s>>>(g, c, w);
+  else if (c.kc <= 16) k_report<16><<<w.Wb, RT, 0, s>>>(g, c, w);
+  else k_report<32><<<w.Wb, RT, 0, s>>>(g, c, w);
+}
+
+void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
+                  cudaStream_t s) {
+  const int ncase = g.N1 + g.NM + g.NI;
+  dim3 grid(64, ncase + 1);
+  k_probe<<<grid, 256, 0, s>>>(g, w, n0, n1, ok);
+}
+
+int kernels_per_wave(const DevGrid& g) {
+  return 4 + (g.N1 > 0) + (g.NM + g.NI > 0);
+}
+
+}  // namespace bdc

@@ -1,0 +1,512 @@
+// bdc_update.cu -- Kernel 1: the per-topology low-rank PTDF update.
+//
+// One CTA per task, FP64 throughout.  The updated PTDF of a task is never
+// materialised; it is carried as a rank-r correction of the shared base
+//     P''[row, col] = P0[row, base(col)] + sum_j B[j][row] * C[j][col]
+// (rows of disconnected branches forced to exactly 0), where the first k
+// terms are the sequential busbar-split chain and the next d terms the
+// disconnections.  Logical column ids: 0..C0-1 are the base columns, C0+j is
+// the new busbar column of split j (base(C0+j) = column of its substation).
+//
+// Follows, step for step:
+//   decode + canonical order      session.py:207-225, solver.py:148-197
+//   compute_bsdf / apply_bsdf     factors.py:428-585  (split chain, _apply_splits solver.py:363-378)
+//   compute_modf / apply_modf     factors.py:373-425  (disconnections, solver.py:389-406)
+//   lodf_column / apply_outage    factors.py:333-370  (multi_outage_method="sequential")
+//   single-outage LODF block      solver.py:474-503   (den, islanding, W factors)
+//   multi-branch cases            solver.py:448-454   (m x m inner system per case)
+//   injection cases / slots       solver.py:455-467, 555-572
+//   candidate injection vectors   solver.py:575-595   (y_t = C''^T p_t, so n0 = f0 + B'' y_t)
+#include "bdc_device.cuh"
+
+namespace bdc {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+
+struct UpdShared {
+  int sub[RMAX];
+  unsigned bits[RMAX];
+  int k, d, nd, fail, farg, nrh, nact;
+  int wcnt[NW];
+  int rh_key[RHMAX];   // row*2 + end
+  int rh_col[RHMAX];
+  int dead[RMAX];
+  int orow[RMAX];      // outage rows in task order
+  int ofc[RMAX], otc[RMAX];  // current endpoint columns of the outaged rows
+  // split step scratch
+  int a, nm, nst;
+  int mrow[EMAX], mend[EMAX];
+  double msign[EMAX];
+  int srow[EMAX], sfar[EMAX];
+  double ssign[EMAX], sw[EMAX];
+  double den;
+  double mB[EMAX][RMAX];     // B[i][moved row]
+  double sCfar[EMAX][RMAX];  // C[i][far of stay element]
+  double sCa[RMAX];          // C[i][a]
+  double inner[MMAX * MMAX];
+  double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
+  double oB[RMAX][RMAX];     // B[i'][outage row i]
+  double ybase[RMAX];
+  int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
+  double act_sp[ACTMAX];
+  int nisl;
+};
+
+__device__ __forceinline__ int base_col(const DevGrid& g, const UpdShared& s, int col) {
+  return col < g.C0 ? col : g.sub_col[s.sub[col - g.C0]];
+}
+
+__device__ __forceinline__ int curcol(const UpdShared& s, int row, int end, int dflt) {
+  int key = row * 2 + end, c = dflt;
+  for (int i = 0; i < s.nrh; ++i)
+    if (s.rh_key[i] == key) c = s.rh_col[i];
+  return c;
+}
+
+// Ordered block-wide compaction helper: returns this thread's slot among the
+// flagged threads of the current chunk and the chunk total (all threads).
+__device__ __forceinline__ int block_rank(bool flag, int* wcnt, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned bal = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) wcnt[wid] = __popc(bal);
+  __syncthreads();
+  int off = 0;
+  total = 0;
+  for (int i = 0; i < NW; ++i) {
+    if (i < wid) off += wcnt[i];
+    total += wcnt[i];
+  }
+  __syncthreads();
+  return off + __popc(bal & ((1u << lane) - 1u));
+}
+
+__device__ void set_island(const Work& w, int b, int order) {
+  atomicOr(&w.isl[(size_t)b * w.NCw + (order >> 5)], 1u << (order & 31));
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(NT) k_update(DevGrid g, DevCfg cfg, Work w) {
+  __shared__ UpdShared s;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int R = g.R, C0 = g.C0, rs = w.rs, Cs = w.Cs;
+  double* Bm = w.Bm + (size_t)b * rs * R;
+  double* Cm = w.Cm + (size_t)b * rs * Cs;
+
+  if (tid == 0) {
+    s.k = 0; s.d = 0; s.nd = 0; s.fail = 0; s.farg = 0; s.nrh = 0; s.nact = 0; s.nisl = 0;
+  }
+  for (int i = tid; i < w.NCw; i += NT) w.isl[(size_t)b * w.NCw + i] = 0u;
+  __syncthreads();
+
+  // ---- decode splits in canonical (ascending substation) order ----------------
+  const uint8_t* sp = w.splits + (size_t)b * g.S * w.Ein;
+  for (int c0 = 0; c0 < g.S; c0 += NT) {
+    int si = c0 + tid;
+    unsigned bits = 0;
+    if (si < g.S) {
+      int cnt = g.sub_count[si];
+      for (int e = 0; e < cnt; ++e)
+        if (sp[(size_t)si * w.Ein + e]) bits |= 1u << e;
+    }
+    int total;
+    int pos = block_rank(bits != 0, s.wcnt, total);
+    if (bits != 0) {
+      int p = s.k + pos;
+      if (p < RMAX) { s.sub[p] = si; s.bits[p] = bits; }
+    }
+    __syncthreads();
+    if (tid == 0) s.k += total;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int64_t* dr = w.discos + (size_t)b * w.D;
+    int d = 0;
+    for (int i = 0; i < w.D; ++i) {
+      int64_t k = dr[i];
+      if (k >= 0) {
+        if (d < RMAX) s.orow[d] = g.branch_row[k];
+        ++d;
+      }
+    }
+    s.d = d;
+    if (s.k + d > rs) { s.fail = BDC_TASK_DETACHED; s.farg = -2; }
+  }
+  __syncthreads();
+  const int k = s.k;
+  if (s.fail) goto done;
+
+  // ---- split chain (factors.py:428-585) -----------------------------------------
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const int si = s.sub[j], a = g.sub_col[si], cnt = g.sub_count[si];
+      const unsigned bits = s.bits[j];
+      double stay_b = 0.0;
+      for (int e = 0; e < cnt; ++e)
+        if (!((bits >> e) & 1u)) stay_b += g.sub_elem_b[si * g.E + e];
+      if (!(stay_b > 0.0)) {
+        s.fail = BDC_TASK_DEGENERATE_SPLIT; s.farg = j;
+      } else {
+        int nm = 0, nst = 0;
+        for (int e = 0; e < cnt; ++e) {
+          int row = g.sub_elem_row[si * g.E + e];
+          int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+          double sign; int far, end;
+          if (fc == a) { sign = 1.0; far = tc; end = 0; }
+          else if (tc == a) { sign = -1.0; far = fc; end = 1; }
+          else { s.fail = BDC_TASK_DETACHED; s.farg = j; break; }
+          if ((bits >> e) & 1u) {
+            s.mrow[nm] = row; s.msign[nm] = sign; s.mend[nm] = end; ++nm;
+          } else {
+            s.srow[nst] = row; s.ssign[nst] = sign; s.sfar[nst] = far;
+            s.sw[nst] = g.sub_elem_b[si * g.E + e] / stay_b; ++nst;
+          }
+        }
+        s.a = a; s.nm = nm; s.nst = nst;
+      }
+    }
+    __syncthreads();
+    if (s.fail) goto done;
+    const int a = s.a, nm = s.nm, nst = s.nst;
+    for (int idx = tid; idx < nm * j; idx += NT) {
+      int m = idx / j, i = idx % j;
+      s.mB[m][i] = Bm[(size_t)i * R + s.mrow[m]];
+    }
+    __syncthreads();
+    // coupler row over every current column: c[col] = sum_moved sign * P_{j-1}[row, col]
+    const int ncols = C0 + j;
+    for (int col = tid; col < ncols; col += NT) {
+      const int bc = base_col(g, s, col);
+      double c = 0.0;
+      for (int m = 0; m < nm; ++m) {
+        double v = g.P0[(size_t)s.mrow[m] * C0 + bc];
+        for (int i = 0; i < j; ++i) v = fma(s.mB[m][i], Cm[(size_t)i * Cs + col], v);
+        c += s.msign[m] * v;
+      }
+      Cm[(size_t)j * Cs + col] = c;
+    }
+    // the new busbar column starts as a copy of column a for every earlier term
+    for (int i = tid; i < j; i += NT) Cm[(size_t)i * Cs + C0 + j] = Cm[(size_t)i * Cs + a];
+    __syncthreads();
+    if (tid == 0) {
+      const double ca = Cm[(size_t)j * Cs + a];
+      Cm[(size_t)j * Cs + C0 + j] = ca - 1.0;
+      double den = ca;
+      for (int st = 0; st < nst; ++st) den -= s.sw[st] * Cm[(size_t)j * Cs + s.sfar[st]];
+      if (fabs(den) < ISL_TOL) { s.fail = BDC_TASK_SINGULAR_SPLIT; s.farg = j; }
+      s.den = den;
+    }
+    for (int idx = tid; idx < (nst + 1) * j; idx += NT) {
+      int st = idx / j, i = idx % j;
+      if (st < nst) s.sCfar[st][i] = Cm[(size_t)i * Cs + s.sfar[st]];
+      else s.sCa[i] = Cm[(size_t)i * Cs + a];
+    }
+    __syncthreads();
+    if (s.fail) goto done;
+    {
+      const double den = s.den;
+      for (int r = tid; r < R; r += NT) {
+        double bi[RMAX];
+#pragma unroll
+        for (int i = 0; i < RMAX; ++i) bi[i] = (i < j) ? Bm[(size_t)i * R + r] : 0.0;
+        double pa = g.P0T[(size_t)a * R + r];
+#pragma unroll
+        for (int i = 0; i < RMAX; ++i) if (i < j) pa = fma(bi[i], s.sCa[i], pa);
+        double num = 0.0;
+        for (int st = 0; st < nst; ++st) {
+          const int bf = base_col(g, s, s.sfar[st]);
+          double pf = g.P0T[(size_t)bf * R + r];
+#pragma unroll
+          for (int i = 0; i < RMAX; ++i) if (i < j) pf = fma(bi[i], s.sCfar[st][i], pf);
+          num += s.sw[st] * (pf - pa);
+          if (r == s.srow[st]) num += s.ssign[st] * s.sw[st];
+        }
+        Bm[(size_t)j * R + r] = num / den;
+      }
+    }
+    if (tid == 0) {
+      for (int m = 0; m < nm; ++m) {
+        s.rh_key[s.nrh] = s.mrow[m] * 2 + s.mend[m];
+        s.rh_col[s.nrh] = C0 + j;
+        ++s.nrh;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- disconnections (solver.py:389-406) ------------------------------------------
+  if (s.d > 0) {
+    const int d = s.d;
+    if (d > cfg.maxout) {
+      if (tid == 0) { s.fail = BDC_TASK_TOO_MANY_OUTAGES; s.farg = d; }
+      __syncthreads();
+      goto done;
+    }
+    if (tid == 0)
+      for (int i = 0; i < d; ++i) {
+        int row = s.orow[i];
+        s.ofc[i] = curcol(s, row, 0, g.row_from[row]);
+        s.otc[i] = curcol(s, row, 1, g.row_to[row]);
+      }
+    __syncthreads();
+    if (cfg.method == 0) {
+      // MODF: one d x d inner system against the post-split matrix (factors.py:373-425)
+      // rhs[i][r] = P'[r, f'_i] - P'[r, t'_i] into B slots k+i
+      for (int r = tid; r < R; r += NT) {
+        double bi[RMAX];
+#pragma unroll
+        for (int i = 0; i < RMAX; ++i) bi[i] = (i < k) ? Bm[(size_t)i * R + r] : 0.0;
+        for (int i = 0; i < d; ++i) {
+          const int fc = s.ofc[i], tc = s.otc[i];
+          double pf = g.P0T[(size_t)base_col(g, s, fc) * R + r];
+          double pt = g.P0T[(size_t)base_col(g, s, tc) * R + r];
+#pragma unroll
+          for (int ip = 0; ip < RMAX; ++ip)
+            if (ip < k) {
+              pf = fma(bi[ip], Cm[(size_t)ip * Cs + fc], pf);
+              pt = fma(bi[ip], Cm[(size_t)ip * Cs + tc], pt);
+            }
+          Bm[(size_t)(k + i) * R + r] = pf - pt;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double A[MMAX * MMAX];
+        bool big = d > MMAX;
+        if (!big) {
+          for (int aa = 0; aa < d; ++aa)
+            for (int bb = 0; bb < d; ++bb)
+              A[aa * d + bb] = (aa == bb ? 1.0 : 0.0) - Bm[(size_t)(k + bb) * R + s.orow[aa]];
+          double smax, smin;
+          svd_minmax(A, d, smax, smin);
+          if (smin < ISL_TOL * fmax(1.0, smax)) { s.fail = BDC_TASK_DISCONNECT_ISLAND; s.farg = -1; }
+          else invert_small(A, d, s.inv);
+        } else {
+          s.fail = BDC_TASK_DETACHED; s.farg = -3;
+        }
+      }
+      for (int idx = tid; idx < d * k; idx += NT) {
+        int i = idx / k, ip = idx % k;
+        s.oB[i][ip] = Bm[(size_t)ip * R + s.orow[i]];
+      }
+      __syncthreads();
+      if (s.fail) goto done;
+      // MODF values in place: modf[r][i] = sum_bb rhs[bb][r] inv[bb][i]; rows O -> -e_i
+      for (int r = tid; r < R; r += NT) {
+        double rhs[MMAX];
+        for (int bb = 0; bb < d; ++bb) rhs[bb] = Bm[(size_t)(k + bb) * R + r];
+        int own = -1;
+        for (int aa = 0; aa < d; ++aa) if (s.orow[aa] == r) own = aa;
+        for (int i = 0; i < d; ++i) {
+          double v;
+          if (own >= 0) v = (own == i) ? -1.0 : 0.0;
+          else {
+            v = 0.0;
+            for (int bb = 0; bb < d; ++bb) v += rhs[bb] * s.inv[bb * d + i];
+          }
+          Bm[(size_t)(k + i) * R + r] = v;
+        }
+      }
+      // outage rows of the post-split matrix become the new coupler rows
+      const int ncols = C0 + k;
+      for (int idx = tid; idx < d * ncols; idx += NT) {
+        int i = idx / ncols, col = idx % ncols;
+        double v = g.P0[(size_t)s.orow[i] * C0 + base_col(g, s, col)];
+        for (int ip = 0; ip < k; ++ip) v = fma(s.oB[i][ip], Cm[(size_t)ip * Cs + col], v);
+        Cm[(size_t)(k + i) * Cs + col] = v;
+      }
+      if (tid == 0) {
+        for (int i = 0; i < d; ++i) s.dead[i] = s.orow[i];
+        s.nd = d;
+      }
+      __syncthreads();
+    } else {
+      // sequential single outages (factors.py:333-370), each one rank-1 term
+      for (int i = 0; i < d; ++i) {
+        const int kk = k + i, row = s.orow[i], fc = s.ofc[i], tc = s.otc[i];
+        const int bf = base_col(g, s, fc), bt = base_col(g, s, tc);
+        for (int ip = tid; ip < kk; ip += NT) {
+          s.sCfar[0][ip] = Cm[(size_t)ip * Cs + fc];
+          s.sCfar[1][ip] = Cm[(size_t)ip * Cs + tc];
+          s.oB[0][ip] = Bm[(size_t)ip * R + row];
+        }
+        __syncthreads();
+        for (int r = tid; r < R; r += NT) {
+          double v = 0.0;
+          if (!is_dead(s.dead, s.nd, r)) {
+            double pf = g.P0T[(size_t)bf * R + r], pt = g.P0T[(size_t)bt * R + r];
+            for (int ip = 0; ip < kk; ++ip) {
+              double bv = Bm[(size_t)ip * R + r];
+              pf = fma(bv, s.sCfar[0][ip], pf);
+              pt = fma(bv, s.sCfar[1][ip], pt);
+            }
+            v = pf - pt;
+          }
+          Bm[(size_t)kk * R + r] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double den = 1.0 - Bm[(size_t)kk * R + row];
+          if (fabs(den) < ISL_TOL) { s.fail = BDC_TASK_DISCONNECT_ISLAND; s.farg = i; }
+          s.den = den;
+        }
+        __syncthreads();
+        if (s.fail) goto done;
+        for (int r = tid; r < R; r += NT)
+          Bm[(size_t)kk * R + r] = (r == row) ? -1.0 : Bm[(size_t)kk * R + r] / s.den;
+        const int ncols = C0 + k;
+        for (int col = tid; col < ncols; col += NT) {
+          double v = g.P0[(size_t)row * C0 + base_col(g, s, col)];
+          for (int ip = 0; ip < kk; ++ip) v = fma(s.oB[0][ip], Cm[(size_t)ip * Cs + col], v);
+          Cm[(size_t)kk * Cs + col] = v;
+        }
+        __syncthreads();
+        if (tid == 0) { s.dead[s.nd] = row; ++s.nd; }
+        __syncthreads();
+      }
+    }
+  }
+
+  {
+    // ---- contingency factors (solver.py:438-503) -----------------------------------
+    const int rt = k + s.d;
+    const int nd = s.nd;
+    // single-branch cases: W(c,:), den_c, feasibility
+    for (int c = tid; c < g.N1; c += NT) {
+      const int row = g.sc_row[c];
+      const int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+      double* Wc = w.Wsc + ((size_t)b * g.N1 + c) * rs;
+      double diag = g.sc_delta[c];
+      const bool dead = is_dead(s.dead, nd, row);
+      for (int j = 0; j < rt; ++j) {
+        double wv = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
+        Wc[j] = wv;
+        diag = fma(Bm[(size_t)j * R + row], wv, diag);
+      }
+      if (dead) diag = 0.0;
+      const double den = 1.0 - diag;
+      const bool ok = fabs(den) >= ISL_TOL;
+      w.den[(size_t)b * g.N1 + c] = den;
+      w.sc_ok[(size_t)b * g.N1 + c] = ok;
+      if (!ok) { set_island(w, b, g.sc_order[c]); atomicAdd(&s.nisl, 1); }
+    }
+    // multi-branch cases: m x m inner system, SVD islanding test, inverse
+    for (int q = tid; q < g.NM; q += NT) {
+      const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+      double A[MMAX * MMAX];
+      for (int i = 0; i < m; ++i) {
+        const int row = g.mb_row[st + i];
+        const int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+        double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+        for (int j = 0; j < rt; ++j) Wq[j] = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
+      }
+      for (int aa = 0; aa < m; ++aa) {
+        const int ra = g.mb_row[st + aa];
+        const bool dead = is_dead(s.dead, nd, ra);
+        for (int bb = 0; bb < m; ++bb) {
+          double v = g.Dm64[(size_t)(st + bb) * R + ra];
+          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + bb) * rs;
+          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + ra], Wq[j], v);
+          if (dead) v = 0.0;
+          A[aa * m + bb] = (aa == bb ? 1.0 : 0.0) - v;
+        }
+      }
+      double smax, smin;
+      svd_minmax(A, m, smax, smin);
+      const bool ok = !(smin < ISL_TOL * fmax(1.0, smax));
+      if (ok) invert_small(A, m, w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX);
+      w.mc_ok[(size_t)b * g.NM + q] = ok;
+      if (!ok) { set_island(w, b, g.mc_order[q]); atomicAdd(&s.nisl, 1); }
+    }
+    // injection cases: coupler coefficients of the outaged injection's columns
+    for (int q = tid; q < g.NI; q += NT) {
+      int ca, cb;
+      const int sl = g.ic_slot[q];
+      if (sl >= 0) {
+        ca = g.slot_col[sl]; cb = ca;
+        for (int j = 0; j < k; ++j) if (s.sub[j] == g.slot_sub[sl]) cb = C0 + j;
+      } else {
+        ca = cb = g.ic_col[q];
+      }
+      double* pa = w.cia + ((size_t)b * g.NI + q) * rs;
+      double* pb = w.cib + ((size_t)b * g.NI + q) * rs;
+      for (int j = 0; j < rt; ++j) { pa[j] = Cm[(size_t)j * Cs + ca]; pb[j] = Cm[(size_t)j * Cs + cb]; }
+    }
+    // active slots (slot at a split substation, nonzero setpoint), in slot order
+    for (int c0 = 0; c0 < g.K; c0 += NT) {
+      const int sl = c0 + tid;
+      int cb = -1;
+      if (sl < g.K && g.slot_sp[sl] != 0.0)
+        for (int j = 0; j < k; ++j) if (s.sub[j] == g.slot_sub[sl]) cb = C0 + j;
+      int total;
+      int pos = block_rank(cb >= 0, s.wcnt, total);
+      if (cb >= 0) {
+        int p = s.nact + pos;
+        if (p < ACTMAX) {
+          s.act_slot[p] = sl; s.act_ca[p] = g.slot_col[sl]; s.act_cb[p] = cb;
+          s.act_sp[p] = g.slot_sp[sl];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s.nact += total;
+      __syncthreads();
+    }
+    if (s.nact > ACTMAX) {
+      if (tid == 0) { s.fail = BDC_TASK_DETACHED; s.farg = -4; }
+      __syncthreads();
+      goto done;
+    }
+    // y_base[j] = sum_col p_base[col] C[j][col]  (every slot at home)
+    {
+      const int lane = tid & 31, wid = tid >> 5;
+      for (int j = wid; j < rt; j += NW) {
+        double acc = 0.0;
+        for (int col = lane; col < C0; col += 32) acc = fma(g.p_base[col], Cm[(size_t)j * Cs + col], acc);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s.ybase[j] = acc;
+      }
+    }
+    __syncthreads();
+    // Y[j][t] = y_base[j] + sum_active bit(t, s) * sp_s (C[j][col_b] - C[j][col_a])
+    const uint8_t* ib = w.inj + (size_t)b * w.T * g.K;
+    double* Y = w.Y + (size_t)b * rs * w.T;
+    for (int idx = tid; idx < rt * w.T; idx += NT) {
+      const int j = idx / w.T, t = idx % w.T;
+      double y = s.ybase[j];
+      for (int a2 = 0; a2 < s.nact; ++a2)
+        if (ib[(size_t)t * g.K + s.act_slot[a2]])
+          y += s.act_sp[a2] * (Cm[(size_t)j * Cs + s.act_cb[a2]] - Cm[(size_t)j * Cs + s.act_ca[a2]]);
+      Y[idx] = y;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (s.nisl > 0 && cfg.policy == 1) { s.fail = BDC_TASK_ISLAND_ERROR; s.farg = s.nisl; }
+      w.rank[b] = rt;
+    }
+  }
+  __syncthreads();
+
+done:
+  if (tid == 0) {
+    w.status[b] = s.fail;
+    w.sarg[b] = s.farg;
+    w.nsplit[b] = s.k;
+    w.ndead[b] = s.nd;
+    w.nisl[b] = s.nisl;
+    for (int i = 0; i < s.nd; ++i) w.dead[(size_t)b * RMAX + i] = s.dead[i];
+    for (int j = 0; j < s.k && j < RMAX; ++j) w.splitsub[(size_t)b * RMAX + j] = s.sub[j];
+    // splits applied until the first failure (Instrumentation.count_bsdf, solver.py:375)
+    int applied = s.k;
+    if (s.fail == BDC_TASK_DEGENERATE_SPLIT || s.fail == BDC_TASK_SINGULAR_SPLIT) applied = s.farg;
+    atomicAdd(w.bsdf, (unsigned long long)applied);
+  }
+}
+
+void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t st) {
+  k_update<<<w.Wb, NT, 0, st>>>(g, c, w);
+}
+
+}  // namespace bdc
