@@ -193,7 +193,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_W = L.add(B * g.N1 * rs * 8), o_den = L.add(B * g.N1 * 8), o_ok = L.add(B * g.N1);
   size_t o_Wm = L.add(B * g.NMB * rs * 8), o_mi = L.add(B * g.NM * MMAX * MMAX * 8), o_mo = L.add(B * g.NM);
   size_t o_ca = L.add(B * g.NI * rs * 8), o_cb = L.add(B * g.NI * rs * 8);
-  size_t o_Y = L.add(B * rs * T * 8), o_n0 = L.add(B * g.R * T * 8), o_n0s = L.add(B * g.M * T * 4);
+  size_t o_Y = L.add(B * rs * T * 8), o_n0s = L.add(B * g.M * T * 4);
   size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
   size_t o_met = L.add(B * 8), o_best = L.add(B * 8), o_fe = L.add(B);
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
@@ -214,7 +214,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.Wsc = (double*)(base + o_W); x.den = (double*)(base + o_den); x.sc_ok = (uint8_t*)(base + o_ok);
   x.Wm = (double*)(base + o_Wm); x.minv = (double*)(base + o_mi); x.mc_ok = (uint8_t*)(base + o_mo);
   x.cia = (double*)(base + o_ca); x.cib = (double*)(base + o_cb);
-  x.Y = (double*)(base + o_Y); x.n0 = (double*)(base + o_n0); x.n0s = (float*)(base + o_n0s);
+  x.Y = (double*)(base + o_Y); x.n0s = (float*)(base + o_n0s);
   x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b);
   x.metric = (double*)(base + o_met); x.best = (int64_t*)(base + o_best); x.feasible = (uint8_t*)(base + o_fe);
   x.n0cnt = (int*)(base + o_n0c); x.n0pos = (int*)(base + o_n0p); x.n0flow = (double*)(base + o_n0f);
@@ -425,7 +425,6 @@ extern "C" int bdc_probe_flows(BdcSession* s, const uint8_t* splits, const int64
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   if (e == cudaSuccess && hs[0] == 0) {
-    launch_n0(g, w, st);
     launch_probe(g, w, dn0, dn1, dok, st);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(n0, dn0, (size_t)g.R * T * 8, cudaMemcpyDeviceToHost, st);

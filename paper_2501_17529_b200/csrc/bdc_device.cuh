@@ -61,7 +61,6 @@ struct Work {
   uint8_t* mc_ok; // (Wb, NM)
   double* cia; double* cib;  // (Wb, NI, rs) coupler coefficients of the injection column
   double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
-  double* n0;     // (Wb, R, T)    N-0 flows, FP64, dead rows exactly 0
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
   double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
@@ -157,7 +156,19 @@ __device__ inline bool invert_small(const double* A, int n, double* Ainv) {
   return true;
 }
 
-// Kernel launchers (bdc_kernels.cu).
+// FP64 N-0 flow of one row for one candidate, from the task's factors:
+// n0 = f0 + B'' y_t, exactly 0 on disconnected rows (solver.py:575-595).
+__device__ __forceinline__ double n0_at(const DevGrid& g, const Work& w, int b, int row, int t,
+                                        int rt, const int* dead, int nd) {
+  if (is_dead(dead, nd, row)) return 0.0;
+  double v = g.f0[row];
+  const double* Bm = w.Bm + (size_t)b * w.rs * g.R;
+  const double* Y = w.Y + (size_t)b * w.rs * w.T;
+  for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * g.R + row], Y[(size_t)j * w.T + t], v);
+  return v;
+}
+
+// Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_single(const DevGrid& g, const Work& w, cudaStream_t s);

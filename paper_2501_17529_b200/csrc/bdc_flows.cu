@@ -1,9 +1,9 @@
 // bdc_flows.cu -- Kernels 2-4: N-0 contraction, fused N-1 screening, winner selection.
 //
-//   k_n0      N-0 flows of every candidate: n0 = f0 + B'' y_t (FP64), the
-//             rank-r form of `_candidate_base_flows` (solver.py:575-595);
-//             writes n0 (FP64) and the rating-scaled FP32 copy n0s that the
-//             N-1 stage streams, and folds max|n0|/rating into the metric.
+//   k_n0      N-0 flows of every candidate on the monitored rows,
+//             n0 = f0 + B'' y_t (FP64, the rank-r form of `_candidate_base_flows`,
+//             solver.py:575-595), written once as FP32 n0/rating (the only
+//             per-task tensor the N-1 stage streams) and folded into the metric.
 //   k_single  THE hot kernel.  Single-branch N-1 for every (case, candidate)
 //             pair of a task, fused: forms LODF columns on the fly from the
 //             shared base D_base and the task's rank-r factors
@@ -11,80 +11,120 @@
 //             outage update F = n0 + L n0[r_c] (solver.py:612-613), takes
 //             |F|/rating and max-reduces over monitored rows and cases into
 //             the per-candidate metric (solver.py:625-631, agg_m :235-252).
-//             The (case x candidate x branch) tensor never leaves registers.
+//             The (case x candidate x branch) tensor never leaves registers;
+//             row chunks of n0/rating and D_base stream through shared memory
+//             with cp.async double buffering.
 //   k_other   multi-branch (MODF, solver.py:614-618) and injection
-//             (solver.py:619-622) contingencies, same fusion, FP64.
+//             (solver.py:619-622) contingencies of one task, same fusion.
 //   k_select  islanding penalty floor and first-index argmin (solver.py:804-823).
 #include "bdc_device.cuh"
 
 namespace bdc {
 
-// ------------------------------------------------------------------------------- k_n0
 namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// 4-byte async copy global->shared; src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp4(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 constexpr int N0_TB = 128;
 constexpr int N0_RB = 32;
+
 }  // namespace
 
+// ------------------------------------------------------------------------------- k_n0
 __global__ void __launch_bounds__(N0_TB) k_n0(DevGrid g, Work w) {
-  const int b = blockIdx.z, r0 = blockIdx.y * N0_RB, tid = threadIdx.x;
+  const int b = blockIdx.z, p0 = blockIdx.y * N0_RB, tid = threadIdx.x;
   const int t = blockIdx.x * N0_TB + tid;
   if (w.status[b] != 0) return;
-  const int rs = w.rs, rt = w.rank[b], T = w.T, R = g.R;
+  const int rs = w.rs, rt = w.rank[b], T = w.T, R = g.R, M = g.M;
   __shared__ double sB[RMAX][N0_RB];
+  __shared__ double sF[N0_RB], sI[N0_RB];
   __shared__ int sdead[RMAX];
   const int nd = w.ndead[b];
-  for (int idx = tid; idx < rt * N0_RB; idx += N0_TB) {
-    int j = idx / N0_RB, rr = idx % N0_RB, r = r0 + rr;
-    sB[j][rr] = r < R ? w.Bm[((size_t)b * rs + j) * R + r] : 0.0;
-  }
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  __syncthreads();
+  for (int idx = tid; idx < rt * N0_RB; idx += N0_TB) {
+    const int j = idx / N0_RB, pp = idx % N0_RB, p = p0 + pp;
+    sB[j][pp] = p < M ? w.Bm[((size_t)b * rs + j) * R + g.mon_row[p]] : 0.0;
+  }
+  for (int pp = tid; pp < N0_RB; pp += N0_TB) {
+    const int p = p0 + pp;
+    const int row = p < M ? g.mon_row[p] : -1;
+    const bool live = row >= 0 && !is_dead(sdead, nd, row);
+    sF[pp] = live ? g.f0[row] : 0.0;
+    sI[pp] = live ? g.inv_rating[p] : 0.0;  // dead rows: flow exactly 0
+  }
   __syncthreads();
   if (t >= T) return;
   double y[RMAX];
 #pragma unroll
   for (int j = 0; j < RMAX; ++j) y[j] = (j < rt) ? w.Y[((size_t)b * rs + j) * T + t] : 0.0;
   float mx = 0.f;
-  const int rend = min(R, r0 + N0_RB);
-  for (int r = r0; r < rend; ++r) {
-    const int rr = r - r0;
-    double v = g.f0[r];
+  const int pend = min(M, p0 + N0_RB);
+  for (int p = p0; p < pend; ++p) {
+    const int pp = p - p0;
+    double v = sF[pp];
 #pragma unroll
     for (int j = 0; j < RMAX; ++j)
-      if (j < rt) v = fma(sB[j][rr], y[j], v);
-    if (is_dead(sdead, nd, r)) v = 0.0;
-    w.n0[((size_t)b * R + r) * T + t] = v;
-    const int p = g.row_mon_pos[r];
-    if (p >= 0) {
-      const float sc = (float)(v * g.inv_rating[p]);
-      w.n0s[((size_t)b * g.M + p) * T + t] = sc;
-      mx = fmaxf(mx, fabsf(sc));
-    }
+      if (j < rt) v = fma(sB[j][pp], y[j], v);
+    const float sc = (float)(v * sI[pp]);
+    w.n0s[((size_t)b * M + p) * T + t] = sc;
+    mx = fmaxf(mx, fabsf(sc));
   }
   atomic_max_pos(&w.m32[(size_t)b * T + t], mx);
 }
 
 // --------------------------------------------------------------------------- k_single
-// Thread tile: CPT cases x TPT candidates; CTA tile NC = CPT*TX cases x TT = TPT*TY
-// candidates; monitored rows streamed through shared memory RC at a time.
-template <int CPT, int TPT, int TX, int TY>
-__global__ void __launch_bounds__(TX* TY) k_single(DevGrid g, Work w) {
-  constexpr int NTH = TX * TY, NC = CPT * TX, TT = TPT * TY, RC = 32;
+// Thread tile: CPT cases x TPT candidates; CTA tile NC = CPT*TX cases x
+// TT = TPT*TY candidates; monitored rows streamed RC at a time through a
+// cp.async double buffer (n0/rating chunk [RC][TT], D_base chunk [RC][NC],
+// B'' rows [rt][RC]).
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+__global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, Work w) {
+  constexpr int NTH = TX * TY, NC = CPT * TX, TT = TPT * TY;
   const int b = blockIdx.z;
   if (w.status[b] != 0) return;
   const int c0 = blockIdx.x * NC, t0 = blockIdx.y * TT;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   const int rs = w.rs, rt = w.rank[b], T = w.T, M = g.M, N1 = g.N1, R = g.R;
-  extern __shared__ double sW[];  // [NC][rt]
+  // dynamic: [sW NC*rs f64][sBb 2*rs*RC f64][sN 2*RC*TT f32][sD 2*RC*NC f32]
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* sW = reinterpret_cast<double*>(dsm);   // [NC][rt]
+  double* sBb = sW + NC * rs;                    // [2][rt][RC] B'' rows of the chunk
+  float* sNp = reinterpret_cast<float*>(sBb + 2 * rs * RC);
+  float* sDp = sNp + 2 * RC * TT;
+#define SN(bf, r_, t_) sNp[((bf) * RC + (r_)) * TT + (t_)]
+#define SD(bf, r_, c_) sDp[((bf) * RC + (r_)) * NC + (c_)]
   __shared__ double sInvDen[NC];
   __shared__ int sRowC[NC];
-  __shared__ double sB[RMAX][RC];
-  __shared__ double sInv[RC];
-  __shared__ int sRow[RC];
+  __shared__ double sInv[2][RC];
+  __shared__ int sRow[2][RC];
   __shared__ __align__(16) float sL[RC][NC];
-  __shared__ __align__(16) float sN[RC][TT];
   __shared__ int sdead[RMAX];
   const int nd = w.ndead[b];
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  const float* n0s = w.n0s + (size_t)b * M * T;
+  const bool vecN = (T % 4) == 0 && (t0 % 4) == 0;
+  const bool vecD = (N1 % 4) == 0;
 
+  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   for (int idx = tid; idx < NC * rt; idx += NTH) {
     const int cc = idx / rt, j = idx % rt, c = c0 + cc;
     sW[idx] = c < N1 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
@@ -95,24 +135,10 @@ __global__ void __launch_bounds__(TX* TY) k_single(DevGrid g, Work w) {
     sInvDen[cc] = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
     sRowC[cc] = c < N1 ? g.sc_row[c] : -1;
   }
-  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   __syncthreads();
 
-  float acc[CPT][TPT], sv[CPT][TPT];
-#pragma unroll
-  for (int i = 0; i < CPT; ++i) {
-    const int row = sRowC[tx * CPT + i];
-#pragma unroll
-    for (int jj = 0; jj < TPT; ++jj) {
-      const int t = t0 + ty * TPT + jj;
-      sv[i][jj] = (row >= 0 && t < T) ? (float)w.n0[((size_t)b * R + row) * T + t] : 0.f;
-      acc[i][jj] = 0.f;
-    }
-  }
-  const bool vecN = (T % 4) == 0;
-
-  for (int m0 = 0; m0 < M; m0 += RC) {
-    __syncthreads();
+  // stage one row chunk (async): row ids + 1/rating, B'' rows, n0/rating, D_base
+  auto issue = [&](int m0, int buf) {
     for (int rr = tid; rr < RC; rr += NTH) {
       const int m = m0 + rr;
       int row = -1;
@@ -122,39 +148,104 @@ __global__ void __launch_bounds__(TX* TY) k_single(DevGrid g, Work w) {
         inv = g.inv_rating[m];
         if (is_dead(sdead, nd, row)) row = -1;
       }
-      sRow[rr] = row;
-      sInv[rr] = inv;
+      sRow[buf][rr] = row;
+      sInv[buf][rr] = inv;
     }
     for (int idx = tid; idx < rt * RC; idx += NTH) {
       const int j = idx / RC, rr = idx % RC, m = m0 + rr;
-      sB[j][rr] = m < M ? w.Bm[((size_t)b * rs + j) * R + g.mon_row[m]] : 0.0;
+      const bool ok = m < M;
+      cp8(&sBb[(buf * rs + j) * RC + rr], ok ? &Bm[(size_t)j * R + g.mon_row[m]] : Bm, ok);
     }
     if (vecN) {
       for (int idx = tid; idx < RC * (TT / 4); idx += NTH) {
         const int rr = idx / (TT / 4), q = idx % (TT / 4), m = m0 + rr, t = t0 + 4 * q;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (m < M && t < T) v = *reinterpret_cast<const float4*>(&w.n0s[((size_t)b * M + m) * T + t]);
-        *reinterpret_cast<float4*>(&sN[rr][4 * q]) = v;
+        const bool ok = m < M && t < T;
+        cp16(&SN(buf, rr, 4 * q), ok ? &n0s[(size_t)m * T + t] : n0s, ok);
       }
     } else {
       for (int idx = tid; idx < RC * TT; idx += NTH) {
         const int rr = idx / TT, tt = idx % TT, m = m0 + rr, t = t0 + tt;
-        sN[rr][tt] = (m < M && t < T) ? w.n0s[((size_t)b * M + m) * T + t] : 0.f;
+        const bool ok = m < M && t < T;
+        cp4(&SN(buf, rr, tt), ok ? &n0s[(size_t)m * T + t] : n0s, ok);
       }
     }
+    if (vecD) {
+      for (int idx = tid; idx < RC * (NC / 4); idx += NTH) {
+        const int rr = idx / (NC / 4), q = idx % (NC / 4), m = m0 + rr, c = c0 + 4 * q;
+        const bool ok = m < M && c < N1;
+        cp16(&SD(buf, rr, 4 * q), ok ? &g.D32[(size_t)m * N1 + c] : g.D32, ok);
+      }
+    } else {
+      for (int idx = tid; idx < RC * NC; idx += NTH) {
+        const int rr = idx / NC, cc = idx % NC, m = m0 + rr, c = c0 + cc;
+        const bool ok = m < M && c < N1;
+        cp4(&SD(buf, rr, cc), ok ? &g.D32[(size_t)m * N1 + c] : g.D32, ok);
+      }
+    }
+    cp_commit();
+  };
+
+  issue(0, 0);
+
+  // s(c,t) = n0[r_c][t] from the factors (FP64 -> FP32), computed cooperatively
+  // RC cases at a time into the (still idle) second n0 buffer while chunk 0 is in flight
+  float acc[CPT][TPT], sv[CPT][TPT];
+  {
+    const double* Y = w.Y + (size_t)b * rs * T;
+    for (int cb = 0; cb < NC; cb += RC) {
+      for (int idx = tid; idx < RC * TT; idx += NTH) {
+        const int cc = cb + idx / TT, tt = idx % TT, t = t0 + tt;
+        const int row = sRowC[cc];
+        float sval = 0.f;
+        if (row >= 0 && t < T && !is_dead(sdead, nd, row)) {
+          double v = g.f0[row];
+          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Y[(size_t)j * T + t], v);
+          sval = (float)v;
+        }
+        SN(1, idx / TT, tt) = sval;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int cc = tx * CPT + i;
+        if (cc >= cb && cc < cb + RC) {
+#pragma unroll
+          for (int jj = 0; jj < TPT; ++jj) sv[i][jj] = SN(1, cc - cb, ty * TPT + jj);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TPT; ++jj) acc[i][jj] = 0.f;
+  }
+
+  const int nchunks = (M + RC - 1) / RC;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) {
+      issue((ch + 1) * RC, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
     __syncthreads();
-    // LODF columns of this row chunk, formed on the fly in FP64, stored scaled by 1/rating
+    // LODF columns of this chunk, formed on the fly in FP64, stored scaled by 1/rating
     for (int idx = tid; idx < RC * NC; idx += NTH) {
-      const int rr = idx / NC, cc = idx % NC, m = m0 + rr, c = c0 + cc;
-      const int row = sRow[rr];
+      const int rr = idx / NC, cc = idx % NC;
+      const int row = sRow[buf][rr];
       float lv = 0.f;
-      if (row >= 0 && c < N1 && sInvDen[cc] != 0.0) {
+      const double idn = sInvDen[cc];
+      if (row >= 0 && idn != 0.0) {
         if (row == sRowC[cc]) {
-          lv = (float)(-sInv[rr]);
+          lv = (float)(-sInv[buf][rr]);
         } else {
-          double v = (double)g.D32[(size_t)m * N1 + c];
-          for (int j = 0; j < rt; ++j) v = fma(sB[j][rr], sW[cc * rt + j], v);
-          lv = (float)(v * sInvDen[cc] * sInv[rr]);
+          double v = (double)SD(buf, rr, cc);
+          const double* Bc = &sBb[(buf * rs) * RC + rr];
+          const double* Wc = &sW[cc * rt];
+          for (int j = 0; j < rt; ++j) v = fma(Bc[j * RC], Wc[j], v);
+          lv = (float)(v * idn * sInv[buf][rr]);
         }
       }
       sL[rr][cc] = lv;
@@ -166,13 +257,14 @@ __global__ void __launch_bounds__(TX* TY) k_single(DevGrid g, Work w) {
 #pragma unroll
       for (int i = 0; i < CPT; ++i) l[i] = sL[rr][tx * CPT + i];
 #pragma unroll
-      for (int jj = 0; jj < TPT; ++jj) n[jj] = sN[rr][ty * TPT + jj];
+      for (int jj = 0; jj < TPT; ++jj) n[jj] = SN(buf, rr, ty * TPT + jj);
 #pragma unroll
       for (int i = 0; i < CPT; ++i)
 #pragma unroll
         for (int jj = 0; jj < TPT; ++jj)
           acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
     }
+    __syncthreads();
   }
   constexpr int GW = TX < 32 ? TX : 32;  // lanes of a warp sharing one candidate group
 #pragma unroll
@@ -185,121 +277,152 @@ __global__ void __launch_bounds__(TX* TY) k_single(DevGrid g, Work w) {
     const int t = t0 + ty * TPT + jj;
     if ((tx % GW) == 0 && t < T) atomic_max_pos(&w.m32[(size_t)b * T + t], v);
   }
+#undef SN
+#undef SD
 }
 
 // ---------------------------------------------------------------------------- k_other
+// One CTA per (task, candidate chunk): every multi-branch and injection case,
+// FP32 like k_single.  Case q contributes F = n0 + sum_j L_j(q, r) s_j(q, t)
+// with (multi) L_j = MODF column j, s_j = n0[r_j] or (injection) L_0 =
+// -sp P''[:, col_a], s_0 = 1, L_1 = -sp (P''[:, col_b] - P''[:, col_a]),
+// s_1 = candidate bit.  Columns are formed per row chunk in FP64.
 namespace {
-constexpr int OT = 256;   // threads; one candidate per thread per t-chunk
-constexpr int ORC = 128;  // monitored rows per chunk
+constexpr int OT = 256;   // threads
+constexpr int OTT = 64;   // candidates per CTA
+constexpr int ORC = 32;   // monitored rows per chunk
+constexpr int OQ = 8;     // other cases per pass
+constexpr int OJ = MMAX;  // terms per case
 }  // namespace
 
 __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
-  const int q = blockIdx.x, b = blockIdx.z, tid = threadIdx.x;
-  const int t = blockIdx.y * OT + tid;
+  const int b = blockIdx.z, tid = threadIdx.x, t0 = blockIdx.x * OTT;
+  const int q0 = blockIdx.y * OQ;
   if (w.status[b] != 0) return;
-  const bool multi = q < g.NM;
-  if (multi && !w.mc_ok[(size_t)b * g.NM + q]) return;  // islanded: penalty, not flows
   const int rs = w.rs, rt = w.rank[b], T = w.T, R = g.R, M = g.M;
-  __shared__ double sL[ORC][MMAX];
-  __shared__ double sInv[ORC];
-  __shared__ int sRow[ORC];
+  const int nq = min(OQ, g.NM + g.NI - q0);
+  __shared__ float sS[OQ][OJ][OTT];     // s_j(q, t)
+  __shared__ float sL[ORC][OQ][OJ];     // L_j(q, r) / rating
+  __shared__ float sN[ORC][OTT];
+  __shared__ int sM[OQ];                // terms of case q (0: islanded -> skipped)
   __shared__ int sdead[RMAX];
-  __shared__ double sMinv[MMAX * MMAX];
-  __shared__ double sW[MMAX][RMAX];
-  __shared__ double sCa[RMAX], sCb[RMAX];
   const int nd = w.ndead[b];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
-  int m, st = 0, qi = 0, ca = 0;
-  double sp = 0.0;
-  if (multi) {
-    st = g.mc_start[q];
-    m = g.mc_start[q + 1] - st;
-    for (int i = tid; i < m * m; i += OT) sMinv[i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
-    for (int i = tid; i < m * rt; i += OT) sW[i / rt][i % rt] = w.Wm[((size_t)b * g.NMB + st + i / rt) * rs + i % rt];
-  } else {
-    qi = q - g.NM;
-    m = 2;
-    const int sl = g.ic_slot[qi];
-    ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
-    sp = g.ic_sp[qi];
-    for (int j = tid; j < rt; j += OT) {
-      sCa[j] = w.cia[((size_t)b * g.NI + qi) * rs + j];
-      sCb[j] = w.cib[((size_t)b * g.NI + qi) * rs + j];
+  for (int qq = tid; qq < OQ; qq += OT) {
+    int m = 0;
+    const int q = q0 + qq;
+    if (qq < nq) {
+      if (q < g.NM) m = w.mc_ok[(size_t)b * g.NM + q] ? g.mc_start[q + 1] - g.mc_start[q] : 0;
+      else m = 2;
     }
+    sM[qq] = m;
   }
-  // per-candidate multipliers of the correction columns
-  double sv[MMAX];
-  for (int j = 0; j < MMAX; ++j) sv[j] = 0.0;
-  if (t < T) {
-    if (multi) {
-      for (int j = 0; j < m; ++j) sv[j] = w.n0[((size_t)b * R + g.mb_row[st + j]) * T + t];
-    } else {
-      const int sl = g.ic_slot[qi];
-      sv[0] = 1.0;
-      sv[1] = (sl >= 0 && w.inj[((size_t)b * T + t) * g.K + sl]) ? 1.0 : 0.0;
+  __syncthreads();
+  // multipliers s_j(q, t)
+  for (int idx = tid; idx < nq * OJ * OTT; idx += OT) {
+    const int qq = idx / (OJ * OTT), j = (idx / OTT) % OJ, tt = idx % OTT, t = t0 + tt, q = q0 + qq;
+    float v = 0.f;
+    if (j < sM[qq] && t < T) {
+      if (q < g.NM) {
+        v = (float)n0_at(g, w, b, g.mb_row[g.mc_start[q] + j], t, rt, sdead, nd);
+      } else {
+        const int sl = g.ic_slot[q - g.NM];
+        v = (j == 0) ? 1.f : ((sl >= 0 && w.inj[((size_t)b * T + t) * g.K + sl]) ? 1.f : 0.f);
+      }
     }
+    sS[qq][j][tt] = v;
   }
-  float mx = 0.f;
+  // thread -> (case, candidate) pairs
+  float acc[(OQ * OTT + OT - 1) / OT];
+  constexpr int NP = (OQ * OTT + OT - 1) / OT;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc[k] = 0.f;
+  const double* Bm = w.Bm + (size_t)b * rs * R;
   for (int m0 = 0; m0 < M; m0 += ORC) {
     __syncthreads();
-    for (int rr = tid; rr < ORC; rr += OT) {
-      const int mm = m0 + rr;
-      int row = -1;
-      if (mm < M) {
-        row = g.mon_row[mm];
-        sInv[rr] = g.inv_rating[mm];
-        if (is_dead(sdead, nd, row)) row = -1;
-      } else {
-        sInv[rr] = 0.0;
-      }
-      sRow[rr] = row;
-      double L[MMAX];
-      for (int j = 0; j < MMAX; ++j) L[j] = 0.0;
-      if (row >= 0) {
-        if (multi) {
+    for (int idx = tid; idx < ORC * OTT; idx += OT) {
+      const int rr = idx / OTT, tt = idx % OTT, m = m0 + rr, t = t0 + tt;
+      sN[rr][tt] = (m < M && t < T) ? w.n0s[((size_t)b * M + m) * T + t] : 0.f;
+    }
+    for (int idx = tid; idx < ORC * nq; idx += OT) {
+      const int rr = idx / nq, qq = idx % nq, m = m0 + rr, q = q0 + qq;
+      float Lf[OJ];
+      for (int j = 0; j < OJ; ++j) Lf[j] = 0.f;
+      const int mq = sM[qq];
+      const int row = m < M ? g.mon_row[m] : -1;
+      if (row >= 0 && mq > 0 && !is_dead(sdead, nd, row)) {
+        const double inv = g.inv_rating[m];
+        if (q < g.NM) {
+          const int st = g.mc_start[q];
           int own = -1;
-          for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+          for (int a = 0; a < mq; ++a) if (g.mb_row[st + a] == row) own = a;
           if (own >= 0) {
-            L[own] = -1.0;
+            Lf[own] = (float)(-inv);
           } else {
             double Dv[MMAX];
-            for (int i = 0; i < m; ++i) {
+            for (int i = 0; i < mq; ++i) {
               double v = g.Dm64[(size_t)(st + i) * R + row];
-              for (int j = 0; j < rt; ++j) v = fma(w.Bm[((size_t)b * rs + j) * R + row], sW[i][j], v);
+              const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
               Dv[i] = v;
             }
-            for (int j = 0; j < m; ++j) {
+            const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
+            for (int j = 0; j < mq; ++j) {
               double v = 0.0;
-              for (int i = 0; i < m; ++i) v += Dv[i] * sMinv[i * m + j];
-              L[j] = v;
+              for (int i = 0; i < mq; ++i) v += Dv[i] * Mi[i * mq + j];
+              Lf[j] = (float)(v * inv);
             }
           }
         } else {
+          const int qi = q - g.NM, sl = g.ic_slot[qi];
+          const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
+          const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
+          const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
           double pa = g.P0T[(size_t)ca * R + row], pb = pa;
           for (int j = 0; j < rt; ++j) {
-            const double bv = w.Bm[((size_t)b * rs + j) * R + row];
-            pa = fma(bv, sCa[j], pa);
-            pb = fma(bv, sCb[j], pb);
+            const double bv = Bm[(size_t)j * R + row];
+            pa = fma(bv, pa_[j], pa);
+            pb = fma(bv, pb_[j], pb);
           }
-          L[0] = -sp * pa;
-          L[1] = -sp * (pb - pa);
+          const double sp = g.ic_sp[qi];
+          Lf[0] = (float)(-sp * pa * inv);
+          Lf[1] = (float)(-sp * (pb - pa) * inv);
         }
       }
-      for (int j = 0; j < MMAX; ++j) sL[rr][j] = L[j];
+      for (int j = 0; j < OJ; ++j) sL[rr][qq][j] = Lf[j];
     }
     __syncthreads();
-    if (t < T) {
-      const int rend = min(ORC, M - m0);
+    const int rend = min(ORC, M - m0);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int pid = tid + k * OT;
+      const int qq = pid / OTT, tt = pid % OTT;
+      if (qq >= nq) continue;
+      const int mq = sM[qq];
+      if (mq == 0) continue;
+      float a = acc[k];
       for (int rr = 0; rr < rend; ++rr) {
-        const int row = sRow[rr];
-        if (row < 0) continue;
-        double f = w.n0[((size_t)b * R + row) * T + t];
-        for (int j = 0; j < m; ++j) f = fma(sL[rr][j], sv[j], f);
-        mx = fmaxf(mx, (float)(fabs(f) * sInv[rr]));
+        float f = sN[rr][tt];
+        for (int j = 0; j < mq; ++j) f = fmaf(sL[rr][qq][j], sS[qq][j][tt], f);
+        a = fmaxf(a, fabsf(f));
       }
+      acc[k] = a;
     }
   }
-  if (t < T) atomic_max_pos(&w.m32[(size_t)b * T + t], mx);
+  // every thread's pairs share one candidate slot per k: reduce through smem atomics
+  __syncthreads();
+  float* sMax = &sN[0][0];
+  for (int tt = tid; tt < OTT; tt += OT) sMax[tt] = 0.f;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int pid = tid + k * OT;
+    const int qq = pid / OTT, tt = pid % OTT;
+    if (qq < nq) atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(acc[k]));
+  }
+  __syncthreads();
+  for (int tt = tid; tt < OTT; tt += OT)
+    if (t0 + tt < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + tt], sMax[tt]);
 }
 
 // --------------------------------------------------------------------------- k_select
@@ -337,37 +460,45 @@ __global__ void k_select(DevGrid g, DevCfg cfg, Work w) {
 
 // ---------------------------------------------------------------------------- launches
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s) {
-  dim3 grid((w.T + N0_TB - 1) / N0_TB, (g.R + N0_RB - 1) / N0_RB, w.Wb);
+  if (g.M == 0) return;
+  dim3 grid((w.T + N0_TB - 1) / N0_TB, (g.M + N0_RB - 1) / N0_RB, w.Wb);
   k_n0<<<grid, N0_TB, 0, s>>>(g, w);
 }
 
-template <int CPT, int TPT, int TX, int TY>
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
 static void launch_single_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int NC = CPT * TX, TT = TPT * TY;
-  const size_t dyn = (size_t)NC * w.rs * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_single<CPT, TPT, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
-    attr = true;
+  const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
+                     (2 * (size_t)RC * TT + 2 * (size_t)RC * NC) * sizeof(float);
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    // opt in to every byte of shared memory the kernel's static part leaves free
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_single<CPT, TPT, TX, TY, RC, MINB>);
+    max_dyn = optin - (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(k_single<CPT, TPT, TX, TY, RC, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
   dim3 grid((g.N1 + NC - 1) / NC, (w.T + TT - 1) / TT, w.Wb);
-  k_single<CPT, TPT, TX, TY><<<grid, TX * TY, dyn, s>>>(g, w);
+  k_single<CPT, TPT, TX, TY, RC, MINB><<<grid, TX * TY, dyn, s>>>(g, w);
 }
 
 void launch_single(const DevGrid& g, const Work& w, cudaStream_t s) {
-  if (g.N1 == 0) return;
-  if (w.T >= 96) launch_single_t<2, 16, 32, 8>(g, w, s);       // 64 cases x 128 candidates
-  else if (w.T >= 48) launch_single_t<2, 8, 32, 8>(g, w, s);   // 64 x 64
-  else if (w.T >= 24) launch_single_t<4, 4, 32, 8>(g, w, s);   // 128 x 32
-  else if (w.T >= 12) launch_single_t<4, 4, 64, 4>(g, w, s);   // 256 x 16
-  else launch_single_t<4, 2, 64, 4>(g, w, s);                  // 256 x 8
+  if (g.N1 == 0 || g.M == 0) return;
+  if (w.T >= 96) launch_single_t<2, 16, 32, 8, 32, 2>(g, w, s);      // 64 cases x 128 candidates
+  else if (w.T >= 48) launch_single_t<2, 8, 32, 8, 32, 3>(g, w, s);  // 64 x 64
+  else if (w.T >= 24) launch_single_t<4, 4, 32, 8, 32, 3>(g, w, s);  // 128 x 32
+  else if (w.T >= 12) launch_single_t<4, 4, 64, 4, 32, 3>(g, w, s);  // 256 x 16
+  else launch_single_t<4, 2, 64, 4, 32, 3>(g, w, s);                 // 256 x 8
 }
 
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s) {
   const int nq = g.NM + g.NI;
-  if (nq == 0) return;
-  dim3 grid(nq, (w.T + OT - 1) / OT, w.Wb);
+  if (nq == 0 || g.M == 0) return;
+  dim3 grid((w.T + OTT - 1) / OTT, (nq + OQ - 1) / OQ, w.Wb);
   k_other<<<grid, OT, 0, s>>>(g, w);
 }
 

@@ -74,11 +74,18 @@ __device__ void wl_insert(WarpList& L, int kg, double r, int c, int p, double f)
   if (L.n < kg) ++L.n;
 }
 
-// Merge each lane's list into the warp list: kc rounds of warp argmax.
+__device__ __forceinline__ double warp_thresh(const volatile WarpList& L, int kg) {
+  return L.n == kg ? L.rel[kg - 1] : -1.0;
+}
+
+// Merge the lanes' lists into the warp list: up to kc rounds of warp argmax,
+// stopping as soon as the best remaining head cannot enter the warp's top-kg.
 template <int KC>
 __device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int case_order) {
   const int lane = threadIdx.x & 31;
   for (int round = 0; round < kc; ++round) {
+    const double th = warp_thresh(L, kg);
+    if (!__any_sync(0xffffffffu, lt.rel[0] >= 0.0 && lt.rel[0] >= th)) break;
     double r = lt.rel[0];
     int p = lt.pos[0], src = lane;
     for (int o = 16; o; o >>= 1) {
@@ -87,7 +94,6 @@ __device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int cas
       const int os = __shfl_xor_sync(0xffffffffu, src, o);
       if (better(orr, op, r, p)) { r = orr; p = op; src = os; }
     }
-    if (r < 0.0) break;  // every lane empty
     const double f = __shfl_sync(0xffffffffu, lt.flow[0], src);
     if (lane == src) lt.pop();
     if (lane == 0) wl_insert(L, kg, r, case_order, p, f);
@@ -95,14 +101,10 @@ __device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int cas
   }
 }
 
-__device__ __forceinline__ double warp_thresh(const WarpList& L, int kg) {
-  return L.n == kg ? L.rel[kg - 1] : -1.0;
-}
-
 }  // namespace
 
 template <int KC>
-__global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.x;
   if (w.status[b] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -114,19 +116,30 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
   __shared__ WarpList wl[RW];
   __shared__ int sdead[RMAX];
   __shared__ double sred[RW];
-  __shared__ double sbr[RW];
-  __shared__ int sbp[RW];
+  __shared__ double sbr[2][RW];
+  __shared__ int sbp[2][RW];
   __shared__ double sWc[RW][RMAX];
   __shared__ double sMinv[RW][MMAX * MMAX];
+  __shared__ double sY[RMAX];
   __shared__ int sN0pos[KMAX];
   const int nd = w.ndead[b];
-  for (int r = tid; r < R; r += RT) n0b[r] = w.n0[((size_t)b * R + r) * T + best];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  if (tid < rt) sY[tid] = w.Y[((size_t)b * rs + tid) * T + best];
   if (lane == 0) wl[wid].n = 0;
+  __syncthreads();
+  // the winner's N-0 column, FP64, from the factors
+  for (int r = tid; r < R; r += RT) {
+    double v = 0.0;
+    if (!is_dead(sdead, nd, r)) {
+      v = g.f0[r];
+      for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + r], sY[j], v);
+    }
+    n0b[r] = v;
+  }
   __syncthreads();
 
   double mymax = 0.0;
-  // ---- N-0 report: kg rounds of block argmax over reportable positions ----------------
+  // ---- N-0 report: kg rounds of block argmax (one barrier per round) ----------------
   {
     double pr = 1e300;
     int pp = -1;
@@ -136,8 +149,7 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
       int bp = INT_MAX;
       for (int p = tid; p < M; p += RT) {
         const int row = g.mon_row[p];
-        const double f = n0b[row];
-        const double rel = fabs(f) / g.rating[p];
+        const double rel = fabs(n0b[row]) * g.inv_rating[p];
         if (round == 0) mymax = fmax(mymax, rel);
         if (is_dead(sdead, nd, row)) continue;
         // next entry in (rel desc, pos asc) order after the previous pick
@@ -149,15 +161,12 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
         const int op = __shfl_xor_sync(0xffffffffu, bp, o);
         if (better(orr, op, br, bp)) { br = orr; bp = op; }
       }
-      if (lane == 0) { sbr[wid] = br; sbp[wid] = bp; }
+      const int sl = round & 1;
+      if (lane == 0) { sbr[sl][wid] = br; sbp[sl][wid] = bp; }
       __syncthreads();
-      if (tid == 0) {
-        for (int i = 1; i < RW; ++i)
-          if (better(sbr[i], sbp[i], sbr[0], sbp[0])) { sbr[0] = sbr[i]; sbp[0] = sbp[i]; }
-      }
-      __syncthreads();
-      br = sbr[0]; bp = sbp[0];
-      __syncthreads();
+      br = sbr[sl][0]; bp = sbp[sl][0];
+      for (int i = 1; i < RW; ++i)
+        if (better(sbr[sl][i], sbp[sl][i], br, bp)) { br = sbr[sl][i]; bp = sbp[sl][i]; }
       if (br < 0.0) break;
       if (tid == 0) sN0pos[round] = bp;
       pr = br; pp = bp;
@@ -170,7 +179,7 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
         const double f = n0b[g.mon_row[p]];
         w.n0pos[(size_t)b * kg + i] = p;
         w.n0flow[(size_t)b * kg + i] = f;
-        w.n0rel[(size_t)b * kg + i] = fabs(f) / g.rating[p];
+        w.n0rel[(size_t)b * kg + i] = fabs(f) * g.inv_rating[p];
       }
     }
   }
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
     if (kind == 0) {
       const int rowc = g.sc_row[q];
       const double sc = n0b[rowc];
-      const double den = w.den[(size_t)b * g.N1 + q];
+      const double idn = 1.0 / w.den[(size_t)b * g.N1 + q];
       for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * g.N1 + q) * rs + j];
       __syncwarp();
       const double* Dc = g.D64 + (size_t)q * R;
@@ -209,9 +218,9 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
         } else {
           double dv = Dc[row];
           for (int j = 0; j < rt; ++j) dv = fma(Bm[(size_t)j * R + row], sWc[wid][j], dv);
-          f = n0b[row] + (dv / den) * sc;
+          f = n0b[row] + (dv * idn) * sc;
         }
-        const double rel = fabs(f) / g.rating[p];
+        const double rel = fabs(f) * g.inv_rating[p];
         mymax = fmax(mymax, rel);
         if (row != rowc && rel >= thresh) lt.insert(rel, p, f);
       }
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
             f += l * sv[j];
           }
         }
-        const double rel = fabs(f) / g.rating[p];
+        const double rel = fabs(f) * g.inv_rating[p];
         mymax = fmax(mymax, rel);
         if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
       }
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(RT) k_report(DevGrid g, DevCfg cfg, Work w) {
         double pc = g.P0T[(size_t)ca * R + row];
         for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
         const double f = n0b[row] - pc * sp;
-        const double rel = fabs(f) / g.rating[p];
+        const double rel = fabs(f) * g.inv_rating[p];
         mymax = fmax(mymax, rel);
         if (rel >= thresh) lt.insert(rel, p, f);
       }
@@ -305,7 +314,7 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)R * T;
        idx += (long long)gridDim.x * blockDim.x) {
     const int row = (int)(idx / T), t = (int)(idx % T);
-    const double n0v = w.n0[(size_t)row * T + t];
+    const double n0v = n0_at(g, w, 0, row, t, rt, dead, nd);
     if (ci == ncase) { n0o[idx] = n0v; continue; }
     const bool drow = is_dead(dead, nd, row);
     int order;
@@ -314,7 +323,7 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
       order = g.sc_order[ci];
       if (w.sc_ok[ci]) {
         const int rowc = g.sc_row[ci];
-        const double sc = w.n0[(size_t)rowc * T + t];
+        const double sc = n0_at(g, w, 0, rowc, t, rt, dead, nd);
         if (drow) f = 0.0;
         else if (row == rowc) f = n0v - sc;
         else {
@@ -342,7 +351,7 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
                 for (int jj = 0; jj < rt; ++jj) v = fma(Bm[(size_t)jj * R + row], w.Wm[(size_t)(st + i) * rs + jj], v);
                 l += v * w.minv[(size_t)q * MMAX * MMAX + i * m + j];
               }
-            f += l * w.n0[(size_t)g.mb_row[st + j] * T + t];
+            f += l * n0_at(g, w, 0, g.mb_row[st + j], t, rt, dead, nd);
           }
         }
       }
