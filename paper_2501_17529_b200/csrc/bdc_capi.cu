@@ -195,6 +195,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_ca = L.add(B * g.NI * rs * 8), o_cb = L.add(B * g.NI * rs * 8);
   size_t o_Y = L.add(B * rs * T * 8), o_n0s = L.add(B * g.M * T * 4);
   size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
+  size_t o_cmax = L.add(B * (size_t)(g.N1 + g.NM + g.NI) * T * 4);
   size_t o_met = L.add(B * 8), o_best = L.add(B * 8), o_fe = L.add(B);
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
   size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
@@ -216,6 +217,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.cia = (double*)(base + o_ca); x.cib = (double*)(base + o_cb);
   x.Y = (double*)(base + o_Y); x.n0s = (float*)(base + o_n0s);
   x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b);
+  x.cmax = (float*)(base + o_cmax);
   x.metric = (double*)(base + o_met); x.best = (int64_t*)(base + o_best); x.feasible = (uint8_t*)(base + o_fe);
   x.n0cnt = (int*)(base + o_n0c); x.n0pos = (int*)(base + o_n0p); x.n0flow = (double*)(base + o_n0f);
   x.n0rel = (double*)(base + o_n0r);
@@ -316,8 +318,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
     launch_update(g, s->cfg, x, st);
-    cudaEventRecord(E[2], st);
-    launch_n0(g, x, st);
+    cudaEventRecord(E[2], st);  // (N-0 contraction is fused into the update kernel's epilogue)
     cudaEventRecord(E[3], st);
     launch_single(g, x, st);
     cudaEventRecord(E[4], st);

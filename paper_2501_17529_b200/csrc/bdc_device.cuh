@@ -16,6 +16,11 @@ constexpr int KMAX = BDC_MAX_TOPK;        // top-k limits
 constexpr int ACTMAX = 64;                // active slots (slots at split substations) per task
 constexpr int RHMAX = RMAX * EMAX;        // re-homed branch ends per task
 constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors.py:48-49)
+// Absolute margin (in units of relative loading) on the FP32 screening values
+// used to decide which cases the FP64 winner report must revisit.  The FP32
+// path's observed error is ~1e-6 (tests: <= 1e-5 enforced), so 1e-3 is a
+// >= 100x safety factor; a wider margin only costs report time.
+constexpr float SCREEN_EPS = 1e-3f;
 
 // Grid tables, device-resident for the session lifetime.
 struct DevGrid {
@@ -63,6 +68,7 @@ struct Work {
   double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
+  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate)
   double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
   // outputs (device)
   double* metric; int64_t* best; uint8_t* feasible;

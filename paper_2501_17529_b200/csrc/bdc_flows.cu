@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, Work w) {
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   for (int idx = tid; idx < NC * rt; idx += NTH) {
     const int cc = idx / rt, j = idx % rt, c = c0 + cc;
-    sW[idx] = c < N1 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
+    sW[j * NC + cc] = c < N1 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
   }
   for (int cc = tid; cc < NC; cc += NTH) {
     const int c = c0 + cc;
@@ -231,24 +231,37 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, Work w) {
       cp_wait<0>();
     }
     __syncthreads();
-    // LODF columns of this chunk, formed on the fly in FP64, stored scaled by 1/rating
-    for (int idx = tid; idx < RC * NC; idx += NTH) {
-      const int rr = idx / NC, cc = idx % NC;
-      const int row = sRow[buf][rr];
-      float lv = 0.f;
+    // LODF columns of this chunk, formed on the fly in FP64, stored scaled by 1/rating.
+    // Thread owns one case column cc and RPT rows; the rank-r correction runs as
+    // j-outer register accumulation (W[j][cc] once, B rows broadcast from smem).
+    {
+      constexpr int RG = NTH / NC;   // row groups
+      constexpr int RPT = RC / RG;   // rows per thread (multiple of 8)
+      static_assert(RPT % 8 == 0, "row tile");
+      const int cc = tid % NC, rg = tid / NC;
       const double idn = sInvDen[cc];
-      if (row >= 0 && idn != 0.0) {
-        if (row == sRowC[cc]) {
-          lv = (float)(-sInv[buf][rr]);
-        } else {
-          double v = (double)SD(buf, rr, cc);
-          const double* Bc = &sBb[(buf * rs) * RC + rr];
-          const double* Wc = &sW[cc * rt];
-          for (int j = 0; j < rt; ++j) v = fma(Bc[j * RC], Wc[j], v);
-          lv = (float)(v * idn * sInv[buf][rr]);
+      const int rowc = sRowC[cc];
+#pragma unroll
+      for (int kb = 0; kb < RPT; kb += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (double)SD(buf, rg + (kb + k) * RG, cc);
+        for (int j = 0; j < rt; ++j) {
+          const double wj = sW[j * NC + cc];
+          const double* Bj = &sBb[(buf * rs + j) * RC + rg];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = fma(Bj[(kb + k) * RG], wj, v[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int rr = rg + (kb + k) * RG;
+          const int row = sRow[buf][rr];
+          const double sc = idn * sInv[buf][rr];
+          float lv = 0.f;
+          if (row >= 0 && idn != 0.0) lv = (row == rowc) ? (float)(-sInv[buf][rr]) : (float)(v[k] * sc);
+          sL[rr][cc] = lv;
         }
       }
-      sL[rr][cc] = lv;
     }
     __syncthreads();
 #pragma unroll 4
@@ -265,6 +278,20 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, Work w) {
           acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
     }
     __syncthreads();
+  }
+  // per-(case, candidate) maxima: the winner report's exact pruning bound
+  {
+    float* cm = w.cmax + (size_t)b * (N1 + g.NM + g.NI) * T;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = c0 + tx * CPT + i;
+      if (c >= N1) continue;
+#pragma unroll
+      for (int jj = 0; jj < TPT; ++jj) {
+        const int t = t0 + ty * TPT + jj;
+        if (t < T) cm[(size_t)c * T + t] = acc[i][jj];
+      }
+    }
   }
   constexpr int GW = TX < 32 ? TX : 32;  // lanes of a warp sharing one candidate group
 #pragma unroll
@@ -414,11 +441,15 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
   float* sMax = &sN[0][0];
   for (int tt = tid; tt < OTT; tt += OT) sMax[tt] = 0.f;
   __syncthreads();
+  float* cm = w.cmax + (size_t)b * (g.N1 + g.NM + g.NI) * T;
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
     const int pid = tid + k * OT;
     const int qq = pid / OTT, tt = pid % OTT;
-    if (qq < nq) atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(acc[k]));
+    if (qq < nq) {
+      atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(acc[k]));
+      if (t0 + tt < T) cm[(size_t)(g.N1 + q0 + qq) * T + t0 + tt] = acc[k];
+    }
   }
   __syncthreads();
   for (int tt = tid; tt < OTT; tt += OT)

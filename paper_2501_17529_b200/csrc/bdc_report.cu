@@ -20,6 +20,7 @@ namespace {
 
 constexpr int RT = 256;
 constexpr int RW = RT / 32;
+constexpr int CAND_CAP = 1024;
 
 __device__ __forceinline__ bool better(double r1, int p1, double r2, int p2) {
   return r1 > r2 || (r1 == r2 && p1 < p2);
@@ -184,17 +185,73 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
     }
   }
 
-  // ---- every feasible contingency of the winner ------------------------------------------
-  LaneTop<KC> lt;
+  // ---- which contingencies can matter: exact pruning on the FP32 screening maxima --------
+  // A case can place an entry in the final top-kg only if its true max loading is at
+  // least the kg-th largest true case max; with |FP32 - FP64| <= SCREEN_EPS that means
+  // cmax >= kth(cmax) - 2 eps.  The metric's binding case satisfies the same bound.
   const int ncase = g.N1 + g.NM + g.NI;
-  for (int ci = wid; ci < ncase; ci += RW) {
+  const float* cm = w.cmax + (size_t)b * ncase * T + best;
+  auto feasible_case = [&](int ci) -> bool {
+    if (ci < g.N1) return w.sc_ok[(size_t)b * g.N1 + ci] != 0;
+    if (ci < g.N1 + g.NM) return w.mc_ok[(size_t)b * g.NM + (ci - g.N1)] != 0;
+    return true;
+  };
+  float theta = -1.f;
+  {
+    float pv = 3.4e38f;
+    int pi = -1, found = 0;
+    float kth = -1.f;
+    for (int round = 0; round < kg; ++round) {
+      double br = -1.0;
+      int bp = INT_MAX;
+      for (int ci = tid; ci < ncase; ci += RT) {
+        if (!feasible_case(ci)) continue;
+        const float v = cm[(size_t)ci * T];
+        if (!(v < pv || (v == pv && ci > pi))) continue;
+        if (better(v, ci, br, bp)) { br = v; bp = ci; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (better(orr, op, br, bp)) { br = orr; bp = op; }
+      }
+      const int sl = round & 1;
+      if (lane == 0) { sbr[sl][wid] = br; sbp[sl][wid] = bp; }
+      __syncthreads();
+      br = sbr[sl][0]; bp = sbp[sl][0];
+      for (int i = 1; i < RW; ++i)
+        if (better(sbr[sl][i], sbp[sl][i], br, bp)) { br = sbr[sl][i]; bp = sbp[sl][i]; }
+      if (br < 0.0) break;
+      pv = (float)br; pi = bp; kth = (float)br;
+      ++found;
+    }
+    theta = found == kg ? kth - 2.f * SCREEN_EPS : -1.f;
+  }
+  __shared__ int sCand[CAND_CAP];
+  __shared__ int sNCand;
+  if (tid == 0) sNCand = 0;
+  __syncthreads();
+  for (int ci = tid; ci < ncase; ci += RT) {
+    if (feasible_case(ci) && cm[(size_t)ci * T] >= theta) {
+      const int p = atomicAdd(&sNCand, 1);
+      if (p < CAND_CAP) sCand[p] = ci;
+    }
+  }
+  __syncthreads();
+  const int ncand = sNCand;
+  const bool listed = ncand <= CAND_CAP;  // else scan every case with the same predicate
+  const int nloop = listed ? ncand : ncase;
+
+  // ---- FP64 re-evaluation of the candidate cases for the winner ----------------------------
+  LaneTop<KC> lt;
+  for (int li = wid; li < nloop; li += RW) {
+    const int ci = listed ? sCand[li] : li;
+    if (!listed && !(feasible_case(ci) && cm[(size_t)ci * T] >= theta)) continue;
     int order, kind = 0, q = ci;
     if (ci < g.N1) {
-      if (!w.sc_ok[(size_t)b * g.N1 + ci]) continue;
       order = g.sc_order[ci];
     } else if (ci < g.N1 + g.NM) {
       kind = 1; q = ci - g.N1;
-      if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
       order = g.mc_order[q];
     } else {
       kind = 2; q = ci - g.N1 - g.NM;
@@ -386,7 +443,7 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
 }
 
 int kernels_per_wave(const DevGrid& g) {
-  return 4 + (g.N1 > 0) + (g.NM + g.NI > 0);
+  return 3 + (g.N1 > 0 && g.M > 0) + (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

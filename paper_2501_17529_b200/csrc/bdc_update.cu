@@ -53,7 +53,9 @@ struct UpdShared {
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
   double act_sp[ACTMAX];
   int nisl;
+  unsigned tmax[1024];  // per-candidate N-0 max (float bits), one t-chunk
 };
+constexpr int NT0MAX = 1024;
 
 __device__ __forceinline__ int base_col(const DevGrid& g, const UpdShared& s, int col) {
   return col < g.C0 ? col : g.sub_col[s.sub[col - g.C0]];
@@ -89,7 +91,7 @@ __device__ void set_island(const Work& w, int b, int order) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT) k_update(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w) {
   __shared__ UpdShared s;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int R = g.R, C0 = g.C0, rs = w.rs, Cs = w.Cs;
@@ -209,18 +211,13 @@ __global__ void __launch_bounds__(NT) k_update(DevGrid g, DevCfg cfg, Work w) {
     {
       const double den = s.den;
       for (int r = tid; r < R; r += NT) {
-        double bi[RMAX];
-#pragma unroll
-        for (int i = 0; i < RMAX; ++i) bi[i] = (i < j) ? Bm[(size_t)i * R + r] : 0.0;
         double pa = g.P0T[(size_t)a * R + r];
-#pragma unroll
-        for (int i = 0; i < RMAX; ++i) if (i < j) pa = fma(bi[i], s.sCa[i], pa);
+        for (int i = 0; i < j; ++i) pa = fma(Bm[(size_t)i * R + r], s.sCa[i], pa);
         double num = 0.0;
         for (int st = 0; st < nst; ++st) {
           const int bf = base_col(g, s, s.sfar[st]);
           double pf = g.P0T[(size_t)bf * R + r];
-#pragma unroll
-          for (int i = 0; i < RMAX; ++i) if (i < j) pf = fma(bi[i], s.sCfar[st][i], pf);
+          for (int i = 0; i < j; ++i) pf = fma(Bm[(size_t)i * R + r], s.sCfar[st][i], pf);
           num += s.sw[st] * (pf - pa);
           if (r == s.srow[st]) num += s.ssign[st] * s.sw[st];
         }
@@ -256,19 +253,15 @@ __global__ void __launch_bounds__(NT) k_update(DevGrid g, DevCfg cfg, Work w) {
       // MODF: one d x d inner system against the post-split matrix (factors.py:373-425)
       // rhs[i][r] = P'[r, f'_i] - P'[r, t'_i] into B slots k+i
       for (int r = tid; r < R; r += NT) {
-        double bi[RMAX];
-#pragma unroll
-        for (int i = 0; i < RMAX; ++i) bi[i] = (i < k) ? Bm[(size_t)i * R + r] : 0.0;
         for (int i = 0; i < d; ++i) {
           const int fc = s.ofc[i], tc = s.otc[i];
           double pf = g.P0T[(size_t)base_col(g, s, fc) * R + r];
           double pt = g.P0T[(size_t)base_col(g, s, tc) * R + r];
-#pragma unroll
-          for (int ip = 0; ip < RMAX; ++ip)
-            if (ip < k) {
-              pf = fma(bi[ip], Cm[(size_t)ip * Cs + fc], pf);
-              pt = fma(bi[ip], Cm[(size_t)ip * Cs + tc], pt);
-            }
+          for (int ip = 0; ip < k; ++ip) {
+            const double bv = Bm[(size_t)ip * R + r];
+            pf = fma(bv, Cm[(size_t)ip * Cs + fc], pf);
+            pt = fma(bv, Cm[(size_t)ip * Cs + tc], pt);
+          }
           Bm[(size_t)(k + i) * R + r] = pf - pt;
         }
       }
@@ -485,6 +478,33 @@ __global__ void __launch_bounds__(NT) k_update(DevGrid g, DevCfg cfg, Work w) {
     if (tid == 0) {
       if (s.nisl > 0 && cfg.policy == 1) { s.fail = BDC_TASK_ISLAND_ERROR; s.farg = s.nisl; }
       w.rank[b] = rt;
+    }
+    __syncthreads();
+    // ---- N-0 contraction (solver.py:575-595): n0 = f0 + B'' y_t on the monitored rows,
+    // stored as FP32 n0/rating for the N-1 stage; its max is the N-0 part of the metric
+    if (!s.fail) {
+      const int T = w.T, M = g.M;
+      float* n0s = w.n0s + (size_t)b * M * T;
+      for (int tc = 0; tc < T; tc += NT0MAX) {
+        const int tn = min(NT0MAX, T - tc);
+        for (int i = tid; i < tn; i += NT) s.tmax[i] = 0u;
+        __syncthreads();
+        for (int idx = tid; idx < M * tn; idx += NT) {
+          const int p = idx / tn, t = tc + idx % tn;
+          const int row = g.mon_row[p];
+          float sc = 0.f;
+          if (!is_dead(s.dead, nd, row)) {
+            double v = g.f0[row];
+            for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Y[(size_t)j * T + t], v);
+            sc = (float)(v * g.inv_rating[p]);
+          }
+          n0s[(size_t)p * T + t] = sc;
+          atomicMax(&s.tmax[t - tc], __float_as_uint(fabsf(sc)));
+        }
+        __syncthreads();
+        for (int i = tid; i < tn; i += NT) w.m32[(size_t)b * T + tc + i] = s.tmax[i];
+        __syncthreads();
+      }
     }
   }
   __syncthreads();
