@@ -51,7 +51,47 @@ struct BdcSession {
   DevCfg cfg{};
   std::vector<void*> owned;
   int64_t wave_cap = 0;
+  size_t total_mem = 0;
+  // cached wave workspaces (one per concurrent call), reused across calls
+  std::mutex ws_mu;
+  std::vector<std::pair<char*, size_t>> ws_free;
 };
+
+namespace {
+// Borrow a workspace of at least `bytes` from the session cache (or allocate one);
+// returned to the cache when the call ends (the call synchronises its stream first).
+struct WsLease {
+  BdcSession* s;
+  char* p = nullptr;
+  size_t bytes = 0;
+  WsLease(BdcSession* s_, size_t need) : s(s_) {
+    {
+      std::lock_guard<std::mutex> lk(s->ws_mu);
+      for (size_t i = 0; i < s->ws_free.size(); ++i)
+        if (s->ws_free[i].second >= need) {
+          p = s->ws_free[i].first;
+          bytes = s->ws_free[i].second;
+          s->ws_free.erase(s->ws_free.begin() + i);
+          return;
+        }
+    }
+    if (cudaMalloc((void**)&p, need) != cudaSuccess) {
+      cudaGetLastError();
+      std::lock_guard<std::mutex> lk(s->ws_mu);  // drop smaller cached buffers and retry
+      for (auto& f : s->ws_free) cudaFree(f.first);
+      s->ws_free.clear();
+      p = nullptr;
+      if (cudaMalloc((void**)&p, need) != cudaSuccess) { cudaGetLastError(); p = nullptr; return; }
+    }
+    bytes = need;
+  }
+  ~WsLease() {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    s->ws_free.emplace_back(p, bytes);
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -139,6 +179,9 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   s->cfg.method = C->multi_outage_method;
   s->cfg.maxout = C->max_simultaneous_outages;
   s->cfg.penalty = C->islanding_penalty;
+  size_t fb = 0, tb = 0;
+  cudaMemGetInfo(&fb, &tb);
+  s->total_mem = tb;
   // keep freed workspace in the stream-ordered pool between calls
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -153,6 +196,7 @@ int bdc_session_destroy(BdcSession* s) {
   if (!s) return BDC_OK;
   cudaSetDevice(s->device);
   for (void* p : s->owned) cudaFree(p);
+  for (auto& f : s->ws_free) cudaFree(f.first);
   delete s;
   return BDC_OK;
 }
@@ -196,6 +240,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_Y = L.add(B * rs * T * 8), o_n0s = L.add(B * g.M * T * 4);
   size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
   size_t o_cmax = L.add(B * (size_t)(g.N1 + g.NM + g.NI) * T * 4);
+  const size_t NTERM = (size_t)g.NMB + 2 * (size_t)g.NI;
+  size_t o_Lo = L.add(B * (size_t)g.M * NTERM * 4), o_So = L.add(B * NTERM * T * 4);
   size_t o_met = L.add(B * 8), o_best = L.add(B * 8), o_fe = L.add(B);
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
   size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
@@ -218,6 +264,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.Y = (double*)(base + o_Y); x.n0s = (float*)(base + o_n0s);
   x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b);
   x.cmax = (float*)(base + o_cmax);
+  x.Lo = (float*)(base + o_Lo); x.So = (float*)(base + o_So); x.NTERM = (int)NTERM;
   x.metric = (double*)(base + o_met); x.best = (int64_t*)(base + o_best); x.feasible = (uint8_t*)(base + o_fe);
   x.n0cnt = (int*)(base + o_n0c); x.n0pos = (int*)(base + o_n0p); x.n0flow = (double*)(base + o_n0f);
   x.n0rel = (double*)(base + o_n0r);
@@ -274,20 +321,21 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   cudaStream_t st = sg.s;
 
   // wave size: bounded by a workspace budget, the grid-z limit and the user cap
+  // (a deterministic function of the batch shape and the device size, so repeated
+  // calls reuse the session's cached workspace instead of re-mapping memory)
   size_t per = carve(g, 1, T, D, Ein, rs, nullptr, nullptr);
-  size_t freeb = 0, totb = 0;
-  CK(cudaMemGetInfo(&freeb, &totb));
-  size_t budget = std::min<size_t>(freeb / 3, (size_t)16 << 30);
+  size_t budget = std::min<size_t>(s->total_mem / 8, (size_t)16 << 30);
   int64_t Wb = (int64_t)(budget / per);
   if (Wb < 1) return fail(BDC_ELIMIT, "one task does not fit in device memory");
   Wb = std::min<int64_t>(Wb, 32768);
   if (s->wave_cap > 0) Wb = std::min<int64_t>(Wb, s->wave_cap);
   Wb = std::min<int64_t>(Wb, B);
+  if (B > Wb) Wb = (B + ((B + Wb - 1) / Wb) - 1) / ((B + Wb - 1) / Wb);  // balance the waves
   Work w{};
   size_t bytes = carve(g, (int)Wb, T, D, Ein, rs, nullptr, nullptr);
-  char* ws = nullptr;
-  CK(cudaMallocAsync((void**)&ws, bytes, st));
-  carve(g, (int)Wb, T, D, Ein, rs, ws, &w);
+  WsLease ws(s, bytes);
+  if (!ws.p) return fail(BDC_ECUDA, "workspace allocation failed (" + std::to_string(bytes) + " bytes)");
+  carve(g, (int)Wb, T, D, Ein, rs, ws.p, &w);
   CK(cudaMemsetAsync(w.lf, 0, 32, st));
 
   const int nwaves = (int)((B + Wb - 1) / Wb);
@@ -364,7 +412,6 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   }
   unsigned long long counters[2] = {0, 0};
   if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 16, cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(ws, st);
   cudaError_t es = cudaStreamSynchronize(st);
   if (err == cudaSuccess) err = es;
   if (err == cudaSuccess) {

@@ -69,6 +69,11 @@ struct Work {
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
   float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate)
+  // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j]
+  // (term j of multi case q at mc_start[q]+i, of injection case qi at NMB+2qi+{0,1})
+  float* Lo;      // (Wb, M, NTERM)  correction columns / rating on monitored rows
+  float* So;      // (Wb, NTERM, T)  per-candidate multipliers
+  int NTERM;      // NMB + 2 NI
   double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
   // outputs (device)
   double* metric; int64_t* best; uint8_t* feasible;

@@ -309,151 +309,95 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, Work w) {
 }
 
 // ---------------------------------------------------------------------------- k_other
-// One CTA per (task, candidate chunk): every multi-branch and injection case,
-// FP32 like k_single.  Case q contributes F = n0 + sum_j L_j(q, r) s_j(q, t)
-// with (multi) L_j = MODF column j, s_j = n0[r_j] or (injection) L_0 =
-// -sp P''[:, col_a], s_0 = 1, L_1 = -sp (P''[:, col_b] - P''[:, col_a]),
-// s_1 = candidate bit.  Columns are formed per row chunk in FP64.
+// One CTA per (task, candidate tile): every multi-branch and injection case of
+// the task, FP32 like k_single.  The update kernel already laid the cases out
+// as correction terms, F = n0 + sum_j Lo[r][j] So[j][t] (MODF columns with the
+// pre-outage flows of the outaged rows, or the injection column with 1 and the
+// candidate's slot bit), so this is a pure stream over monitored-row chunks.
 namespace {
 constexpr int OT = 256;   // threads
 constexpr int OTT = 64;   // candidates per CTA
 constexpr int ORC = 32;   // monitored rows per chunk
-constexpr int OQ = 8;     // other cases per pass
-constexpr int OJ = MMAX;  // terms per case
+constexpr int OQG = OT / OTT;  // case groups
 }  // namespace
 
 __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
-  const int b = blockIdx.z, tid = threadIdx.x, t0 = blockIdx.x * OTT;
-  const int q0 = blockIdx.y * OQ;
+  const int b = blockIdx.y, tid = threadIdx.x, t0 = blockIdx.x * OTT;
   if (w.status[b] != 0) return;
-  const int rs = w.rs, rt = w.rank[b], T = w.T, R = g.R, M = g.M;
-  const int nq = min(OQ, g.NM + g.NI - q0);
-  __shared__ float sS[OQ][OJ][OTT];     // s_j(q, t)
-  __shared__ float sL[ORC][OQ][OJ];     // L_j(q, r) / rating
-  __shared__ float sN[ORC][OTT];
-  __shared__ int sM[OQ];                // terms of case q (0: islanded -> skipped)
-  __shared__ int sdead[RMAX];
-  const int nd = w.ndead[b];
-  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
-  for (int qq = tid; qq < OQ; qq += OT) {
-    int m = 0;
-    const int q = q0 + qq;
-    if (qq < nq) {
-      if (q < g.NM) m = w.mc_ok[(size_t)b * g.NM + q] ? g.mc_start[q + 1] - g.mc_start[q] : 0;
-      else m = 2;
-    }
-    sM[qq] = m;
+  const int T = w.T, M = g.M, NTM = w.NTERM, nq = g.NM + g.NI;
+  extern __shared__ __align__(16) float osm[];
+  float* sS = osm;                        // [NTM][OTT]
+  float* sLo = sS + NTM * OTT;            // [2][ORC][NTM]
+  float* sN = sLo + 2 * ORC * NTM;        // [2][ORC][OTT]
+  const float* Lo = w.Lo + (size_t)b * M * NTM;
+  const float* n0s = w.n0s + (size_t)b * M * T;
+  const int tt = tid % OTT, qg = tid / OTT, t = t0 + tt;
+  for (int idx = tid; idx < NTM * OTT; idx += OT) {
+    const int j = idx / OTT, u = t0 + idx % OTT;
+    sS[idx] = u < T ? w.So[((size_t)b * NTM + j) * T + u] : 0.f;
   }
-  __syncthreads();
-  // multipliers s_j(q, t)
-  for (int idx = tid; idx < nq * OJ * OTT; idx += OT) {
-    const int qq = idx / (OJ * OTT), j = (idx / OTT) % OJ, tt = idx % OTT, t = t0 + tt, q = q0 + qq;
-    float v = 0.f;
-    if (j < sM[qq] && t < T) {
-      if (q < g.NM) {
-        v = (float)n0_at(g, w, b, g.mb_row[g.mc_start[q] + j], t, rt, sdead, nd);
-      } else {
-        const int sl = g.ic_slot[q - g.NM];
-        v = (j == 0) ? 1.f : ((sl >= 0 && w.inj[((size_t)b * T + t) * g.K + sl]) ? 1.f : 0.f);
-      }
+  auto issue = [&](int m0, int buf) {
+    for (int idx = tid; idx < ORC * NTM; idx += OT) {
+      const int rr = idx / NTM, j = idx % NTM, m = m0 + rr;
+      const bool ok = m < M;
+      cp4(&sLo[(buf * ORC + rr) * NTM + j], ok ? &Lo[(size_t)m * NTM + j] : Lo, ok);
     }
-    sS[qq][j][tt] = v;
-  }
-  // thread -> (case, candidate) pairs
-  float acc[(OQ * OTT + OT - 1) / OT];
-  constexpr int NP = (OQ * OTT + OT - 1) / OT;
-#pragma unroll
-  for (int k = 0; k < NP; ++k) acc[k] = 0.f;
-  const double* Bm = w.Bm + (size_t)b * rs * R;
-  for (int m0 = 0; m0 < M; m0 += ORC) {
-    __syncthreads();
     for (int idx = tid; idx < ORC * OTT; idx += OT) {
-      const int rr = idx / OTT, tt = idx % OTT, m = m0 + rr, t = t0 + tt;
-      sN[rr][tt] = (m < M && t < T) ? w.n0s[((size_t)b * M + m) * T + t] : 0.f;
+      const int rr = idx / OTT, u = idx % OTT, m = m0 + rr;
+      const bool ok = m < M && t0 + u < T;
+      cp4(&sN[(buf * ORC + rr) * OTT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
     }
-    for (int idx = tid; idx < ORC * nq; idx += OT) {
-      const int rr = idx / nq, qq = idx % nq, m = m0 + rr, q = q0 + qq;
-      float Lf[OJ];
-      for (int j = 0; j < OJ; ++j) Lf[j] = 0.f;
-      const int mq = sM[qq];
-      const int row = m < M ? g.mon_row[m] : -1;
-      if (row >= 0 && mq > 0 && !is_dead(sdead, nd, row)) {
-        const double inv = g.inv_rating[m];
-        if (q < g.NM) {
-          const int st = g.mc_start[q];
-          int own = -1;
-          for (int a = 0; a < mq; ++a) if (g.mb_row[st + a] == row) own = a;
-          if (own >= 0) {
-            Lf[own] = (float)(-inv);
-          } else {
-            double Dv[MMAX];
-            for (int i = 0; i < mq; ++i) {
-              double v = g.Dm64[(size_t)(st + i) * R + row];
-              const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
-              Dv[i] = v;
-            }
-            const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
-            for (int j = 0; j < mq; ++j) {
-              double v = 0.0;
-              for (int i = 0; i < mq; ++i) v += Dv[i] * Mi[i * mq + j];
-              Lf[j] = (float)(v * inv);
-            }
-          }
-        } else {
-          const int qi = q - g.NM, sl = g.ic_slot[qi];
-          const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
-          const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
-          const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
-          double pa = g.P0T[(size_t)ca * R + row], pb = pa;
-          for (int j = 0; j < rt; ++j) {
-            const double bv = Bm[(size_t)j * R + row];
-            pa = fma(bv, pa_[j], pa);
-            pb = fma(bv, pb_[j], pb);
-          }
-          const double sp = g.ic_sp[qi];
-          Lf[0] = (float)(-sp * pa * inv);
-          Lf[1] = (float)(-sp * (pb - pa) * inv);
-        }
-      }
-      for (int j = 0; j < OJ; ++j) sL[rr][qq][j] = Lf[j];
+    cp_commit();
+  };
+  // this thread's cases: q = qg, qg + OQG, ...; islanded multi cases are skipped
+  constexpr int QMAX = 16;
+  float acc[QMAX];
+#pragma unroll
+  for (int k = 0; k < QMAX; ++k) acc[k] = 0.f;
+  issue(0, 0);
+  const int nchunks = (M + ORC - 1) / ORC;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) {
+      issue((ch + 1) * ORC, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
     __syncthreads();
-    const int rend = min(ORC, M - m0);
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int pid = tid + k * OT;
-      const int qq = pid / OTT, tt = pid % OTT;
-      if (qq >= nq) continue;
-      const int mq = sM[qq];
-      if (mq == 0) continue;
+    const float* L = &sLo[buf * ORC * NTM];
+    const float* N = &sN[buf * ORC * OTT];
+    int k = 0;
+    for (int q = qg; q < nq && k < QMAX; q += OQG, ++k) {
+      int st, m;
+      if (q < g.NM) { st = g.mc_start[q]; m = g.mc_start[q + 1] - st; }
+      else { st = g.NMB + 2 * (q - g.NM); m = 2; }
       float a = acc[k];
-      for (int rr = 0; rr < rend; ++rr) {
-        float f = sN[rr][tt];
-        for (int j = 0; j < mq; ++j) f = fmaf(sL[rr][qq][j], sS[qq][j][tt], f);
+      for (int rr = 0; rr < ORC; ++rr) {
+        float f = N[rr * OTT + tt];
+        for (int j = 0; j < m; ++j) f = fmaf(L[rr * NTM + st + j], sS[(st + j) * OTT + tt], f);
         a = fmaxf(a, fabsf(f));
       }
       acc[k] = a;
     }
+    __syncthreads();
   }
-  // every thread's pairs share one candidate slot per k: reduce through smem atomics
-  __syncthreads();
-  float* sMax = &sN[0][0];
-  for (int tt = tid; tt < OTT; tt += OT) sMax[tt] = 0.f;
-  __syncthreads();
-  float* cm = w.cmax + (size_t)b * (g.N1 + g.NM + g.NI) * T;
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    const int pid = tid + k * OT;
-    const int qq = pid / OTT, tt = pid % OTT;
-    if (qq < nq) {
-      atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(acc[k]));
-      if (t0 + tt < T) cm[(size_t)(g.N1 + q0 + qq) * T + t0 + tt] = acc[k];
-    }
+  // per-(case, candidate) maxima, then the per-candidate max over cases
+  float* cm = w.cmax + (size_t)b * (g.N1 + nq) * T;
+  float mx = 0.f;
+  int k = 0;
+  for (int q = qg; q < nq && k < QMAX; q += OQG, ++k) {
+    const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
+    const float v = ok ? acc[k] : 0.f;
+    if (t < T) cm[(size_t)(g.N1 + q) * T + t] = v;
+    mx = fmaxf(mx, v);
   }
+  float* sMax = sN;  // reuse
+  if (tid < OTT) sMax[tid] = 0.f;
   __syncthreads();
-  for (int tt = tid; tt < OTT; tt += OT)
-    if (t0 + tt < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + tt], sMax[tt]);
+  atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(mx));
+  __syncthreads();
+  if (tid < OTT && t0 + tid < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + tid], sMax[tid]);
 }
 
 // --------------------------------------------------------------------------- k_select
@@ -529,8 +473,17 @@ void launch_single(const DevGrid& g, const Work& w, cudaStream_t s) {
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s) {
   const int nq = g.NM + g.NI;
   if (nq == 0 || g.M == 0) return;
-  dim3 grid((w.T + OTT - 1) / OTT, (nq + OQ - 1) / OQ, w.Wb);
-  k_other<<<grid, OT, 0, s>>>(g, w);
+  const size_t dyn = ((size_t)w.NTERM * OTT + 2 * (size_t)ORC * w.NTERM + 2 * (size_t)ORC * OTT) * 4;
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    max_dyn = optin;
+    cudaFuncSetAttribute(k_other, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+  }
+  dim3 grid((w.T + OTT - 1) / OTT, w.Wb);
+  k_other<<<grid, OT, dyn, s>>>(g, w);
 }
 
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {

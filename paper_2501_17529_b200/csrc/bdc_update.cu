@@ -505,6 +505,74 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
         for (int i = tid; i < tn; i += NT) w.m32[(size_t)b * T + tc + i] = s.tmax[i];
         __syncthreads();
       }
+      // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
+      // F = n0 + sum_j Lo[r][j] So[j][t]; columns formed once per task in FP64
+      const int NTM = w.NTERM;
+      if (NTM > 0) {
+        float* Lo = w.Lo + (size_t)b * M * NTM;
+        float* So = w.So + (size_t)b * NTM * T;
+        for (int idx = tid; idx < M * (g.NM + g.NI); idx += NT) {
+          const int p = idx / (g.NM + g.NI), q = idx % (g.NM + g.NI);
+          const int row = g.mon_row[p];
+          const double inv = g.inv_rating[p];
+          const bool dead = is_dead(s.dead, nd, row);
+          if (q < g.NM) {
+            const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+            float* out = Lo + (size_t)p * NTM + st;
+            if (dead || !w.mc_ok[(size_t)b * g.NM + q]) {
+              for (int j = 0; j < m; ++j) out[j] = 0.f;
+              continue;
+            }
+            int own = -1;
+            for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+            if (own >= 0) {
+              for (int j = 0; j < m; ++j) out[j] = (j == own) ? (float)(-inv) : 0.f;
+              continue;
+            }
+            double Dv[MMAX];
+            for (int i = 0; i < m; ++i) {
+              double v = g.Dm64[(size_t)(st + i) * R + row];
+              const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+              Dv[i] = v;
+            }
+            const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
+            for (int j = 0; j < m; ++j) {
+              double v = 0.0;
+              for (int i = 0; i < m; ++i) v += Dv[i] * Mi[i * m + j];
+              out[j] = (float)(v * inv);
+            }
+          } else {
+            const int qi = q - g.NM, sl = g.ic_slot[qi];
+            float* out = Lo + (size_t)p * NTM + g.NMB + 2 * qi;
+            if (dead) { out[0] = 0.f; out[1] = 0.f; continue; }
+            const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
+            const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
+            const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
+            double pa = g.P0T[(size_t)ca * R + row], pb = pa;
+            for (int j = 0; j < rt; ++j) {
+              const double bv = Bm[(size_t)j * R + row];
+              pa = fma(bv, pa_[j], pa);
+              pb = fma(bv, pb_[j], pb);
+            }
+            const double sp = g.ic_sp[qi];
+            out[0] = (float)(-sp * pa * inv);
+            out[1] = (float)(-sp * (pb - pa) * inv);
+          }
+        }
+        const uint8_t* ib = w.inj + (size_t)b * T * g.K;
+        for (int idx = tid; idx < NTM * T; idx += NT) {
+          const int j = idx / T, t = idx % T;
+          float v;
+          if (j < g.NMB) {
+            v = (float)n0_at(g, w, b, g.mb_row[j], t, rt, s.dead, nd);
+          } else {
+            const int qi = (j - g.NMB) >> 1, sl = g.ic_slot[qi];
+            v = ((j - g.NMB) & 1) == 0 ? 1.f : ((sl >= 0 && ib[(size_t)t * g.K + sl]) ? 1.f : 0.f);
+          }
+          So[idx] = v;
+        }
+      }
     }
   }
   __syncthreads();
