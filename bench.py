@@ -375,8 +375,9 @@ def run_ours(args):
         try:
             with open(tp) as fh:
                 tj = json.load(fh)
-            if tj.get("workload") == args.config:
-                traffic = tj.get("dram_bytes_per_task", 0) * B / max(1, waves)
+            pw = tj.get("per_workload", {}).get(args.config)
+            if pw:
+                traffic = pw["dram_bytes_per_task"] * B / max(1, waves)
         except (OSError, ValueError):
             traffic = None
     step_ms = elapsed_max / args.steps
