@@ -83,6 +83,7 @@ typedef struct {
   const int32_t* sc_row;     /* (N1)      */
   const int32_t* sc_order;   /* (N1)      */
   const double* sc_delta;    /* (N1)      */
+  const double* sc_dscale;   /* (N1)      max_m |D_base(mon_row[m], c)| / rating[m] */
   const double* D64;         /* (N1, R)   */
   const float* D32;          /* (M, N1)   */
   const int32_t* mc_start;   /* (NM+1)    */
@@ -140,6 +141,10 @@ typedef struct {
   float* cand_metric;        /* (B, T) FP32 screening metric per candidate, optional */
   int64_t* loadflows;        /* (1) T*(1+feasible cases) summed over feasible tasks */
   int64_t* bsdf_applications;/* (1) optional */
+  int64_t* n1_pairs;         /* (1) optional: (single case, candidate) pairs the N-1
+                                kernel evaluated; the rest were skipped by the exact
+                                dominance screen (solver.py:798-822) */
+  int32_t screen;            /* 0 = brute force every pair, 1 = exact dominance screen */
   /* timing (filled by the engine; milliseconds of device time per stage, summed over waves) */
   float stage_ms[8];
   int32_t waves;

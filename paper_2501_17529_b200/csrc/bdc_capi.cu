@@ -156,8 +156,23 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   UP(sc_row, G->N1);
   UP(sc_order, G->N1);
   UP(sc_delta, G->N1);
+  UP(sc_dscale, G->N1);
   UP(D64, (size_t)G->N1 * G->R);
-  UP(D32, (size_t)G->N1 * G->M);
+  // D_base on monitored rows, rows padded to a multiple of 4 cases so every
+  // chunk copy of the N-1 kernels is a 16-byte cp.async
+  g.N1p = (G->N1 + 3) & ~3;
+  if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
+    float* d = nullptr;
+    e = cudaMalloc((void**)&d, (size_t)g.N1p * G->M * sizeof(float));
+    if (e == cudaSuccess) {
+      o.push_back(d);
+      g.D32 = d;
+      e = cudaMemset(d, 0, (size_t)g.N1p * G->M * sizeof(float));
+      if (e == cudaSuccess)
+        e = cudaMemcpy2D(d, (size_t)g.N1p * sizeof(float), G->D32, (size_t)G->N1 * sizeof(float),
+                         (size_t)G->N1 * sizeof(float), G->M, cudaMemcpyHostToDevice);
+    }
+  }
   UP(mc_start, G->NM + 1);
   UP(mc_order, G->NM);
   UP(mb_row, G->NMB);
@@ -246,7 +261,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
   size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
   size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
-  size_t o_lf = L.add(16), o_bs = L.add(16);
+  size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)g.N1 * 4);
+  size_t o_s32 = L.add(B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
+  size_t o_top = L.add(B * (size_t)PTOP_MAX * 4), o_done = L.add(B * (size_t)g.N1);
+  size_t o_lf = L.add(32), o_bs = L.add(16);
   if (!base) return L.total;
   Work& x = *w;
   x.Wb = Wb; x.T = T; x.D = D; x.Ein = Ein; x.rs = rs; x.Cs = Cs; x.NCw = NCw;
@@ -270,7 +288,15 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.n0rel = (double*)(base + o_n0r);
   x.n1cnt = (int*)(base + o_n1c); x.n1case = (int*)(base + o_n1k); x.n1pos = (int*)(base + o_n1p);
   x.n1flow = (double*)(base + o_n1f); x.n1rel = (double*)(base + o_n1r);
-  x.lf = (unsigned long long*)(base + o_lf); x.bsdf = (unsigned long long*)(base + o_bs);
+  // counters, one 32-byte block zeroed per call: [0] loadflows [1] bsdf [2] evaluated pairs
+  x.lf = (unsigned long long*)(base + o_lf);
+  x.bsdf = x.lf + 1;
+  x.pairs = x.lf + 2;
+  (void)o_bs;
+  x.m0 = (float*)(base + o_m0); x.scale = (float*)(base + o_sc);
+  x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
+  x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
+  x.ptop = single_tile_cases(T);
   return L.total;
 }
 
@@ -336,6 +362,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   WsLease ws(s, bytes);
   if (!ws.p) return fail(BDC_ECUDA, "workspace allocation failed (" + std::to_string(bytes) + " bytes)");
   carve(g, (int)Wb, T, D, Ein, rs, ws.p, &w);
+  w.screen = bt->screen ? 1 : 0;
+  w.ranked = (w.screen && g.N1 > w.ptop) ? 1 : 0;
   CK(cudaMemsetAsync(w.lf, 0, 32, st));
 
   const int nwaves = (int)((B + Wb - 1) / Wb);
@@ -365,18 +393,20 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
+    // stage_ms: 0 h2d, 1 update (+ fused N-0, screen data), 2 multi/injection N-1,
+    // 3 single N-1 (top tile + screened sweep), 4 select, 5 (unused), 6 report, 7 d2h
     launch_update(g, s->cfg, x, st);
-    cudaEventRecord(E[2], st);  // (N-0 contraction is fused into the update kernel's epilogue)
-    cudaEventRecord(E[3], st);
-    launch_single(g, x, st);
-    cudaEventRecord(E[4], st);
+    cudaEventRecord(E[2], st);
     launch_other(g, x, st);
-    cudaEventRecord(E[5], st);
+    cudaEventRecord(E[3], st);
+    launch_single(g, s->cfg, x, st);
+    cudaEventRecord(E[4], st);
     launch_select(g, s->cfg, x, st);
+    cudaEventRecord(E[5], st);
     cudaEventRecord(E[6], st);
     launch_report(g, s->cfg, x, st);
     cudaEventRecord(E[7], st);
-    launches += kernels_per_wave(g);
+    launches += kernels_per_wave(g, x);
     err = cudaGetLastError();
     if (err != cudaSuccess) break;
     // outputs
@@ -410,8 +440,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     cudaEventRecord(E[8], st);
     err = e2;
   }
-  unsigned long long counters[2] = {0, 0};
-  if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 16, cudaMemcpyDeviceToHost, st);
+  unsigned long long counters[4] = {0, 0, 0, 0};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 32, cudaMemcpyDeviceToHost, st);
   cudaError_t es = cudaStreamSynchronize(st);
   if (err == cudaSuccess) err = es;
   if (err == cudaSuccess) {
@@ -420,7 +450,6 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
       for (int k = 0; k < 8; ++k) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, E[k], E[k + 1]) == cudaSuccess) {
-          // stage_ms: 0 h2d, 1 update, 2 n0, 3 single N-1, 4 other N-1, 5 select, 6 report, 7 d2h
           bt->stage_ms[k] += ms;
         }
       }
@@ -430,6 +459,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (err != cudaSuccess) return fail(BDC_ECUDA, std::string("bdc_solve: ") + cudaGetErrorString(err));
   if (bt->loadflows) *bt->loadflows = (int64_t)counters[0];
   if (bt->bsdf_applications) *bt->bsdf_applications = (int64_t)counters[1];
+  if (bt->n1_pairs) *bt->n1_pairs = (int64_t)counters[2];
   bt->waves = nwaves;
   bt->kernel_launches = launches;
   return BDC_OK;

@@ -21,12 +21,17 @@ constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors
 // path's observed error is ~1e-6 (tests: <= 1e-5 enforced), so 1e-3 is a
 // >= 100x safety factor; a wider margin only costs report time.
 constexpr float SCREEN_EPS = 1e-3f;
+constexpr int PTOP_MAX = 256;             // largest case tile of the single-branch sweep
+
+// Case-tile width of the single-branch sweep for T candidates (bdc_single.cu).
+inline int single_tile_cases(int T) { return T >= 48 ? 64 : (T >= 24 ? 128 : 256); }
 
 // Grid tables, device-resident for the session lifetime.
 struct DevGrid {
   int R, C0, M, S, E, K, N1, NM, NMB, NI, NC, NBR, static_col;
+  int N1p;  // row stride of D32 (N1 rounded up to a multiple of 4)
   const double *P0, *P0T, *f0, *p_base, *rating, *inv_rating, *sub_elem_b, *slot_sp;
-  const double *sc_delta, *D64, *Dm64, *ic_sp;
+  const double *sc_delta, *sc_dscale, *D64, *Dm64, *ic_sp;
   const float* D32;
   const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;
   const int *sub_elem_row, *slot_sub, *slot_col, *sc_row, *sc_order, *mc_start, *mc_order;
@@ -68,7 +73,18 @@ struct Work {
   double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
-  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate)
+  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate); single
+                  //                   cases are filled for the winner column only
+  float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
+  float* scale;   // (Wb, N1)      FP32 max_r |LODF(r,c)|/rating_r (dominance-screen bound)
+  unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
+  int screen;     // 1 = exact dominance screen on
+  int ptop;       // cases evaluated first (the top tile by screening bound)
+  int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
+  float* s32;     // (Wb, N1, T)   n0[r_c][t] (pre-outage flow of each single case), FP32
+  uint32_t* bkey; // (Wb, N1)      max_t bound(c, t) as float bits (ranking key)
+  int* top;       // (Wb, ptop)    the ptop cases with the largest bound, ascending index
+  uint8_t* done;  // (Wb, N1)      1 if the case is in top (evaluated in the first pass)
   // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j]
   // (term j of multi case q at mc_start[q]+i, of injection case qi at NMB+2qi+{0,1})
   float* Lo;      // (Wb, M, NTERM)  correction columns / rating on monitored rows
@@ -179,15 +195,37 @@ __device__ __forceinline__ double n0_at(const DevGrid& g, const Work& w, int b, 
   return v;
 }
 
+// cp.async helpers (global -> shared, zero-filling when !ok).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// 4-byte async copy global->shared; src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp4(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
-void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
-void launch_single(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_topk(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s);
-int kernels_per_wave(const DevGrid& g);
+int kernels_per_wave(const DevGrid& g, const Work& w);
 
 }  // namespace bdc

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
       for (int ci = tid; ci < ncase; ci += RT) {
         if (!feasible_case(ci)) continue;
         const float v = cm[(size_t)ci * T];
+        if (v < 0.f) continue;  // screened-out pair: only an upper bound is known
         if (!(v < pv || (v == pv && ci > pi))) continue;
         if (better(v, ci, br, bp)) { br = v; bp = ci; }
       }
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
   if (tid == 0) sNCand = 0;
   __syncthreads();
   for (int ci = tid; ci < ncase; ci += RT) {
-    if (feasible_case(ci) && cm[(size_t)ci * T] >= theta) {
+    if (feasible_case(ci) && fabsf(cm[(size_t)ci * T]) >= theta) {
       const int p = atomicAdd(&sNCand, 1);
       if (p < CAND_CAP) sCand[p] = ci;
     }
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
   LaneTop<KC> lt;
   for (int li = wid; li < nloop; li += RW) {
     const int ci = listed ? sCand[li] : li;
-    if (!listed && !(feasible_case(ci) && cm[(size_t)ci * T] >= theta)) continue;
+    if (!listed && !(feasible_case(ci) && fabsf(cm[(size_t)ci * T]) >= theta)) continue;
     int order, kind = 0, q = ci;
     if (ci < g.N1) {
       order = g.sc_order[ci];
@@ -442,8 +443,11 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
   k_probe<<<grid, 256, 0, s>>>(g, w, n0, n1, ok);
 }
 
-int kernels_per_wave(const DevGrid& g) {
-  return 3 + (g.N1 > 0 && g.M > 0) + (g.NM + g.NI > 0 && g.M > 0);
+int kernels_per_wave(const DevGrid& g, const Work& w) {
+  const bool single = g.N1 > 0 && g.M > 0;
+  // update, select, report (+ single: [scale, top-k,] top tile, screened sweep) (+ other)
+  return 3 + (single ? 1 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
+         (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

@@ -502,7 +502,10 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
           atomicMax(&s.tmax[t - tc], __float_as_uint(fabsf(sc)));
         }
         __syncthreads();
-        for (int i = tid; i < tn; i += NT) w.m32[(size_t)b * T + tc + i] = s.tmax[i];
+        for (int i = tid; i < tn; i += NT) {
+          w.m32[(size_t)b * T + tc + i] = s.tmax[i];
+          w.m0[(size_t)b * T + tc + i] = __uint_as_float(s.tmax[i]);
+        }
         __syncthreads();
       }
       // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
@@ -573,6 +576,26 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
           So[idx] = v;
         }
       }
+      __syncthreads();
+      // ---- pre-outage flow s(c,t) = n0[r_c][t] of every single case (FP32), read by the
+      // dominance-screen passes and the N-1 sweep (solver.py:612-613, 815) ------------
+      if (g.N1 > 0 && M > 0) {
+        const int lane = tid & 31, wid = tid >> 5;
+        float* s32 = w.s32 + (size_t)b * g.N1 * T;
+        for (int c = wid; c < g.N1; c += NW) {
+          const int rowc = g.sc_row[c];
+          const bool live = w.sc_ok[(size_t)b * g.N1 + c] && !is_dead(s.dead, nd, rowc);
+          for (int t = lane; t < T; t += 32) {
+            float sv = 0.f;
+            if (live) {
+              double v = g.f0[rowc];
+              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + rowc], Y[(size_t)j * T + t], v);
+              sv = (float)v;
+            }
+            s32[(size_t)c * T + t] = sv;
+          }
+        }
+      }
     }
   }
   __syncthreads();
@@ -593,8 +616,80 @@ done:
   }
 }
 
+// The ptop single cases with the largest screening bound bkey_c (the cases the
+// reference's metric_first visits first, solver.py:818): one CTA per task, radix
+// select on the key bits, ties resolved toward the lower case index.
+__global__ void __launch_bounds__(NT) k_topk(DevGrid g, Work w) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (w.status[b] != 0) return;
+  __shared__ int hist[256];
+  __shared__ int wcnt[NW];
+  __shared__ int sel_digit, sel_above, ntop, ntie;
+  const int N1 = g.N1;
+  const uint32_t* key = w.bkey + (size_t)b * N1;
+  const int P = min(w.ptop, N1);
+  uint32_t prefix = 0, mask = 0;
+  int need = P;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < N1; c += NT) {
+      const uint32_t k = key[c];
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0, d = 255;
+      for (; d > 0; --d) {
+        if (acc + hist[d] >= need) break;
+        acc += hist[d];
+      }
+      sel_digit = d;
+      sel_above = acc;
+    }
+    __syncthreads();
+    need -= sel_above;
+    prefix |= (uint32_t)sel_digit << shift;
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  // prefix = the P-th largest key: every key above it is taken, then `need` ties in index order
+  uint8_t* done = w.done + (size_t)b * N1;
+  int* top = w.top + (size_t)b * w.ptop;
+  if (tid == 0) { ntop = 0; ntie = 0; }
+  __syncthreads();
+  for (int c0 = 0; c0 < N1; c0 += NT) {
+    const int c = c0 + tid;
+    const uint32_t k = c < N1 ? key[c] : 0u;
+    const bool tie = c < N1 && k == prefix;
+    int total;
+    const int pos = block_rank(tie, wcnt, total);
+    const bool take = c < N1 && (k > prefix || (tie && ntie + pos < need));
+    if (c < N1) done[c] = take ? 1 : 0;
+    __syncthreads();
+    if (tid == 0) ntie += total;
+    __syncthreads();
+  }
+  for (int c0 = 0; c0 < N1; c0 += NT) {
+    const int c = c0 + tid;
+    const bool take = c < N1 && done[c];
+    int total;
+    const int pos = block_rank(take, wcnt, total);
+    if (take) top[ntop + pos] = c;
+    __syncthreads();
+    if (tid == 0) ntop += total;
+    __syncthreads();
+  }
+  for (int i = ntop + tid; i < w.ptop; i += NT) top[i] = -1;
+}
+
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t st) {
   k_update<<<w.Wb, NT, 0, st>>>(g, c, w);
+}
+
+void launch_topk(const DevGrid& g, const Work& w, cudaStream_t st) {
+  if (g.N1 == 0 || g.M == 0) return;
+  k_topk<<<w.Wb, NT, 0, st>>>(g, w);
 }
 
 }  // namespace bdc

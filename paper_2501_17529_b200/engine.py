@@ -51,7 +51,7 @@ class _Grid(ctypes.Structure):
         for n in (
             "P0", "P0T", "row_from", "row_to", "branch_row", "f0", "p_base", "mon_row", "rating",
             "row_mon_pos", "sub_col", "sub_count", "sub_elem_row", "sub_elem_b", "slot_sub",
-            "slot_col", "slot_sp", "sc_row", "sc_order", "sc_delta", "D64", "D32", "mc_start",
+            "slot_col", "slot_sp", "sc_row", "sc_order", "sc_delta", "sc_dscale", "D64", "D32", "mc_start",
             "mc_order", "mb_row", "Dm64", "ic_slot", "ic_col", "ic_sp", "ic_order",
         )
     ]
@@ -100,6 +100,8 @@ class _Batch(ctypes.Structure):
         ("cand_metric", _P),
         ("loadflows", _P),
         ("bsdf_applications", _P),
+        ("n1_pairs", _P),
+        ("screen", ctypes.c_int32),
         ("stage_ms", ctypes.c_float * 8),
         ("waves", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
@@ -180,6 +182,9 @@ class Engine:
         self.base = base
         self.config = config
         self.device = device
+        # exact dominance screen of the reference's metric_first mode
+        # (solver.py:798-822); False brute-forces every (case, candidate) pair
+        self.screen = True
         self.tables = tb = build_tables(grid, base)
         if tb.E > MAX_ELEMENTS:
             raise ValidationError(f"substations with more than {MAX_ELEMENTS} branch elements")
@@ -228,6 +233,7 @@ class Engine:
         g.sc_row = arr("sc_row", tb.sc_row, np.int32)
         g.sc_order = arr("sc_order", tb.sc_order, np.int32)
         g.sc_delta = arr("sc_delta", tb.sc_delta, np.float64)
+        g.sc_dscale = arr("sc_dscale", tb.sc_dscale, np.float64)
         g.D64 = arr("D64", tb.D64, np.float64)
         g.D32 = arr("D32", tb.D32, np.float32)
         g.mc_start = arr("mc_start", tb.mc_start, np.int32)
@@ -374,10 +380,14 @@ class Engine:
         for name, t in outputs.items():
             setattr(bt, name, ctypes.c_void_p(t.data_ptr()))
         lf = loadflows if loadflows is not None else np.zeros(1, dtype=np.int64)
+        pairs = np.zeros(1, dtype=np.int64)
         bt.loadflows = _ptr(lf)
+        bt.n1_pairs = _ptr(pairs)
+        bt.screen = int(self.screen)
         rc = self.lib.bdc_solve(self.handle, ctypes.byref(bt))
         if rc != 0:
             raise EngineUnavailable(f"bdc_solve failed ({rc}): {_err(self.lib)}")
+        self.last_pairs = int(pairs[0])
         return [float(x) for x in bt.stage_ms], int(bt.waves), int(bt.kernel_launches), int(lf[0])
 
     def probe_flows(self, splits_row: np.ndarray, discos_row: np.ndarray, inj_rows: np.ndarray):
@@ -431,6 +441,7 @@ class BatchOutput:
         self.cand_metric = np.zeros((B, T), dtype=np.float32) if want_candidates else None
         self._lf = np.zeros(1, dtype=np.int64)
         self._bsdf = np.zeros(1, dtype=np.int64)
+        self._pairs = np.zeros(1, dtype=np.int64)
         self.stage_ms = [0.0] * 8
         self.waves = 0
         self.kernel_launches = 0
@@ -445,6 +456,8 @@ class BatchOutput:
         bt.cand_metric = _ptr(self.cand_metric)
         bt.loadflows = _ptr(self._lf)
         bt.bsdf_applications = _ptr(self._bsdf)
+        bt.n1_pairs = _ptr(self._pairs)
+        bt.screen = int(self.engine.screen)
 
     def finish(self, bt: _Batch) -> None:
         self.stage_ms = [float(x) for x in bt.stage_ms]
@@ -470,6 +483,12 @@ class BatchOutput:
     @property
     def bsdf_applications(self) -> int:
         return int(self._bsdf[0])
+
+    @property
+    def n1_pairs(self) -> int:
+        """(single case, candidate) pairs the N-1 sweep evaluated (the rest were
+        skipped by the exact dominance screen)."""
+        return int(self._pairs[0])
 
     # ------------------------------------------------------------ decoding
     def islanded_orders(self, b: int) -> list[int]:

@@ -223,6 +223,7 @@ class BaseTables:
     sc_row: np.ndarray          # (N1,) i32
     sc_order: np.ndarray        # (N1,) i32
     sc_delta: np.ndarray        # (N1,) f64 D_base(r_c, c)
+    sc_dscale: np.ndarray       # (N1,) f64 max_m |D_base(mon_row[m], c)| / rating[m]
     D64: np.ndarray             # (N1, R) f64 D_base columns, case-major
     D32: np.ndarray             # (M, N1) f32 D_base on monitored rows, row-major
     # multi-branch cases (NM cases, NMB = total member branches)
@@ -267,6 +268,19 @@ class BaseTables:
     @property
     def NI(self) -> int:
         return len(self.ic_slot)
+
+
+def _dscale(D64: np.ndarray, mon_row: np.ndarray, rating: np.ndarray) -> np.ndarray:
+    """Per single case, max over monitored rows of |D_base|/rating (a session constant
+    of the device dominance screen's analytic bound), in row blocks to bound memory."""
+    out = np.zeros(D64.shape[0])
+    if D64.size == 0 or len(mon_row) == 0:
+        return out
+    inv = 1.0 / rating
+    for c0 in range(0, D64.shape[0], 1024):
+        blk = np.abs(D64[c0 : c0 + 1024][:, mon_row]) * inv[None, :]
+        out[c0 : c0 + 1024] = blk.max(axis=1)
+    return out
 
 
 def build_tables(grid: Grid, base: PtdfMatrix) -> BaseTables:
@@ -413,6 +427,7 @@ def build_tables(grid: Grid, base: PtdfMatrix) -> BaseTables:
         sc_row=sc_row_a,
         sc_order=np.array(sc_order, dtype=np.int32),
         sc_delta=np.ascontiguousarray(sc_delta),
+        sc_dscale=_dscale(D64, mon_row, grid.ratings[mon] if len(mon) else np.zeros(0)),
         D64=D64,
         D32=D32,
         mc_start=np.array(mc_start, dtype=np.int32),

@@ -193,3 +193,30 @@ def test_library_solve_batch_matches_session(sessions):
         if pr.feasible:
             assert abs(doc["metric"] - pr.metric) <= TAU
             assert doc["best_injection"] < len(t.injection_sets)
+
+
+@pytest.mark.parametrize("name", ["fixture_a", "fixture_b", "case300", "g14", "g118"])
+def test_dominance_screen_is_exact(name, sessions):
+    """The device dominance screen (solver.py:798-822) never changes a result."""
+    case = next(c for c in CASES if c["name"] == name)
+    sess = sessions(case)
+    arr, _ = load_case(name)
+    eng = sess.engine
+    outs = {}
+    for flag in (True, False):
+        eng.screen = flag
+        outs[flag] = eng.solve(arr["splits"], arr["disconnections"], arr["injection_sets"], want_candidates=True)
+    eng.screen = True
+    on, off = outs[True], outs[False]
+    assert np.array_equal(on.best, off.best)
+    assert np.array_equal(on.metric, off.metric, equal_nan=True)
+    assert on.reports() == off.reports()
+    pen = sess.config.islanding_penalty
+    for b in range(len(on.best)):
+        if not on.feasible[b]:
+            continue
+        a, c = on.cand_metric[b], off.cand_metric[b]
+        if on.n_islanded[b] > 0:
+            a, c = np.maximum(a, pen), np.maximum(c, pen)
+        assert np.array_equal(a, c), b
+    assert on.n1_pairs <= off.n1_pairs

@@ -46,8 +46,8 @@ def test_struct_layouts_match_header():
     """ctypes mirrors of BdcGrid/BdcConfig/BdcBatch have the C sizes (compiled probe)."""
     from paper_2501_17529_b200 import engine
 
-    # 13 int32 + 30 pointers, padded to 8
-    assert ctypes.sizeof(engine._Grid) == 13 * 4 + 4 + 30 * 8
+    # 13 int32 + 31 pointers, padded to 8
+    assert ctypes.sizeof(engine._Grid) == 13 * 4 + 4 + 31 * 8
     assert ctypes.sizeof(engine._Config) == 32
     assert engine._Batch.stage_ms.offset % 4 == 0
 
