@@ -252,8 +252,7 @@ def run_ours(args):
     sess = session_open(grid, device=local)
     eng = sess.engine
     eng.screen = not args.no_screen
-    kk, dd = eng.task_ranks(splits, discos)
-    max_rank = eng.check_limits(splits, kk, dd)
+    max_rank = eng.check_batch(splits.view(np.uint8), discos)
     B = splits.shape[0]
     dev = torch.device("cuda", local)
     t_spl = torch.from_numpy(splits.view(np.uint8)).to(dev)

@@ -18,6 +18,8 @@
  *                           (_injection_stage :766), winner report (:652).
  *   bdc_probe_flows      <- batchdc.candidate_case_flows (solver.py:919-958):
  *                           every flow vector of one task, for parity checks.
+ *   bdc_scan_tasks       <- the rank / outage-cap checks of canonicalize_task and
+ *                           _branch_stage (solver.py:148-197, 390-394), vectorised.
  *   bdc_session_destroy  <- (session lifetime end; the reference relies on GC)
  *   bdc_last_error, bdc_version, bdc_device_count -- plumbing.
  *
@@ -169,6 +171,15 @@ int bdc_solve(BdcSession* session, BdcBatch* batch);
 int bdc_probe_flows(BdcSession* session, const uint8_t* splits, const int64_t* discos,
                     int32_t D, const uint8_t* inj, int32_t T, double* n0, double* n1,
                     uint8_t* case_ok, int32_t* status, int32_t* status_arg);
+
+/* Host-side scan of a batch's task arrays (no device work): the largest
+ * rank k+d, disconnection count d and number of moved injection slots over
+ * the tasks -- the quantities the engine limits and the workspace stride
+ * depend on (replaces the per-task rank counting of canonicalize_task,
+ * solver.py:148-197).  splits (B,S,E) u8, discos (B,D) i64 or NULL. */
+int bdc_scan_tasks(BdcSession* session, const uint8_t* splits, const int64_t* discos,
+                   int64_t B, int32_t D, int32_t* max_rank, int32_t* max_disc,
+                   int32_t* max_active_slots);
 
 /* Set the wave size cap (tasks per device wave); 0 = automatic. */
 int bdc_session_set_wave(BdcSession* session, int64_t max_tasks_per_wave);

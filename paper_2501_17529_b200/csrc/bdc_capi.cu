@@ -1,6 +1,7 @@
 // bdc_capi.cu -- the C ABI (include/bdc.h): session lifetime, wave scheduling,
 // host<->device staging.  No exceptions cross the boundary; every entry point
 // returns a status and leaves a thread-local message for bdc_last_error().
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -52,6 +53,7 @@ struct BdcSession {
   std::vector<void*> owned;
   int64_t wave_cap = 0;
   size_t total_mem = 0;
+  std::vector<int32_t> sub_count, slots_per_sub;  // host copies for bdc_scan_tasks
   // cached wave workspaces (one per concurrent call), reused across calls
   std::mutex ws_mu;
   std::vector<std::pair<char*, size_t>> ws_free;
@@ -131,6 +133,9 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   g.R = G->R; g.C0 = G->C0; g.M = G->M; g.S = G->S; g.E = G->E; g.K = G->K;
   g.N1 = G->N1; g.NM = G->NM; g.NMB = G->NMB; g.NI = G->NI; g.NC = G->NC; g.NBR = G->NBR;
   g.static_col = G->static_col;
+  g.MT = 2;
+  for (int q = 0; q < G->NM; ++q)
+    while (g.MT < G->mc_start[q + 1] - G->mc_start[q]) g.MT *= 2;
   std::vector<double> inv(G->M);
   for (int i = 0; i < G->M; ++i) inv[i] = 1.0 / G->rating[i];
   cudaError_t e = cudaSuccess;
@@ -188,6 +193,10 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
     delete s;
     return fail(BDC_ECUDA, std::string("session upload: ") + cudaGetErrorString(e));
   }
+  s->sub_count.assign(G->sub_count, G->sub_count + G->S);
+  s->slots_per_sub.assign(G->S, 0);
+  for (int k = 0; k < G->K; ++k)
+    if (G->slot_sp[k] != 0.0 && G->slot_sub[k] >= 0 && G->slot_sub[k] < G->S) ++s->slots_per_sub[G->slot_sub[k]];
   s->cfg.kc = C->topk_per_case;
   s->cfg.kg = C->topk_global;
   s->cfg.policy = C->islanding_policy;
@@ -216,6 +225,32 @@ int bdc_session_destroy(BdcSession* s) {
   return BDC_OK;
 }
 
+int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, int64_t B, int32_t D,
+                   int32_t* max_rank, int32_t* max_disc, int32_t* max_active) {
+  if (!s || (B > 0 && !splits && s->g.S > 0) || (D > 0 && B > 0 && !discos))
+    return fail(BDC_EINVAL, "null argument");
+  const int S = s->g.S, E = s->g.E > 0 ? s->g.E : 1;
+  int32_t mr = 0, md = 0, ma = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    int k = 0, act = 0, d = 0;
+    const uint8_t* sp = splits + (size_t)b * S * E;
+    for (int si = 0; si < S; ++si) {
+      const uint8_t* e = sp + (size_t)si * E;
+      bool any = false;
+      for (int j = 0; j < E; ++j) any |= e[j] != 0;
+      if (any) { ++k; act += s->slots_per_sub[si]; }
+    }
+    for (int i = 0; i < D; ++i) d += discos[(size_t)b * D + i] >= 0;
+    mr = std::max(mr, k + d);
+    md = std::max(md, d);
+    ma = std::max(ma, act);
+  }
+  if (max_rank) *max_rank = mr;
+  if (max_disc) *max_disc = md;
+  if (max_active) *max_active = ma;
+  return BDC_OK;
+}
+
 int bdc_session_set_wave(BdcSession* s, int64_t cap) {
   if (!s) return fail(BDC_EINVAL, "null session");
   s->wave_cap = cap;
@@ -227,7 +262,7 @@ int bdc_session_set_wave(BdcSession* s, int64_t cap) {
 namespace {
 
 struct Layout {
-  size_t off[64];
+  size_t off[128];
   int n = 0;
   size_t total = 0;
   size_t add(size_t bytes) {
@@ -255,7 +290,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_Y = L.add(B * rs * T * 8), o_n0s = L.add(B * g.M * T * 4);
   size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
   size_t o_cmax = L.add(B * (size_t)(g.N1 + g.NM + g.NI) * T * 4);
-  const size_t NTERM = (size_t)g.NMB + 2 * (size_t)g.NI;
+  const size_t NTERM = ((size_t)g.NM + g.NI) * g.MT;
   size_t o_Lo = L.add(B * (size_t)g.M * NTERM * 4), o_So = L.add(B * NTERM * T * 4);
   size_t o_met = L.add(B * 8), o_best = L.add(B * 8), o_fe = L.add(B);
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
@@ -264,6 +299,13 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)g.N1 * 4);
   size_t o_s32 = L.add(B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
   size_t o_top = L.add(B * (size_t)PTOP_MAX * 4), o_done = L.add(B * (size_t)g.N1);
+  const SweepShape sh = sweep_shape(T);
+  const int nct = (g.N1 + sh.CPT * sh.TX - 1) / (sh.CPT * sh.TX), ntt = (T + sh.TPT * sh.TY - 1) / (sh.TPT * sh.TY);
+  const int nslot = 1 + (g.N1 + RCW - 1) / RCW;
+  size_t o_alive = L.add(B * (size_t)nct * ntt * SWEEP_WARPS);
+  size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4);
+  size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
+  size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
   size_t o_lf = L.add(32), o_bs = L.add(16);
   if (!base) return L.total;
   Work& x = *w;
@@ -297,6 +339,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = single_tile_cases(T);
+  x.alive = (uint8_t*)(base + o_alive); x.nct = nct; x.ntt = ntt;
+  x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.nslot = nslot;
+  x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);
+  x.pflow = (double*)(base + o_pf); x.prel = (double*)(base + o_pr); x.pmax = (double*)(base + o_pm);
   return L.total;
 }
 

@@ -23,13 +23,32 @@ constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors
 constexpr float SCREEN_EPS = 1e-3f;
 constexpr int PTOP_MAX = 256;             // largest case tile of the single-branch sweep
 
-// Case-tile width of the single-branch sweep for T candidates (bdc_single.cu).
-inline int single_tile_cases(int T) { return T >= 48 ? 64 : (T >= 24 ? 128 : 256); }
+// Thread layout of the single-branch sweep for T candidates (bdc_single.cu): a CTA of
+// TX*TY = 256 threads covers NC = CPT*TX cases x TT = TPT*TY candidates; thread
+// (tx, ty) = tid % TX, tid / TX owns CPT cases x TPT candidates.  The winner report
+// uses the same map to find the warp that evaluated a (case, candidate) pair.
+struct SweepShape {
+  int CPT, TPT, TX, TY;
+};
+__host__ __device__ inline SweepShape sweep_shape(int T) {
+  if (T >= 96) return {2, 16, 32, 8};  // 64 cases x 128 candidates
+  if (T >= 48) return {2, 8, 32, 8};   // 64 x 64
+  if (T >= 24) return {4, 4, 32, 8};   // 128 x 32
+  if (T >= 12) return {4, 4, 64, 4};   // 256 x 16
+  return {4, 2, 64, 4};                // 256 x 8
+}
+inline int single_tile_cases(int T) {
+  const SweepShape s = sweep_shape(T);
+  return s.CPT * s.TX;
+}
+constexpr int SWEEP_WARPS = 8;  // warps per sweep CTA (256 threads)
+constexpr int RCW = 128;        // single cases per CTA of the winner report sweep
 
 // Grid tables, device-resident for the session lifetime.
 struct DevGrid {
   int R, C0, M, S, E, K, N1, NM, NMB, NI, NC, NBR, static_col;
   int N1p;  // row stride of D32 (N1 rounded up to a multiple of 4)
+  int MT;   // correction-term slots per multi/injection case (max branches, pow2 >= 2)
   const double *P0, *P0T, *f0, *p_base, *rating, *inv_rating, *sub_elem_b, *slot_sp;
   const double *sc_delta, *sc_dscale, *D64, *Dm64, *ic_sp;
   const float* D32;
@@ -73,8 +92,11 @@ struct Work {
   double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
-  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate); single
-                  //                   cases are filled for the winner column only
+  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate), valid
+                  //                   where evaluated (see alive); other cases always
+  uint8_t* alive; // (Wb, nct, ntt, SWEEP_WARPS) 1 if that warp of the screened sweep
+                  //                   evaluated its pairs (else they were dominated)
+  int nct, ntt;   // case / candidate tiles of the sweep
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
   float* scale;   // (Wb, N1)      FP32 max_r |LODF(r,c)|/rating_r (dominance-screen bound)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
@@ -85,12 +107,21 @@ struct Work {
   uint32_t* bkey; // (Wb, N1)      max_t bound(c, t) as float bits (ranking key)
   int* top;       // (Wb, ptop)    the ptop cases with the largest bound, ascending index
   uint8_t* done;  // (Wb, N1)      1 if the case is in top (evaluated in the first pass)
-  // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j]
-  // (term j of multi case q at mc_start[q]+i, of injection case qi at NMB+2qi+{0,1})
-  float* Lo;      // (Wb, M, NTERM)  correction columns / rating on monitored rows
-  float* So;      // (Wb, NTERM, T)  per-candidate multipliers
-  int NTERM;      // NMB + 2 NI
+  // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j],
+  // MT term slots per case q (multi: one per outaged branch, injection: 2), zero-padded
+  float* Lo;      // (Wb, M, NQ, MT)  correction columns / rating on monitored rows
+  float* So;      // (Wb, NQ, MT, T)  per-candidate multipliers
+  int NTERM;      // NQ * MT, NQ = NM + NI
   double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
+  // winner report: listed cases and per-slot partial top-kg lists
+  int* rlist;     // (Wb, N1)      single cases the FP64 report must visit, ascending
+  int* rcnt;      // (Wb)          their number
+  int nslot;      // 1 + ceil(N1 / RCW) partial lists per task
+  int* pcase;     // (Wb, nslot, KMAX) contingency order of each partial entry
+  int* ppos;      // (Wb, nslot, KMAX) monitored position
+  double* pflow;  // (Wb, nslot, KMAX)
+  double* prel;   // (Wb, nslot, KMAX)  rel = -1 marks an empty entry
+  double* pmax;   // (Wb, nslot)     FP64 max loading over the slot's cases
   // outputs (device)
   double* metric; int64_t* best; uint8_t* feasible;
   int* n0cnt; int* n0pos; double* n0flow; double* n0rel;

@@ -1,121 +1,145 @@
-// bdc_flows.cu -- Kernels 2-4: N-0 contraction, fused N-1 screening, winner selection.
+// bdc_flows.cu -- the multi-branch / injection N-1 stage and winner selection.
 //
-//   k_n0      N-0 flows of every candidate on the monitored rows,
-//             n0 = f0 + B'' y_t (FP64, the rank-r form of `_candidate_base_flows`,
-//             solver.py:575-595), written once as FP32 n0/rating (the only
-//             per-task tensor the N-1 stage streams) and folded into the metric.
-//   k_single  THE hot kernel.  Single-branch N-1 for every (case, candidate)
-//             pair of a task, fused: forms LODF columns on the fly from the
-//             shared base D_base and the task's rank-r factors
-//             (L = (D_base + B'' W^T) / den, solver.py:474-485), applies the
-//             outage update F = n0 + L n0[r_c] (solver.py:612-613), takes
-//             |F|/rating and max-reduces over monitored rows and cases into
-//             the per-candidate metric (solver.py:625-631, agg_m :235-252).
-//             The (case x candidate x branch) tensor never leaves registers;
-//             row chunks of n0/rating and D_base stream through shared memory
-//             with cp.async double buffering.
-//   k_other   multi-branch (MODF, solver.py:614-618) and injection
-//             (solver.py:619-622) contingencies of one task, same fusion.
+//   k_other   multi-branch (MODF, solver.py:614-618) and injection (solver.py:619-622)
+//             contingencies of every candidate, fused: F = n0 + sum_j Lo So,
+//             |F|/rating, max over monitored rows, per-(case, candidate) maxima for the
+//             report and the per-candidate max folded into the metric (agg_m,
+//             solver.py:235-252).  Nothing of size (case x candidate x branch) is written.
 //   k_select  islanding penalty floor and first-index argmin (solver.py:804-823).
+//
+// The single-branch N-1 stage (the hot path) is bdc_single.cu; the N-0 contraction
+// is fused into the update kernel (bdc_update.cu).
 #include "bdc_device.cuh"
 
 namespace bdc {
 
-namespace {
-
-
-}  // namespace
-
 // ---------------------------------------------------------------------------- k_other
-// One CTA per (task, candidate tile): every multi-branch and injection case of
-// the task, FP32 like k_single.  The update kernel already laid the cases out
-// as correction terms, F = n0 + sum_j Lo[r][j] So[j][t] (MODF columns with the
-// pre-outage flows of the outaged rows, or the injection column with 1 and the
-// candidate's slot bit), so this is a pure stream over monitored-row chunks.
+// Multi-branch (MODF, solver.py:614-618) and injection (solver.py:619-622)
+// contingencies of one task, FP32 like k_single.  The update kernel laid every
+// case out as MT zero-padded correction terms, F = n0 + sum_j Lo[r][q][j] So[q][j][t]
+// (MODF columns with the pre-outage flows of the outaged rows, or the injection
+// column with 1 and the candidate's slot bit), so this is a pure stream over
+// monitored-row chunks.  CTA = (task, tile of 32*TPT candidates); lane = TPT
+// consecutive candidates, warp = up to QW cases (warp-uniform, so the Lo reads are
+// shared-memory broadcasts); the multipliers So stay in registers.
 namespace {
-constexpr int OT = 256;   // threads
-constexpr int OTT = 64;   // candidates per CTA
-constexpr int ORC = 32;   // monitored rows per chunk
-constexpr int OQG = OT / OTT;  // case groups
+constexpr int OT = 256;        // threads
+constexpr int OW = OT / 32;    // warps
+constexpr int ORC = 32;        // monitored rows per chunk
 }  // namespace
 
+template <int MT, int QW, int TPT>
 __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
-  const int b = blockIdx.y, tid = threadIdx.x, t0 = blockIdx.x * OTT;
+  constexpr int TT = 32 * TPT, QB = OW * QW;  // candidates per CTA, cases per batch
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int t0 = blockIdx.x * TT;
   if (w.status[b] != 0) return;
-  const int T = w.T, M = g.M, NTM = w.NTERM, nq = g.NM + g.NI;
+  const int T = w.T, M = g.M, NQ = g.NM + g.NI;
   extern __shared__ __align__(16) float osm[];
-  float* sS = osm;                        // [NTM][OTT]
-  float* sLo = sS + NTM * OTT;            // [2][ORC][NTM]
-  float* sN = sLo + 2 * ORC * NTM;        // [2][ORC][OTT]
-  const float* Lo = w.Lo + (size_t)b * M * NTM;
+  float* sN = osm;                   // [2][ORC][TT]   n0 / rating
+  float* sL = sN + 2 * ORC * TT;     // [2][ORC][QB*MT] correction columns of the batch
+  __shared__ float sMax[TT];
+  const float* Lo = w.Lo + (size_t)b * M * NQ * MT;
   const float* n0s = w.n0s + (size_t)b * M * T;
-  const int tt = tid % OTT, qg = tid / OTT, t = t0 + tt;
-  for (int idx = tid; idx < NTM * OTT; idx += OT) {
-    const int j = idx / OTT, u = t0 + idx % OTT;
-    sS[idx] = u < T ? w.So[((size_t)b * NTM + j) * T + u] : 0.f;
-  }
-  auto issue = [&](int m0, int buf) {
-    for (int idx = tid; idx < ORC * NTM; idx += OT) {
-      const int rr = idx / NTM, j = idx % NTM, m = m0 + rr;
-      const bool ok = m < M;
-      cp4(&sLo[(buf * ORC + rr) * NTM + j], ok ? &Lo[(size_t)m * NTM + j] : Lo, ok);
-    }
-    for (int idx = tid; idx < ORC * OTT; idx += OT) {
-      const int rr = idx / OTT, u = idx % OTT, m = m0 + rr;
-      const bool ok = m < M && t0 + u < T;
-      cp4(&sN[(buf * ORC + rr) * OTT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
-    }
-    cp_commit();
-  };
-  // this thread's cases: q = qg, qg + OQG, ...; islanded multi cases are skipped
-  constexpr int QMAX = 16;
-  float acc[QMAX];
+  const float* So = w.So + (size_t)b * NQ * MT * T;
+  float* cm = w.cmax + (size_t)b * (g.N1 + NQ) * T;
+  const bool vecN = (T % 4) == 0;
+  for (int i = tid; i < TT; i += OT) sMax[i] = 0.f;
+
+  for (int qb = 0; qb < NQ; qb += QB) {
+    const int nqb = min(QB, NQ - qb), LW = nqb * MT;  // cases / Lo floats of this batch
+    float sv[QW][MT][TPT], acc[QW][TPT];
 #pragma unroll
-  for (int k = 0; k < QMAX; ++k) acc[k] = 0.f;
-  issue(0, 0);
-  const int nchunks = (M + ORC - 1) / ORC;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < nchunks) {
-      issue((ch + 1) * ORC, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+    for (int k = 0; k < QW; ++k) {
+      const int q = qb + wid + OW * k;
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int i = 0; i < TPT; ++i) {
+          const int t = t0 + lane * TPT + i;
+          sv[k][j][i] = (q < NQ && t < T) ? So[((size_t)q * MT + j) * T + t] : 0.f;
+        }
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) acc[k][i] = 0.f;
     }
-    __syncthreads();
-    const float* L = &sLo[buf * ORC * NTM];
-    const float* N = &sN[buf * ORC * OTT];
-    int k = 0;
-    for (int q = qg; q < nq && k < QMAX; q += OQG, ++k) {
-      int st, m;
-      if (q < g.NM) { st = g.mc_start[q]; m = g.mc_start[q + 1] - st; }
-      else { st = g.NMB + 2 * (q - g.NM); m = 2; }
-      float a = acc[k];
-      for (int rr = 0; rr < ORC; ++rr) {
-        float f = N[rr * OTT + tt];
-        for (int j = 0; j < m; ++j) f = fmaf(L[rr * NTM + st + j], sS[(st + j) * OTT + tt], f);
-        a = fmaxf(a, fabsf(f));
+    auto issue = [&](int m0, int buf) {
+      if (vecN) {
+        for (int idx = tid; idx < ORC * (TT / 4); idx += OT) {
+          const int rr = idx / (TT / 4), u = 4 * (idx % (TT / 4)), m = m0 + rr;
+          const bool ok = m < M && t0 + u < T;
+          cp16(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+        }
+      } else {
+        for (int idx = tid; idx < ORC * TT; idx += OT) {
+          const int rr = idx / TT, u = idx % TT, m = m0 + rr;
+          const bool ok = m < M && t0 + u < T;
+          cp4(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+        }
       }
-      acc[k] = a;
+      // LW = nqb * MT is a multiple of 2; rows of Lo are NQ*MT floats (8-byte aligned)
+      for (int idx = tid; idx < ORC * (LW / 2); idx += OT) {
+        const int rr = idx / (LW / 2), u = 2 * (idx % (LW / 2)), m = m0 + rr;
+        const bool ok = m < M;
+        cp8(&sL[(buf * ORC + rr) * QB * MT + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
+      }
+      cp_commit();
+    };
+    issue(0, 0);
+    const int nchunks = (M + ORC - 1) / ORC;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nchunks) {
+        issue((ch + 1) * ORC, buf ^ 1);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      const int rend = min(ORC, M - ch * ORC);  // zero-filled rows past M are harmless
+      (void)rend;
+#pragma unroll 4
+      for (int rr = 0; rr < ORC; ++rr) {
+        float n[TPT];
+#pragma unroll
+        for (int i = 0; i < TPT; ++i) n[i] = sN[(buf * ORC + rr) * TT + lane * TPT + i];
+#pragma unroll
+        for (int k = 0; k < QW; ++k) {
+          if (wid + OW * k >= nqb) break;  // warp-uniform
+          const float* lrow = &sL[(buf * ORC + rr) * QB * MT + (wid + OW * k) * MT];
+          float l[MT];
+#pragma unroll
+          for (int j = 0; j < MT; ++j) l[j] = lrow[j];
+#pragma unroll
+          for (int i = 0; i < TPT; ++i) {
+            float f = n[i];
+#pragma unroll
+            for (int j = 0; j < MT; ++j) f = fmaf(l[j], sv[k][j][i], f);
+            acc[k][i] = fmaxf(acc[k][i], fabsf(f));
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    // per-(case, candidate) maxima (islanded multi cases contribute 0), candidate max
+#pragma unroll
+    for (int k = 0; k < QW; ++k) {
+      const int q = qb + wid + OW * k;
+      if (q >= NQ) break;
+      const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) {
+        const int u = lane * TPT + i, t = t0 + u;
+        const float v = ok ? acc[k][i] : 0.f;
+        if (t < T) {
+          cm[(size_t)(g.N1 + q) * T + t] = v;
+          atomicMax(reinterpret_cast<unsigned*>(&sMax[u]), __float_as_uint(v));
+        }
+      }
+    }
   }
-  // per-(case, candidate) maxima, then the per-candidate max over cases
-  float* cm = w.cmax + (size_t)b * (g.N1 + nq) * T;
-  float mx = 0.f;
-  int k = 0;
-  for (int q = qg; q < nq && k < QMAX; q += OQG, ++k) {
-    const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
-    const float v = ok ? acc[k] : 0.f;
-    if (t < T) cm[(size_t)(g.N1 + q) * T + t] = v;
-    mx = fmaxf(mx, v);
-  }
-  float* sMax = sN;  // reuse
-  if (tid < OTT) sMax[tid] = 0.f;
   __syncthreads();
-  atomicMax(reinterpret_cast<unsigned*>(&sMax[tt]), __float_as_uint(mx));
-  __syncthreads();
-  if (tid < OTT && t0 + tid < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + tid], sMax[tid]);
+  for (int u = tid; u < TT; u += OT)
+    if (t0 + u < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + u], sMax[u]);
 }
 
 // --------------------------------------------------------------------------- k_select
@@ -152,20 +176,33 @@ __global__ void k_select(DevGrid g, DevCfg cfg, Work w) {
 }
 
 // ---------------------------------------------------------------------------- launches
+namespace {
+template <int MT, int QW, int TPT>
+void launch_other_t(const DevGrid& g, const Work& w, cudaStream_t s) {
+  constexpr int TT = 32 * TPT;
+  const size_t dyn = (2 * (size_t)ORC * TT + 2 * (size_t)ORC * OW * QW * MT) * sizeof(float);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_other<MT, QW, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    init = true;
+  }
+  dim3 grid((w.T + TT - 1) / TT, w.Wb);
+  k_other<MT, QW, TPT><<<grid, OT, dyn, s>>>(g, w);
+}
+template <int MT, int QW>
+void launch_other_m(const DevGrid& g, const Work& w, cudaStream_t s) {
+  if (w.T > 64) launch_other_t<MT, QW, 4>(g, w, s);
+  else if (w.T > 32) launch_other_t<MT, QW, 2>(g, w, s);
+  else launch_other_t<MT, QW, 1>(g, w, s);
+}
+}  // namespace
+
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s) {
   const int nq = g.NM + g.NI;
   if (nq == 0 || g.M == 0) return;
-  const size_t dyn = ((size_t)w.NTERM * OTT + 2 * (size_t)ORC * w.NTERM + 2 * (size_t)ORC * OTT) * 4;
-  static int max_dyn = -1;
-  if (max_dyn < 0) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    max_dyn = optin;
-    cudaFuncSetAttribute(k_other, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  }
-  dim3 grid((w.T + OTT - 1) / OTT, w.Wb);
-  k_other<<<grid, OT, dyn, s>>>(g, w);
+  if (g.MT <= 2) launch_other_m<2, 4>(g, w, s);
+  else if (g.MT <= 4) launch_other_m<4, 2>(g, w, s);
+  else launch_other_m<8, 1>(g, w, s);
 }
 
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {

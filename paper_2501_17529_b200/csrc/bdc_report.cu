@@ -1,5 +1,5 @@
-// bdc_report.cu -- Kernel 5: the winner's sparse report and FP64 metric, and the
-// flow probe used by the parity tests.
+// bdc_report.cu -- the winner's sparse report and FP64 metric (k_rsel, k_rsweep,
+// k_rmerge), and the flow probe used by the parity tests (k_probe).
 //
 // k_report re-evaluates the winning candidate only, in FP64 (metric_first's
 // second pass, PAPER step "recompute p_n0/p_n1 for t_i^*", solver.py:652-713):
@@ -20,7 +20,6 @@ namespace {
 
 constexpr int RT = 256;
 constexpr int RW = RT / 32;
-constexpr int CAND_CAP = 1024;
 
 __device__ __forceinline__ bool better(double r1, int p1, double r2, int p2) {
   return r1 > r2 || (r1 == r2 && p1 < p2);
@@ -39,16 +38,19 @@ struct LaneTop {
   }
   __device__ void insert(double r, int p, double f) {
     if (!better(r, p, rel[KC - 1], pos[KC - 1])) return;
+    // branch-free insertion (static register indices): entries the new one beats
+    // move down one slot, the first one it does not beat keeps it below
+    bool placed = false;
 #pragma unroll
     for (int i = KC - 1; i > 0; --i) {
-      if (better(r, p, rel[i - 1], pos[i - 1])) {
-        rel[i] = rel[i - 1]; pos[i] = pos[i - 1]; flow[i] = flow[i - 1];
-      } else {
-        rel[i] = r; pos[i] = p; flow[i] = f;
-        return;
-      }
+      const bool up = better(r, p, rel[i - 1], pos[i - 1]);
+      const bool put = !up && !placed;
+      rel[i] = up ? rel[i - 1] : (put ? r : rel[i]);
+      pos[i] = up ? pos[i - 1] : (put ? p : pos[i]);
+      flow[i] = up ? flow[i - 1] : (put ? f : flow[i]);
+      placed |= put;
     }
-    rel[0] = r; pos[0] = p; flow[0] = f;
+    if (!placed) { rel[0] = r; pos[0] = p; flow[0] = f; }
   }
   __device__ void pop() {
 #pragma unroll
@@ -102,10 +104,50 @@ __device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int cas
   }
 }
 
+
+// Was the (single case c, candidate t) pair evaluated by the N-1 sweep, i.e. is
+// cmax[c][t] its exact FP32 maximum?  Cases of the TOP tile always are; in the
+// screened sweep it depends on the warp that owned the pair (bdc_single.cu).
+__device__ __forceinline__ bool pair_evaluated(const DevGrid& g, const Work& w, int b, int c, int t) {
+  if (w.ranked ? w.done[(size_t)b * g.N1 + c] != 0 : c < w.ptop) return true;
+  const SweepShape sh = sweep_shape(w.T);
+  const int NC = sh.CPT * sh.TX, TT = sh.TPT * sh.TY;
+  const int ct = c / NC, tx = (c % NC) / sh.CPT, tt = t / TT, ty = (t % TT) / sh.TPT;
+  const int warp = (ty * sh.TX + tx) >> 5;
+  return w.alive[(((size_t)b * w.nct + ct) * w.ntt + tt) * SWEEP_WARPS + warp] != 0;
+}
+
+// Ordered block-wide compaction (as in bdc_update.cu).
+__device__ __forceinline__ int block_rank(bool flag, int* wcnt, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) wcnt[wid] = __popc(bal);
+  __syncthreads();
+  int off = 0;
+  total = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    if (i < wid) off += wcnt[i];
+    total += wcnt[i];
+  }
+  __syncthreads();
+  return off + __popc(bal & ((1u << lane) - 1u));
+}
+
+
 }  // namespace
 
+// ---------------------------------------------------------------------------- k_rsel
+// Winner report, part 1 (one CTA per task): the winner's FP64 N-0 column and N-0
+// top-kg; which contingencies can reach the report; the multi-branch / injection
+// cases among them (few, FP64, one warp per case) into partial list 0.
+//
+// Exact pruning: an entry of case c can enter the final top-kg only if c's true max
+// loading is >= the kg-th largest true case max.  FP32 maxima are within SCREEN_EPS
+// of FP64, so with kth = the kg-th largest exact FP32 maximum, every case whose upper
+// bound (exact FP32 max, or the dominance bound m0 + scale_c |s(c,t)| of a pair the
+// sweep skipped) is >= kth - 2 eps is visited; the metric's binding case is one of them.
 template <int KC>
-__global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.x;
   if (w.status[b] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -119,14 +161,16 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
   __shared__ double sred[RW];
   __shared__ double sbr[2][RW];
   __shared__ int sbp[2][RW];
-  __shared__ double sWc[RW][RMAX];
   __shared__ double sMinv[RW][MMAX * MMAX];
   __shared__ double sY[RMAX];
   __shared__ int sN0pos[KMAX];
+  __shared__ int wcnt[RW];
+  __shared__ int sCnt;
   const int nd = w.ndead[b];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   if (tid < rt) sY[tid] = w.Y[((size_t)b * rs + tid) * T + best];
   if (lane == 0) wl[wid].n = 0;
+  if (tid == 0) sCnt = 0;
   __syncthreads();
   // the winner's N-0 column, FP64, from the factors
   for (int r = tid; r < R; r += RT) {
@@ -185,16 +229,23 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
     }
   }
 
-  // ---- which contingencies can matter: exact pruning on the FP32 screening maxima --------
-  // A case can place an entry in the final top-kg only if its true max loading is at
-  // least the kg-th largest true case max; with |FP32 - FP64| <= SCREEN_EPS that means
-  // cmax >= kth(cmax) - 2 eps.  The metric's binding case satisfies the same bound.
-  const int ncase = g.N1 + g.NM + g.NI;
+  // ---- which contingencies can matter ------------------------------------------------------
+  const int N1 = g.N1, ncase = N1 + g.NM + g.NI;
   const float* cm = w.cmax + (size_t)b * ncase * T + best;
+  const float m0b = w.m0[(size_t)b * T + best];
   auto feasible_case = [&](int ci) -> bool {
-    if (ci < g.N1) return w.sc_ok[(size_t)b * g.N1 + ci] != 0;
-    if (ci < g.N1 + g.NM) return w.mc_ok[(size_t)b * g.NM + (ci - g.N1)] != 0;
+    if (ci < N1) return w.sc_ok[(size_t)b * N1 + ci] != 0;
+    if (ci < N1 + g.NM) return w.mc_ok[(size_t)b * g.NM + (ci - N1)] != 0;
     return true;
+  };
+  // exact FP32 maximum (>= 0), or -1 with the dominance bound in `ub`
+  auto case_value = [&](int ci, float& ub) -> float {
+    if (ci >= N1 || pair_evaluated(g, w, b, ci, best)) {
+      ub = cm[(size_t)ci * T];
+      return ub;
+    }
+    ub = m0b + w.scale[(size_t)b * N1 + ci] * fabsf(w.s32[((size_t)b * N1 + ci) * T + best]);
+    return -1.f;
   };
   float theta = -1.f;
   {
@@ -206,8 +257,9 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
       int bp = INT_MAX;
       for (int ci = tid; ci < ncase; ci += RT) {
         if (!feasible_case(ci)) continue;
-        const float v = cm[(size_t)ci * T];
-        if (v < 0.f) continue;  // screened-out pair: only an upper bound is known
+        float ub;
+        const float v = case_value(ci, ub);
+        if (v < 0.f) continue;  // only an upper bound is known
         if (!(v < pv || (v == pv && ci > pi))) continue;
         if (better(v, ci, br, bp)) { br = v; bp = ci; }
       }
@@ -228,61 +280,39 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
     }
     theta = found == kg ? kth - 2.f * SCREEN_EPS : -1.f;
   }
-  __shared__ int sCand[CAND_CAP];
-  __shared__ int sNCand;
-  if (tid == 0) sNCand = 0;
-  __syncthreads();
-  for (int ci = tid; ci < ncase; ci += RT) {
-    if (feasible_case(ci) && fabsf(cm[(size_t)ci * T]) >= theta) {
-      const int p = atomicAdd(&sNCand, 1);
-      if (p < CAND_CAP) sCand[p] = ci;
+  // single cases to visit, ascending (the sweep kernel evaluates them in FP64)
+  int* rl = w.rlist + (size_t)b * N1;
+  for (int c0 = 0; c0 < N1; c0 += RT) {
+    const int c = c0 + tid;
+    bool take = false;
+    if (c < N1 && feasible_case(c)) {
+      float ub;
+      case_value(c, ub);
+      take = ub >= theta;
     }
+    int total;
+    const int pos = block_rank(take, wcnt, total);
+    if (take) rl[sCnt + pos] = c;
+    __syncthreads();
+    if (tid == 0) sCnt += total;
+    __syncthreads();
   }
-  __syncthreads();
-  const int ncand = sNCand;
-  const bool listed = ncand <= CAND_CAP;  // else scan every case with the same predicate
-  const int nloop = listed ? ncand : ncase;
+  if (tid == 0) w.rcnt[b] = sCnt;
 
-  // ---- FP64 re-evaluation of the candidate cases for the winner ----------------------------
+  // ---- multi-branch and injection cases of the report (FP64, warp per case) --------------
   LaneTop<KC> lt;
-  for (int li = wid; li < nloop; li += RW) {
-    const int ci = listed ? sCand[li] : li;
-    if (!listed && !(feasible_case(ci) && fabsf(cm[(size_t)ci * T]) >= theta)) continue;
-    int order, kind = 0, q = ci;
-    if (ci < g.N1) {
-      order = g.sc_order[ci];
-    } else if (ci < g.N1 + g.NM) {
-      kind = 1; q = ci - g.N1;
+  for (int ci = N1 + wid; ci < ncase; ci += RW) {
+    if (!feasible_case(ci) || !(cm[(size_t)ci * T] >= theta)) continue;
+    int order, kind = 1, q = ci - N1;
+    if (q < g.NM) {
       order = g.mc_order[q];
     } else {
-      kind = 2; q = ci - g.N1 - g.NM;
+      kind = 2; q -= g.NM;
       order = g.ic_order[q];
     }
     lt.clear();
     const double thresh = warp_thresh(wl[wid], kg);
-    if (kind == 0) {
-      const int rowc = g.sc_row[q];
-      const double sc = n0b[rowc];
-      const double idn = 1.0 / w.den[(size_t)b * g.N1 + q];
-      for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * g.N1 + q) * rs + j];
-      __syncwarp();
-      const double* Dc = g.D64 + (size_t)q * R;
-      for (int p = lane; p < M; p += 32) {
-        const int row = g.mon_row[p];
-        if (is_dead(sdead, nd, row)) continue;  // flow exactly 0: neither metric nor report
-        double f;
-        if (row == rowc) {
-          f = n0b[row] + (-1.0) * sc;
-        } else {
-          double dv = Dc[row];
-          for (int j = 0; j < rt; ++j) dv = fma(Bm[(size_t)j * R + row], sWc[wid][j], dv);
-          f = n0b[row] + (dv * idn) * sc;
-        }
-        const double rel = fabs(f) * g.inv_rating[p];
-        mymax = fmax(mymax, rel);
-        if (row != rowc && rel >= thresh) lt.insert(rel, p, f);
-      }
-    } else if (kind == 1) {
+    if (kind == 1) {
       const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
       for (int i = lane; i < m * m; i += 32) sMinv[wid][i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
       __syncwarp();
@@ -334,27 +364,211 @@ __global__ void __launch_bounds__(RT, 3) k_report(DevGrid g, DevCfg cfg, Work w)
     warp_merge<KC>(lt, kc, wl[wid], kg, order);
     __syncwarp();
   }
-
-  // ---- FP64 metric and final merge --------------------------------------------------------
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if (lane == 0) sred[wid] = mymax;
   __syncthreads();
   if (tid == 0) {
     double mx = 0.0;
     for (int i = 0; i < RW; ++i) mx = fmax(mx, sred[i]);
-    if (w.nisl[b] > 0) mx = fmax(mx, cfg.penalty);
-    w.metric[b] = mx;
     WarpList& F = wl[0];
     for (int i = 1; i < RW; ++i)
       for (int e = 0; e < wl[i].n; ++e)
         wl_insert(F, kg, wl[i].rel[e], wl[i].cs[e], wl[i].pos[e], wl[i].flow[e]);
-    w.n1cnt[b] = F.n;
-    for (int e = 0; e < F.n; ++e) {
-      w.n1case[(size_t)b * kg + e] = F.cs[e];
-      w.n1pos[(size_t)b * kg + e] = F.pos[e];
-      w.n1flow[(size_t)b * kg + e] = F.flow[e];
-      w.n1rel[(size_t)b * kg + e] = F.rel[e];
+    const size_t o = (size_t)b * w.nslot * KMAX;
+    for (int e = 0; e < kg; ++e) {
+      const bool has = e < F.n;
+      w.pcase[o + e] = has ? F.cs[e] : INT_MAX;
+      w.ppos[o + e] = has ? F.pos[e] : INT_MAX;
+      w.pflow[o + e] = has ? F.flow[e] : 0.0;
+      w.prel[o + e] = has ? F.rel[e] : -1.0;
     }
+    w.pmax[(size_t)b * w.nslot] = mx;
+  }
+}
+
+// --------------------------------------------------------------------------- k_rsweep
+// Winner report, part 2: the listed single cases in FP64 for the winning candidate,
+// RCW cases per CTA, one case per thread; monitored-row chunks of B'' rows, the N-0
+// column and 1/rating are staged in shared memory once for all the CTA's cases.
+// Each thread keeps its case's stable top-kc (rel desc, position asc; solver.py:287-299)
+// and max; the CTA merges them into its partial top-kg by (rel desc, case order,
+// position) (_merge_entries, solver.py:302-318).
+namespace {
+constexpr int SRC = 64;  // monitored rows per chunk
+}
+
+template <int KC>
+__global__ void __launch_bounds__(RCW) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+  const int b = blockIdx.y, tile = blockIdx.x;
+  if (w.status[b] != 0) return;
+  const int n = w.rcnt[b];
+  if (tile * RCW >= n) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = g.R, M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kg = cfg.kg;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  double* sW = reinterpret_cast<double*>(rsm);  // [rt][RCW]
+  double* sB = sW + (size_t)rs * RCW;           // [rt][SRC]
+  __shared__ double sN0[SRC], sInv[SRC];
+  __shared__ int sRow[SRC];
+  __shared__ int sdead[RMAX];
+  __shared__ double wr[RCW / 32];
+  __shared__ int wo[RCW / 32], wp[RCW / 32], wsrc[RCW / 32];
+  __shared__ int pick_src;
+  const int nd = w.ndead[b];
+  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  const int li = tile * RCW + tid;
+  const int c = li < n ? w.rlist[(size_t)b * N1 + li] : -1;
+  const double* n0b = w.n0b + (size_t)b * R;
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  int rowc = -1, order = INT_MAX;
+  double idn = 0.0, sc = 0.0;
+  if (c >= 0) {
+    rowc = g.sc_row[c];
+    order = g.sc_order[c];
+    idn = 1.0 / w.den[(size_t)b * N1 + c];
+    sc = n0b[rowc];
+    for (int j = 0; j < rt; ++j) sW[j * RCW + tid] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+  }
+  const double* Dc = g.D64 + (size_t)(c >= 0 ? c : 0) * R;
+  LaneTop<KC> lt;
+  lt.clear();
+  double mymax = 0.0;
+  __syncthreads();
+  for (int m0 = 0; m0 < M; m0 += SRC) {
+    for (int rr = tid; rr < SRC; rr += RCW) {
+      const int m = m0 + rr;
+      int row = -1;
+      if (m < M) {
+        row = g.mon_row[m];
+        if (is_dead(sdead, nd, row)) row = -1;
+      }
+      sRow[rr] = row;
+      sN0[rr] = row >= 0 ? n0b[row] : 0.0;
+      sInv[rr] = m < M ? g.inv_rating[m] : 0.0;
+    }
+    for (int idx = tid; idx < rt * SRC; idx += RCW) {
+      const int j = idx / SRC, rr = idx % SRC, m = m0 + rr;
+      sB[j * SRC + rr] = m < M ? Bm[(size_t)j * R + g.mon_row[m]] : 0.0;
+    }
+    __syncthreads();
+    if (c >= 0) {
+      const int rend = min(SRC, M - m0);
+      for (int rr = 0; rr < rend; ++rr) {
+        const int row = sRow[rr];
+        if (row < 0) continue;  // disconnected: flow exactly 0, neither metric nor report
+        double f;
+        if (row == rowc) {
+          f = sN0[rr] + (-1.0) * sc;
+        } else {
+          double dv = __ldg(&Dc[row]);
+          for (int j = 0; j < rt; ++j) dv = fma(sB[j * SRC + rr], sW[j * RCW + tid], dv);
+          f = sN0[rr] + (dv * idn) * sc;
+        }
+        const double rel = fabs(f) * sInv[rr];
+        mymax = fmax(mymax, rel);
+        if (row != rowc) lt.insert(rel, m0 + rr, f);
+      }
+    }
+    __syncthreads();
+  }
+  // CTA max and the partial top-kg: kg rounds of block argmax over the thread heads
+  for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  if (lane == 0) wr[wid] = mymax;
+  __syncthreads();
+  const int slot = 1 + tile;
+  const size_t o = ((size_t)b * w.nslot + slot) * KMAX;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < RCW / 32; ++i) mx = fmax(mx, wr[i]);
+    w.pmax[(size_t)b * w.nslot + slot] = mx;
+  }
+  __syncthreads();
+  for (int e = 0; e < kg; ++e) {
+    double r = c >= 0 ? lt.rel[0] : -1.0;
+    int ord = c >= 0 && r >= 0.0 ? order : INT_MAX, p = lt.pos[0], src = tid;
+    for (int off = 16; off; off >>= 1) {
+      const double orr = __shfl_xor_sync(0xffffffffu, r, off);
+      const int oo = __shfl_xor_sync(0xffffffffu, ord, off);
+      const int op = __shfl_xor_sync(0xffffffffu, p, off);
+      const int os = __shfl_xor_sync(0xffffffffu, src, off);
+      if (better3(orr, oo, op, r, ord, p)) { r = orr; ord = oo; p = op; src = os; }
+    }
+    if (lane == 0) { wr[wid] = r; wo[wid] = ord; wp[wid] = p; wsrc[wid] = src; }
+    __syncthreads();
+    if (tid == 0) {
+      int k = 0;
+      for (int i = 1; i < RCW / 32; ++i)
+        if (better3(wr[i], wo[i], wp[i], wr[k], wo[k], wp[k])) k = i;
+      pick_src = wr[k] >= 0.0 ? wsrc[k] : -1;
+      w.prel[o + e] = wr[k] >= 0.0 ? wr[k] : -1.0;
+      w.pcase[o + e] = wr[k] >= 0.0 ? wo[k] : INT_MAX;
+      w.ppos[o + e] = wr[k] >= 0.0 ? wp[k] : INT_MAX;
+    }
+    __syncthreads();
+    const int ps = pick_src;
+    if (ps < 0) {
+      for (int e2 = e + 1 + tid; e2 < kg; e2 += RCW) {
+        w.prel[o + e2] = -1.0; w.pcase[o + e2] = INT_MAX; w.ppos[o + e2] = INT_MAX;
+      }
+      break;
+    }
+    if (tid == ps) {
+      w.pflow[o + e] = lt.flow[0];
+      lt.pop();
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------------------- k_rmerge
+// Winner report, part 3 (one warp per task): the final top-kg over the partial lists
+// and the FP64 metric max(N-0, every feasible case, penalty) (agg_m, solver.py:235-252).
+__global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = gt >> 5, lane = gt & 31;
+  if (b >= w.Wb || w.status[b] != 0) return;
+  const int kg = cfg.kg;
+  const int nsl = 1 + (w.rcnt[b] + RCW - 1) / RCW;
+  double mx = 0.0;
+  for (int s = lane; s < nsl; s += 32) mx = fmax(mx, w.pmax[(size_t)b * w.nslot + s]);
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const size_t base = (size_t)b * w.nslot * KMAX;
+  const int ne = nsl * KMAX;
+  double pr = 1e300;
+  int pc = -1, pp = -1, cnt = 0;
+  for (int e = 0; e < kg; ++e) {
+    double br = -1.0;
+    int bc = INT_MAX, bp = INT_MAX, bi = -1;
+    for (int i = lane; i < ne; i += 32) {
+      if ((i % KMAX) >= kg) continue;
+      const double r = w.prel[base + i];
+      if (r < 0.0) continue;
+      const int c = w.pcase[base + i], p = w.ppos[base + i];
+      // strictly after the previous pick in (rel desc, case, pos) order
+      if (!better3(pr, pc, pp, r, c, p)) continue;
+      if (better3(r, c, p, br, bc, bp)) { br = r; bc = c; bp = p; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double orr = __shfl_xor_sync(0xffffffffu, br, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better3(orr, oc, op, br, bc, bp)) { br = orr; bc = oc; bp = op; bi = oi; }
+    }
+    if (br < 0.0) break;
+    if (lane == 0) {
+      w.n1case[(size_t)b * kg + e] = bc;
+      w.n1pos[(size_t)b * kg + e] = bp;
+      w.n1flow[(size_t)b * kg + e] = w.pflow[base + bi];
+      w.n1rel[(size_t)b * kg + e] = br;
+    }
+    pr = br; pc = bc; pp = bp;
+    ++cnt;
+  }
+  if (lane == 0) {
+    if (w.nisl[b] > 0) mx = fmax(mx, cfg.penalty);
+    w.metric[b] = mx;
+    w.n1cnt[b] = cnt;
   }
 }
 
@@ -429,11 +643,30 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
   }
 }
 
+namespace {
+template <int KC>
+void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
+  if (g.N1 > 0 && g.M > 0) {
+    const size_t dyn = ((size_t)w.rs * RCW + (size_t)w.rs * SRC) * sizeof(double);
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_rsweep<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(((size_t)RMAX * RCW + (size_t)RMAX * SRC) * sizeof(double)));
+      init = true;
+    }
+    k_rsweep<KC><<<dim3(w.nslot - 1, w.Wb), RCW, dyn, s>>>(g, c, w);
+  }
+  const long long threads = (long long)w.Wb * 32;
+  k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
+}
+}  // namespace
+
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  if (c.kc <= 5) k_report<5><<<w.Wb, RT, 0, s>>>(g, c, w);
-  else if (c.kc <= 8) k_report<8><<<w.Wb, RT, 0, s>>>(g, c, w);
-  else if (c.kc <= 16) k_report<16><<<w.Wb, RT, 0, s>>>(g, c, w);
-  else k_report<32><<<w.Wb, RT, 0, s>>>(g, c, w);
+  if (c.kc <= 5) launch_report_t<5>(g, c, w, s);
+  else if (c.kc <= 8) launch_report_t<8>(g, c, w, s);
+  else if (c.kc <= 16) launch_report_t<16>(g, c, w, s);
+  else launch_report_t<32>(g, c, w, s);
 }
 
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
@@ -445,8 +678,9 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
 
 int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
-  // update, select, report (+ single: [scale, top-k,] top tile, screened sweep) (+ other)
-  return 3 + (single ? 1 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
+  // update, select, report select + merge (+ single: [scale, top-k,] top tile, screened
+  // sweep, report sweep) (+ other)
+  return 4 + (single ? 2 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
          (g.NM + g.NI > 0 && g.M > 0);
 }
 

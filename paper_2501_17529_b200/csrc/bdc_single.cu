@@ -96,6 +96,15 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
     // (N-0, multi/injection cases, the TOP pass) and, for tasks with islanded cases,
     // the penalty floor -- cannot change the metric.  Cases already evaluated by the
     // TOP pass are skipped outright.
+    bool live[CPT];
+    float scl[CPT];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int cc = tx * CPT + i, c = sCase[cc];
+      live[i] = c >= 0 && !done_c(c);
+      scl[i] = (w.screen && live[i]) ? w.scale[(size_t)b * N1 + c] : 0.f;
+      if (w.screen) live[i] = live[i] && sInvDen[cc] != 0.0;
+    }
     bool need = false;
     if (w.screen) {
       const float pen = w.nisl[b] > 0 ? (float)cfg.penalty : 0.f;
@@ -106,35 +115,18 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
         const float lb = fmaxf(__uint_as_float(w.m32[(size_t)b * T + t]), pen);
         const float m0 = w.m0[(size_t)b * T + t];
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-          const int cc = tx * CPT + i, c = sCase[cc];
-          if (c < 0 || sInvDen[cc] == 0.0 || done_c(c)) continue;
-          need |= (m0 + w.scale[(size_t)b * N1 + c] * fabsf(sv[i][jj])) > lb;
-        }
+        for (int i = 0; i < CPT; ++i) need |= live[i] && (m0 + scl[i] * fabsf(sv[i][jj])) > lb;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int c = sCase[tx * CPT + i];
-        need |= c >= 0 && !done_c(c);
-      }
+      for (int i = 0; i < CPT; ++i) need |= live[i];
     }
     warp_alive = __any_sync(0xffffffffu, need);
+    // which warps evaluated their pairs: the winner report takes exact maxima from
+    // alive warps and re-derives the dominance bound for the others
+    if ((tid & 31) == 0)
+      w.alive[(((size_t)b * w.nct + blockIdx.x) * w.ntt + blockIdx.y) * SWEEP_WARPS + (tid >> 5)] = warp_alive;
     const bool block_alive = __syncthreads_or(need);
-    if (!warp_alive) {
-      // every pair of this warp is dominated: record its bound for the report
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int c = sCase[tx * CPT + i];
-        if (c < 0 || done_c(c)) continue;
-        const float sc = w.scale[(size_t)b * N1 + c];
-#pragma unroll
-        for (int jj = 0; jj < TPT; ++jj) {
-          const int t = t0 + ty * TPT + jj;
-          if (t < T) cm[(size_t)c * T + t] = -(w.m0[(size_t)b * T + t] + sc * fabsf(sv[i][jj]));
-        }
-      }
-    }
     if (!block_alive) return;  // no cp.async in flight yet
   }
   if (warp_alive) {
@@ -360,12 +352,13 @@ void launch_single_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
 
 template <int PASS>
 void launch_pass(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  // tile widths must match single_tile_cases(T) (the TOP pass evaluates one tile)
-  if (w.T >= 96) launch_single_t<2, 16, 32, 8, 32, 2, PASS>(g, c, w, s);      // 64 cases x 128 candidates
-  else if (w.T >= 48) launch_single_t<2, 8, 32, 8, 32, 3, PASS>(g, c, w, s);  // 64 x 64
-  else if (w.T >= 24) launch_single_t<4, 4, 32, 8, 32, 3, PASS>(g, c, w, s);  // 128 x 32
-  else if (w.T >= 12) launch_single_t<4, 4, 64, 4, 32, 3, PASS>(g, c, w, s);  // 256 x 16
-  else launch_single_t<4, 2, 64, 4, 32, 3, PASS>(g, c, w, s);                 // 256 x 8
+  // must match sweep_shape(T) (bdc_device.cuh): the report decodes the alive map with it
+  const SweepShape sh = sweep_shape(w.T);
+  if (sh.TPT == 16) launch_single_t<2, 16, 32, 8, 32, 2, PASS>(g, c, w, s);      // 64 cases x 128 candidates
+  else if (sh.TPT == 8) launch_single_t<2, 8, 32, 8, 32, 3, PASS>(g, c, w, s);   // 64 x 64
+  else if (sh.TX == 32) launch_single_t<4, 4, 32, 8, 32, 3, PASS>(g, c, w, s);   // 128 x 32
+  else if (sh.TPT == 4) launch_single_t<4, 4, 64, 4, 32, 3, PASS>(g, c, w, s);   // 256 x 16
+  else launch_single_t<4, 2, 64, 4, 32, 3, PASS>(g, c, w, s);                    // 256 x 8
 }
 
 }  // namespace

@@ -510,26 +510,25 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       }
       // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
       // F = n0 + sum_j Lo[r][j] So[j][t]; columns formed once per task in FP64
-      const int NTM = w.NTERM;
+      const int NTM = w.NTERM, MT = g.MT, NQ = g.NM + g.NI;
       if (NTM > 0) {
         float* Lo = w.Lo + (size_t)b * M * NTM;
         float* So = w.So + (size_t)b * NTM * T;
-        for (int idx = tid; idx < M * (g.NM + g.NI); idx += NT) {
-          const int p = idx / (g.NM + g.NI), q = idx % (g.NM + g.NI);
+        for (int idx = tid; idx < M * NQ; idx += NT) {
+          const int p = idx / NQ, q = idx % NQ;
           const int row = g.mon_row[p];
           const double inv = g.inv_rating[p];
           const bool dead = is_dead(s.dead, nd, row);
+          float* out = Lo + ((size_t)p * NQ + q) * MT;
+          for (int j = 0; j < MT; ++j) out[j] = 0.f;
+          if (dead) continue;
           if (q < g.NM) {
             const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-            float* out = Lo + (size_t)p * NTM + st;
-            if (dead || !w.mc_ok[(size_t)b * g.NM + q]) {
-              for (int j = 0; j < m; ++j) out[j] = 0.f;
-              continue;
-            }
+            if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
             int own = -1;
             for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
             if (own >= 0) {
-              for (int j = 0; j < m; ++j) out[j] = (j == own) ? (float)(-inv) : 0.f;
+              out[own] = (float)(-inv);
               continue;
             }
             double Dv[MMAX];
@@ -547,8 +546,6 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
             }
           } else {
             const int qi = q - g.NM, sl = g.ic_slot[qi];
-            float* out = Lo + (size_t)p * NTM + g.NMB + 2 * qi;
-            if (dead) { out[0] = 0.f; out[1] = 0.f; continue; }
             const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
             const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
             const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
@@ -565,13 +562,14 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
         }
         const uint8_t* ib = w.inj + (size_t)b * T * g.K;
         for (int idx = tid; idx < NTM * T; idx += NT) {
-          const int j = idx / T, t = idx % T;
-          float v;
-          if (j < g.NMB) {
-            v = (float)n0_at(g, w, b, g.mb_row[j], t, rt, s.dead, nd);
-          } else {
-            const int qi = (j - g.NMB) >> 1, sl = g.ic_slot[qi];
-            v = ((j - g.NMB) & 1) == 0 ? 1.f : ((sl >= 0 && ib[(size_t)t * g.K + sl]) ? 1.f : 0.f);
+          const int qj = idx / T, t = idx % T, q = qj / MT, j = qj % MT;
+          float v = 0.f;
+          if (q < g.NM) {
+            const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+            if (j < m) v = (float)n0_at(g, w, b, g.mb_row[st + j], t, rt, s.dead, nd);
+          } else if (j < 2) {
+            const int sl = g.ic_slot[q - g.NM];
+            v = j == 0 ? 1.f : ((sl >= 0 && ib[(size_t)t * g.K + sl]) ? 1.f : 0.f);
           }
           So[idx] = v;
         }

@@ -117,6 +117,7 @@ EXPORTS = (
     "bdc_solve",
     "bdc_probe_flows",
     "bdc_session_set_wave",
+    "bdc_scan_tasks",
 )
 
 _lib = None
@@ -143,6 +144,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.bdc_solve.argtypes = [_P, ctypes.POINTER(_Batch)]
         lib.bdc_probe_flows.argtypes = [_P, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P, _P, _P]
         lib.bdc_session_set_wave.argtypes = [_P, ctypes.c_int64]
+        lib.bdc_scan_tasks.argtypes = [_P, _P, _P, ctypes.c_int64, ctypes.c_int32, _P, _P, _P]
         _lib = lib
         return lib
 
@@ -286,30 +288,35 @@ class Engine:
         self.lib.bdc_session_set_wave(self.handle, int(max_tasks))
 
     # ------------------------------------------------------------------ checks
-    def task_ranks(self, splits: np.ndarray, discos: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-        """Per task: number of non-trivial splits k and of disconnections d."""
-        k = splits.any(axis=2).sum(axis=1) if splits.size else np.zeros(len(splits), np.int64)
-        d = (discos >= 0).sum(axis=1) if discos.size else np.zeros(len(discos), np.int64)
-        return k.astype(np.int64), d.astype(np.int64)
-
-    def check_limits(self, splits: np.ndarray, k: np.ndarray, d: np.ndarray) -> int:
-        rank = k + d
-        rmax = int(rank.max()) if len(rank) else 0
+    def check_batch(self, splits: np.ndarray, discos: np.ndarray) -> int:
+        """Engine limits of one batch (native scan of the task arrays, no device work);
+        returns the workspace rank stride max(k + d).  ``splits`` (B,S,E) u8,
+        ``discos`` (B,D) i64."""
+        B = int(splits.shape[0])
+        D = int(discos.shape[1]) if discos.ndim == 2 else 0
+        mr, md, ma = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+        sp = np.ascontiguousarray(splits, dtype=np.uint8)
+        dc = np.ascontiguousarray(discos, dtype=np.int64)
+        rc = self.lib.bdc_scan_tasks(
+            self.handle, _ptr(sp) if sp.size else None, _ptr(dc) if dc.size else None, B, D,
+            ctypes.byref(mr), ctypes.byref(md), ctypes.byref(ma),
+        )
+        if rc != 0:
+            raise EngineUnavailable(f"bdc_scan_tasks failed ({rc}): {_err(self.lib)}")
+        rmax, dmax, amax = int(mr.value), int(md.value), int(ma.value)
         if rmax > MAX_RANK:
             raise ValidationError(
                 f"a task applies {rmax} splits + disconnections; the engine supports {MAX_RANK}"
             )
-        if self.config.multi_outage_method == "modf" and len(d) and int(d.max()) > MAX_MULTI:
-            if int(d.max()) <= self.config.max_simultaneous_outages:
+        if self.config.multi_outage_method == "modf" and dmax > MAX_MULTI:
+            if dmax <= self.config.max_simultaneous_outages:
                 raise ValidationError(
-                    f"{int(d.max())} simultaneous disconnections exceed the engine's MODF limit of {MAX_MULTI}"
+                    f"{dmax} simultaneous disconnections exceed the engine's MODF limit of {MAX_MULTI}"
                 )
-        if splits.size and self.slots_per_sub.any():
-            active = (splits.any(axis=2) * self.slots_per_sub[None, :]).sum(axis=1)
-            if int(active.max()) > MAX_ACTIVE_SLOTS:
-                raise ValidationError(
-                    f"a task moves {int(active.max())} injection slots; the engine supports {MAX_ACTIVE_SLOTS}"
-                )
+        if amax > MAX_ACTIVE_SLOTS:
+            raise ValidationError(
+                f"a task moves {amax} injection slots; the engine supports {MAX_ACTIVE_SLOTS}"
+            )
         return max(rmax, 1)
 
     # ------------------------------------------------------------------ solve
@@ -335,8 +342,7 @@ class Engine:
         discos = np.ascontiguousarray(discos, dtype=np.int64).reshape(B, -1)
         inj = np.ascontiguousarray(inj, dtype=np.uint8).reshape(B, T, tb.K)
         if max_rank is None:
-            k, d = self.task_ranks(splits, discos)
-            max_rank = self.check_limits(splits, k, d)
+            max_rank = self.check_batch(splits, discos)
         kg = self.config.topk_global
         ncw = max(1, (len(self.case_ids) + 31) // 32)
         out = BatchOutput(self, B, T, kg, ncw, splits, discos, inj, want_candidates)

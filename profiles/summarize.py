@@ -74,9 +74,48 @@ def launches(path):
     print()
 
 
+def source(path, top=25):
+    """Top CUDA source lines by warp-stall samples, per captured kernel
+    (needs -lineinfo at compile time and --import-source on at capture)."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    per_fn = OrderedDict()
+    fn, fpath, hdr = "?", "?", None
+    for r in csv.reader(io.StringIO(out)):
+        if not r:
+            continue
+        if r[0] == "File Path":
+            fpath = r[1].split("/")[-1]
+            continue
+        if r[0] == "Function Name":
+            fn = r[1]
+            continue
+        if r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr) or r[2] != "-":
+            continue  # SASS rows carry an address; line aggregates carry "-"
+        try:
+            v = float(r[4] or 0)
+        except ValueError:
+            continue
+        if v > 0:
+            per_fn.setdefault(fn, []).append((v, f"{fpath}:{r[0]}", r[1].strip()[:100]))
+    for fn, data in per_fn.items():
+        tot = sum(d[0] for d in data) or 1.0
+        print(f"#### hot source lines of `{fn[:110]}` ({path.split('/')[-1]}, share of warp-stall samples)\n")
+        print("| share | line | source |\n|---|---|---|")
+        for v, ln, src in sorted(data, key=lambda x: -x[0])[:top]:
+            print(f"| {v / tot * 100:.1f}% | {ln} | `{src.replace('|', '/')}` |")
+        print()
+
+
 if __name__ == "__main__":
     args = sys.argv[1:]
-    if args and args[0] == "--launches":
+    if args and args[0] == "--source":
+        for p in args[1:]:
+            source(p)
+    elif args and args[0] == "--launches":
         for p in args[1:]:
             launches(p)
     else:
