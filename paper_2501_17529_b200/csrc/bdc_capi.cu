@@ -306,6 +306,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
+  size_t o_b32 = L.add(B * (size_t)rs * g.M * 4), o_bmx = L.add(B * (size_t)rs * 4);
   size_t o_lf = L.add(32), o_bs = L.add(16);
   if (!base) return L.total;
   Work& x = *w;
@@ -339,6 +340,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = single_tile_cases(T);
+  x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx);
   x.alive = (uint8_t*)(base + o_alive); x.nct = nct; x.ntt = ntt;
   x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.nslot = nslot;
   x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);
@@ -437,11 +439,14 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
       err = cudaMemcpyAsync((void*)x.tcount, bt->t_count + b0, (size_t)nb * 4, hk, st);
     if (!bt->t_count) x.tcount = nullptr;
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
     // stage_ms: 0 h2d, 1 update (+ fused N-0, screen data), 2 multi/injection N-1,
     // 3 single N-1 (top tile + screened sweep), 4 select, 5 (unused), 6 report, 7 d2h
     launch_update(g, s->cfg, x, st);
+    launch_n0(g, x, st);
     cudaEventRecord(E[2], st);
     launch_other(g, x, st);
     cudaEventRecord(E[3], st);

@@ -98,7 +98,9 @@ struct Work {
                   //                   evaluated its pairs (else they were dominated)
   int nct, ntt;   // case / candidate tiles of the sweep
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
-  float* scale;   // (Wb, N1)      FP32 max_r |LODF(r,c)|/rating_r (dominance-screen bound)
+  float* scale;   // (Wb, N1)      FP32 upper bound of max_r |LODF(r,c)|/rating_r (dominance screen)
+  float* B32;     // (Wb, rs, M)   FP32 B'' on monitored rows (screening bound only)
+  float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
   int screen;     // 1 = exact dominance screen on
   int ptop;       // cases evaluated first (the top tile by screening bound)
@@ -250,6 +252,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);

@@ -678,9 +678,9 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
 
 int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
-  // update, select, report select + merge (+ single: [scale, top-k,] top tile, screened
+  // update, N-0, select, report select + merge (+ single: [scale, top-k,] top tile, screened
   // sweep, report sweep) (+ other)
-  return 4 + (single ? 2 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
+  return 5 + (single ? 2 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
          (g.NM + g.NI > 0 && g.M > 0);
 }
 

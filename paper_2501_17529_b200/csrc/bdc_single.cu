@@ -10,19 +10,21 @@
 // (case x candidate x branch) tensor never leaves registers.
 //
 // Exact dominance screen (the reference's metric_first, solver.py:798-822):
-//   pass TOP     the ptop cases with the largest bound max_t(m0(t) + scale_c |s(c,t)|)
-//                (selected by the update kernel) are evaluated first, for every
-//                candidate -- the reference likewise visits likely-binding cases first;
+//   k_scale      an upper bound scale_c of max_r |L'(r,c)| per case and the ranking
+//                key max_t(m0(t) + scale_c |s(c,t)|);
+//   pass TOP     the ptop cases with the largest key (k_topk) are evaluated first,
+//                for every candidate -- the reference likewise visits likely-binding
+//                cases first;
 //   pass SCREEN  every other tile; a pair whose bound cannot exceed the running
 //                metric of its candidate cannot change it and is skipped, per CTA
-//                tile and per warp.  Skipped pairs store -bound in cmax (an upper
-//                bound the winner report prunes with); evaluated pairs store the
-//                exact FP32 max.
+//                tile and per warp.  Evaluated pairs store their exact FP32 max in
+//                cmax; the alive map records which warps evaluated, so the winner
+//                report re-derives the bound of skipped pairs.
 #include "bdc_device.cuh"
 
 namespace bdc {
 
-enum { PASS_SCREEN = 0, PASS_TOP = 1, PASS_SCALE = 2 };
+enum { PASS_SCREEN = 0, PASS_TOP = 1 };
 
 template <int CPT, int TPT, int TX, int TY, int RC, int MINB, int PASS>
 __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, Work w) {
@@ -45,8 +47,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
   __shared__ int sRowC[NC];
   __shared__ double sInv[2][RC];
   __shared__ int sRow[2][RC];
-  constexpr int LR = PASS == PASS_SCALE ? 1 : RC;  // the scale pass keeps no LODF tile
-  __shared__ __align__(16) float sL[LR][NC];
+  __shared__ __align__(16) float sL[RC][NC];
   __shared__ int sdead[RMAX];
   const int nd = w.ndead[b];
   const double* Bm = w.Bm + (size_t)b * rs * R;
@@ -84,12 +85,11 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
 #pragma unroll
     for (int jj = 0; jj < TPT; ++jj) {
       const int t = t0 + ty * TPT + jj;
-      sv[i][jj] = (PASS != PASS_SCALE && c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
+      sv[i][jj] = (c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
       acc[i][jj] = 0.f;
     }
   }
-  bool warp_alive = PASS != PASS_SCALE;
-  float colmax = 0.f;  // PASS_SCALE: running max |L|/rating of this thread's column
+  bool warp_alive = true;
   if constexpr (PASS == PASS_SCREEN) {
     // |F| <= m0(t) + scale_c |s(c,t)| (update kernel): a pair whose bound cannot
     // exceed a lower bound of its candidate's final metric -- the running metric
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
       const bool ok = m < M;
       cp8(&sBb[(buf * rs + j) * RC + rr], ok ? &Bm[(size_t)j * R + g.mon_row[m]] : Bm, ok);
     }
-    if constexpr (PASS != PASS_SCALE && TT % 4 == 0) {
+    if constexpr (TT % 4 == 0) {
       if (vecN) {
         constexpr int TQ = TT / 4;
         for (int idx = tid; idx < RC * TQ; idx += NTH) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
         }
       }
     }
-    if (PASS != PASS_SCALE && !vecN) {
+    if (!vecN) {
       for (int idx = tid; idx < RC * TT; idx += NTH) {
         const int rr = idx / TT, tt = idx % TT, m = m0 + rr, t = t0 + tt;
         const bool ok = m < M && t < T;
@@ -234,13 +234,12 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
           const double sc = idn * sInv[buf][rr];
           float lv = 0.f;
           if (row >= 0 && idn != 0.0) lv = (row == rowc) ? (float)(-sInv[buf][rr]) : (float)(v[k] * sc);
-          if constexpr (PASS == PASS_SCALE) colmax = fmaxf(colmax, fabsf(lv));
-          else sL[rr][cc] = lv;
+          sL[rr][cc] = lv;
         }
       }
     }
     __syncthreads();
-    if (PASS != PASS_SCALE && warp_alive) {
+    if (warp_alive) {
       const int rend = min(RC, M - ch * RC);
       if (rend == RC) {
 #pragma unroll 4
@@ -274,30 +273,6 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
     __syncthreads();
   }
 
-  if constexpr (PASS == PASS_SCALE) {
-    // scale_c = max over the rows of |L(r,c)|/rating_r (exact FP32 of the values the
-    // sweep multiplies), then the ranking key bkey_c = max_t(m0(t) + scale_c |s(c,t)|)
-    float* sMax = sDp;  // reuse the (idle) D_base buffer
-    for (int cc = tid; cc < NC; cc += NTH) sMax[cc] = 0.f;
-    __syncthreads();
-    atomicMax(reinterpret_cast<unsigned*>(&sMax[tid % NC]), __float_as_uint(colmax));
-    __syncthreads();
-    const int lane = tid & 31, wid = tid >> 5;
-    const float* m0 = w.m0 + (size_t)b * T;
-    for (int cc = wid; cc < NC; cc += NTH / 32) {
-      const int c = sCase[cc];
-      if (c < 0) continue;
-      const float sc = sMax[cc] * (1.f + 1e-6f);
-      float bm = 0.f;
-      for (int t = lane; t < T; t += 32) bm = fmaxf(bm, m0[t] + sc * fabsf(s32[(size_t)c * T + t]));
-      for (int o = 16; o; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-      if (lane == 0) {
-        w.scale[(size_t)b * N1 + c] = sc;
-        w.bkey[(size_t)b * N1 + c] = sInvDen[cc] != 0.0 ? __float_as_uint(bm) : 0u;
-      }
-    }
-    return;
-  }
   if (!warp_alive) return;
   // exact per-(case, candidate) maxima for the winner report; the per-candidate max
   // over the tile's cases goes into the running metric
@@ -326,6 +301,152 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
 #undef SD
 }
 
+// ---------------------------------------------------------------------------- k_scale
+// Per-case screening scale: an upper bound of max_r |L'(r,c)| over the monitored rows
+// (L' = the FP32 LODF/rating values the sweep multiplies), from an FP32 evaluation
+// L~ = D_base + sum_j B''_j W_j with a rigorous rounding term:
+//     |L - L~| <= gamma (|D| + sum_j |B''_j| |W_j|),  gamma = (rt + 8) 2^-23,
+// bounded per case by sc_dscale_c + sum_j |W_cj| max_r |B''(r,j)|/rating_r.  The own
+// row contributes 1/rating (L' = -1/rating there), disconnected rows nothing.  Then the
+// ranking key bkey_c = max_t (m0(t) + scale_c |s(c,t)|) (solver.py:634-639, 815).
+// One thread per case, monitored-row chunks of D_base and B'' through a cp.async
+// double buffer; 4 rows of B'' per 16-byte shared load.
+namespace {
+constexpr int SC_NC = 256, SC_RC = 16;  // static shared memory stays under 48 KB
+}
+
+// RS = rank bucket >= every task's rank in the wave: W in registers, B'' terms past a
+// task's own rank are zero-filled, so the inner loop is straight-line FFMAs.
+template <int RS>
+__global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
+  const int b = blockIdx.y;
+  if (w.status[b] != 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c0 = blockIdx.x * SC_NC, c = c0 + tid < g.N1 ? c0 + tid : -1;
+  const int rs = w.rs, rt = w.rank[b], M = g.M, N1 = g.N1, T = w.T;
+  __shared__ __align__(16) float sD[2][SC_RC][SC_NC];
+  __shared__ __align__(16) float sB[2][RS][SC_RC];
+  __shared__ float sInv[2][SC_RC];
+  __shared__ float sU[SC_NC];
+  __shared__ int sdead[RMAX];
+  const int nd = w.ndead[b];
+  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  __syncthreads();
+  bool ok = false;
+  int ownp = -1;
+  float wsum = 0.f;
+  double idn = 0.0;
+  float wr[RS];
+#pragma unroll
+  for (int j = 0; j < RS; ++j) wr[j] = 0.f;
+  if (c >= 0) {
+    ok = w.sc_ok[(size_t)b * N1 + c] != 0;
+    idn = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
+    const int rowc = g.sc_row[c];
+    ownp = is_dead(sdead, nd, rowc) ? -1 : g.row_mon_pos[rowc];
+#pragma unroll
+    for (int j = 0; j < RS; ++j)
+      if (j < rt) {
+        const double wv = w.Wsc[((size_t)b * N1 + c) * rs + j];
+        wr[j] = (float)wv;
+        wsum += (float)fabs(wv) * w.bmax[(size_t)b * rs + j];
+      }
+  }
+  const float* B32 = w.B32 + (size_t)b * rs * M;
+  auto issue = [&](int m0, int buf) {
+    for (int idx = tid; idx < SC_RC * (SC_NC / 4); idx += SC_NC) {
+      const int rr = idx / (SC_NC / 4), q = 4 * (idx % (SC_NC / 4)), m = m0 + rr;
+      const bool okd = m < M && c0 + q < g.N1p;  // rows are zero-padded to N1p
+      cp16(&sD[buf][rr][q], okd ? &g.D32[(size_t)m * g.N1p + c0 + q] : g.D32, okd);
+    }
+    for (int idx = tid; idx < RS * SC_RC; idx += SC_NC) {
+      const int j = idx / SC_RC, rr = idx % SC_RC, m = m0 + rr;
+      const bool okb = m < M && j < rt;  // zero-fill terms past the task's rank
+      cp4(&sB[buf][j][rr], okb ? &B32[(size_t)j * M + m] : B32, okb);
+    }
+    if (tid < SC_RC) {
+      const int m = m0 + tid;
+      sInv[buf][tid] = (m < M && !is_dead(sdead, nd, g.mon_row[m])) ? (float)g.inv_rating[m] : 0.f;
+    }
+    cp_commit();
+  };
+  float mx = 0.f;
+  issue(0, 0);
+  const int nchunks = (M + SC_RC - 1) / SC_RC;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1, m0 = ch * SC_RC;
+    if (ch + 1 < nchunks) {
+      issue(m0 + SC_RC, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int ownrr = ownp - m0;
+#pragma unroll 2
+    for (int r4 = 0; r4 < SC_RC; r4 += 4) {
+      float l[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) l[k] = sD[buf][r4 + k][tid];
+#pragma unroll
+      for (int j = 0; j < RS; ++j) {
+        const float4 bq = *reinterpret_cast<const float4*>(&sB[buf][j][r4]);
+        l[0] = fmaf(bq.x, wr[j], l[0]);
+        l[1] = fmaf(bq.y, wr[j], l[1]);
+        l[2] = fmaf(bq.z, wr[j], l[2]);
+        l[3] = fmaf(bq.w, wr[j], l[3]);
+      }
+      const float4 iq = *reinterpret_cast<const float4*>(&sInv[buf][r4]);
+      const float v0 = fabsf(l[0]) * iq.x, v1 = fabsf(l[1]) * iq.y;
+      const float v2 = fabsf(l[2]) * iq.z, v3 = fabsf(l[3]) * iq.w;
+      mx = fmaxf(mx, (r4 + 0 == ownrr) ? 0.f : v0);
+      mx = fmaxf(mx, (r4 + 1 == ownrr) ? 0.f : v1);
+      mx = fmaxf(mx, (r4 + 2 == ownrr) ? 0.f : v2);
+      mx = fmaxf(mx, (r4 + 3 == ownrr) ? 0.f : v3);
+    }
+    __syncthreads();
+  }
+  float U = 0.f;
+  if (c >= 0 && ok) {
+    const float gam = (float)(rt + 8) * 1.1920929e-7f;
+    U = (float)fabs(idn) * (mx + gam * ((float)g.sc_dscale[c] + wsum));
+    if (ownp >= 0) U = fmaxf(U, (float)g.inv_rating[ownp]);
+    U *= 1.f + 4e-6f;
+  }
+  sU[tid] = U;
+  __syncthreads();
+  // ranking key: warp per case
+  const float* m0v = w.m0 + (size_t)b * T;
+  for (int cc = wid; cc < SC_NC; cc += SC_NC / 32) {
+    const int cx = c0 + cc;
+    if (cx >= N1) break;
+    const float sc = sU[cc];
+    const float* sv = w.s32 + ((size_t)b * N1 + cx) * T;
+    float bm = 0.f;
+    for (int t = lane; t < T; t += 32) bm = fmaxf(bm, m0v[t] + sc * fabsf(sv[t]));
+    for (int o = 16; o; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if (lane == 0) {
+      w.scale[(size_t)b * N1 + cx] = sc;
+      w.bkey[(size_t)b * N1 + cx] = w.sc_ok[(size_t)b * N1 + cx] ? __float_as_uint(bm) : 0u;
+    }
+  }
+}
+
+namespace {
+void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
+  const dim3 grid((g.N1 + SC_NC - 1) / SC_NC, w.Wb);
+  const int r = w.rs;
+  if (r <= 1) k_scale<1><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 2) k_scale<2><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 3) k_scale<3><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 4) k_scale<4><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 6) k_scale<6><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 8) k_scale<8><<<grid, SC_NC, 0, s>>>(g, w);
+  else if (r <= 16) k_scale<16><<<grid, SC_NC, 0, s>>>(g, w);
+  else k_scale<32><<<grid, SC_NC, 0, s>>>(g, w);
+}
+}  // namespace
+
 namespace {
 
 template <int CPT, int TPT, int TX, int TY, int RC, int MINB, int PASS>
@@ -346,7 +467,7 @@ void launch_single_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
   const int ctiles = PASS == PASS_TOP ? 1 : (g.N1 + NC - 1) / NC;
-  dim3 grid(ctiles, PASS == PASS_SCALE ? 1 : (w.T + TT - 1) / TT, w.Wb);
+  dim3 grid(ctiles, (w.T + TT - 1) / TT, w.Wb);
   k_single<CPT, TPT, TX, TY, RC, MINB, PASS><<<grid, TX * TY, dyn, s>>>(g, c, w);
 }
 
@@ -366,8 +487,8 @@ void launch_pass(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t 
 void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   if (g.N1 == 0 || g.M == 0) return;
   if (w.ranked) {
-    // exact per-case scale and ranking key, then the top tile by key
-    launch_single_t<1, 1, 256, 1, 32, 3, PASS_SCALE>(g, c, w, s);
+    // per-case scale bound and ranking key, then the top tile by key
+    launch_scale(g, w, s);
     launch_topk(g, w, s);
   }
   launch_pass<PASS_TOP>(g, c, w, s);

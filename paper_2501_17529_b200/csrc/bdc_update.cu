@@ -53,9 +53,7 @@ struct UpdShared {
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
   double act_sp[ACTMAX];
   int nisl;
-  unsigned tmax[1024];  // per-candidate N-0 max (float bits), one t-chunk
 };
-constexpr int NT0MAX = 1024;
 
 __device__ __forceinline__ int base_col(const DevGrid& g, const UpdShared& s, int col) {
   return col < g.C0 ? col : g.sub_col[s.sub[col - g.C0]];
@@ -480,34 +478,8 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       w.rank[b] = rt;
     }
     __syncthreads();
-    // ---- N-0 contraction (solver.py:575-595): n0 = f0 + B'' y_t on the monitored rows,
-    // stored as FP32 n0/rating for the N-1 stage; its max is the N-0 part of the metric
     if (!s.fail) {
       const int T = w.T, M = g.M;
-      float* n0s = w.n0s + (size_t)b * M * T;
-      for (int tc = 0; tc < T; tc += NT0MAX) {
-        const int tn = min(NT0MAX, T - tc);
-        for (int i = tid; i < tn; i += NT) s.tmax[i] = 0u;
-        __syncthreads();
-        for (int idx = tid; idx < M * tn; idx += NT) {
-          const int p = idx / tn, t = tc + idx % tn;
-          const int row = g.mon_row[p];
-          float sc = 0.f;
-          if (!is_dead(s.dead, nd, row)) {
-            double v = g.f0[row];
-            for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Y[(size_t)j * T + t], v);
-            sc = (float)(v * g.inv_rating[p]);
-          }
-          n0s[(size_t)p * T + t] = sc;
-          atomicMax(&s.tmax[t - tc], __float_as_uint(fabsf(sc)));
-        }
-        __syncthreads();
-        for (int i = tid; i < tn; i += NT) {
-          w.m32[(size_t)b * T + tc + i] = s.tmax[i];
-          w.m0[(size_t)b * T + tc + i] = __uint_as_float(s.tmax[i]);
-        }
-        __syncthreads();
-      }
       // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
       // F = n0 + sum_j Lo[r][j] So[j][t]; columns formed once per task in FP64
       const int NTM = w.NTERM, MT = g.MT, NQ = g.NM + g.NI;
@@ -575,25 +547,6 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
         }
       }
       __syncthreads();
-      // ---- pre-outage flow s(c,t) = n0[r_c][t] of every single case (FP32), read by the
-      // dominance-screen passes and the N-1 sweep (solver.py:612-613, 815) ------------
-      if (g.N1 > 0 && M > 0) {
-        const int lane = tid & 31, wid = tid >> 5;
-        float* s32 = w.s32 + (size_t)b * g.N1 * T;
-        for (int c = wid; c < g.N1; c += NW) {
-          const int rowc = g.sc_row[c];
-          const bool live = w.sc_ok[(size_t)b * g.N1 + c] && !is_dead(s.dead, nd, rowc);
-          for (int t = lane; t < T; t += 32) {
-            float sv = 0.f;
-            if (live) {
-              double v = g.f0[rowc];
-              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + rowc], Y[(size_t)j * T + t], v);
-              sv = (float)v;
-            }
-            s32[(size_t)c * T + t] = sv;
-          }
-        }
-      }
     }
   }
   __syncthreads();
@@ -611,6 +564,123 @@ done:
     int applied = s.k;
     if (s.fail == BDC_TASK_DEGENERATE_SPLIT || s.fail == BDC_TASK_SINGULAR_SPLIT) applied = s.farg;
     atomicAdd(w.bsdf, (unsigned long long)applied);
+  }
+}
+
+// ---- N-0 contraction (solver.py:575-595): n0 = f0 + B'' y_t, emitted for
+//   * every monitored row as FP32 n0/rating (the only per-task tensor the N-1 stage
+//     streams); its max over rows is the N-0 part of the metric (m0, m32), and
+//   * the outaged row of every single case as FP32 n0, s(c,t) = n0[r_c][t]
+//     (solver.py:612-613, 815), 0 for islanded cases.
+// CTA = (task, N0_ROWS emitted rows); a warp takes 4 rows x 128 candidates (4 per
+// lane), so every B'' / Y value it loads feeds 4 DFMAs.  Same FP64 expression as
+// the reference's dgemm column (f0 + sum_j B''_j y_j), rounded once.
+constexpr int N0_ROWS = 128;
+
+template <int TPL>
+__global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
+  const int b = blockIdx.y;
+  if (w.status[b] != 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = g.R, T = w.T, M = g.M, N1 = g.N1, NL = M + N1, rs = w.rs, rt = w.rank[b];
+  const int r0 = blockIdx.x * N0_ROWS, nr = min(NL - r0, N0_ROWS);
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  const double* Y = w.Y + (size_t)b * rs * T;
+  float* n0s = w.n0s + (size_t)b * M * T;
+  float* s32 = w.s32 + (size_t)b * N1 * T;
+  constexpr int TCH = 32 * TPL, RG = 4;
+  extern __shared__ __align__(16) double n0sm[];
+  double* sB = n0sm;                       // [rt][N0_ROWS]  B'' on the CTA's rows
+  double* sY = sB + (size_t)rs * N0_ROWS;  // [rt][TCH]      y_t of the candidate chunk
+  __shared__ double sF0[N0_ROWS], sScl[N0_ROWS];
+  __shared__ int sLive[N0_ROWS];
+  __shared__ int sdead[RMAX];
+  __shared__ unsigned tmax[TCH];
+  const int nd = w.ndead[b];
+  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
+  __syncthreads();
+  // the CTA's emitted rows: monitored positions (n0 / rating) then single cases (n0[r_c])
+  for (int i = tid; i < N0_ROWS; i += NT) {
+    const int li = r0 + i;
+    int row = 0, live = 0;
+    double scl = 1.0;
+    if (li < M) {
+      row = g.mon_row[li];
+      scl = g.inv_rating[li];
+      live = !is_dead(sdead, nd, row);
+    } else if (li < NL) {
+      const int c = li - M;
+      row = g.sc_row[c];
+      live = w.sc_ok[(size_t)b * N1 + c] && !is_dead(sdead, nd, row);
+    }
+    sF0[i] = live ? g.f0[row] : 0.0;
+    sScl[i] = scl;
+    sLive[i] = live;
+    for (int j = 0; j < rt; ++j) {
+      const double bv = i < nr ? Bm[(size_t)j * R + row] : 0.0;
+      sB[j * N0_ROWS + i] = bv;
+      if (li < M) {
+        // FP32 B'' on monitored rows and max_r |B''(r,j)|/rating_r for the scale bound
+        w.B32[((size_t)b * rs + j) * M + li] = (float)bv;
+        if (live)
+          atomicMax(reinterpret_cast<unsigned*>(&w.bmax[(size_t)b * rs + j]),
+                    __float_as_uint((float)(fabs(bv) * scl) * (1.f + 1e-6f)));
+      }
+    }
+  }
+  for (int tc = 0; tc < T; tc += TCH) {
+    for (int i = tid; i < TCH; i += NT) tmax[i] = 0u;
+    for (int idx = tid; idx < rt * TCH; idx += NT) {
+      const int j = idx / TCH, t = tc + idx % TCH;
+      sY[idx] = t < T ? Y[(size_t)j * T + t] : 0.0;
+    }
+    __syncthreads();
+    float mx[TPL];
+#pragma unroll
+    for (int k = 0; k < TPL; ++k) mx[k] = 0.f;
+    for (int i0 = wid * RG; i0 < nr; i0 += NW * RG) {
+      double acc[RG][TPL];
+#pragma unroll
+      for (int i = 0; i < RG; ++i)
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) acc[i][k] = sF0[i0 + i];
+      for (int j = 0; j < rt; ++j) {
+        double bv[RG], yv[TPL];
+#pragma unroll
+        for (int i = 0; i < RG; ++i) bv[i] = sB[j * N0_ROWS + i0 + i];
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) yv[k] = sY[j * TCH + lane + 32 * k];
+#pragma unroll
+        for (int i = 0; i < RG; ++i)
+#pragma unroll
+          for (int k = 0; k < TPL; ++k) acc[i][k] = fma(bv[i], yv[k], acc[i][k]);
+      }
+#pragma unroll
+      for (int i = 0; i < RG; ++i) {
+        const int li = r0 + i0 + i;
+        if (i0 + i >= nr) break;
+        float* dst = li < M ? n0s + (size_t)li * T : s32 + (size_t)(li - M) * T;
+        const bool live = sLive[i0 + i] != 0;
+        const double scl = sScl[i0 + i];
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) {
+          const int t = tc + lane + 32 * k;
+          if (t >= T) continue;
+          const float v = live ? (float)(acc[i][k] * scl) : 0.f;
+          dst[t] = v;
+          if (li < M) mx[k] = fmaxf(mx[k], fabsf(v));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < TPL; ++k) atomicMax(&tmax[lane + 32 * k], __float_as_uint(mx[k]));
+    __syncthreads();
+    if (r0 < M)  // CTAs with monitored rows fold their per-candidate max into m0 / m32
+      for (int i = tid; i < min(TCH, T - tc); i += NT) {
+        atomicMax(&w.m32[(size_t)b * T + tc + i], tmax[i]);
+        atomicMax(reinterpret_cast<unsigned*>(&w.m0[(size_t)b * T + tc + i]), tmax[i]);
+      }
+    __syncthreads();
   }
 }
 
@@ -683,6 +753,25 @@ __global__ void __launch_bounds__(NT) k_topk(DevGrid g, Work w) {
 
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t st) {
   k_update<<<w.Wb, NT, 0, st>>>(g, c, w);
+}
+
+void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
+  const int NL = g.M + g.N1;
+  if (NL == 0) return;
+  const dim3 grid((NL + N0_ROWS - 1) / N0_ROWS, w.Wb);
+  const int tpl = w.T > 64 ? 4 : (w.T > 32 ? 2 : 1);
+  const size_t dyn = (size_t)w.rs * (N0_ROWS + 32 * tpl) * sizeof(double);
+  static bool init = false;
+  if (!init) {
+    const int mx = RMAX * (N0_ROWS + 128) * sizeof(double);
+    cudaFuncSetAttribute(k_n0<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_n0<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_n0<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    init = true;
+  }
+  if (tpl == 4) k_n0<4><<<grid, NT, dyn, st>>>(g, w);
+  else if (tpl == 2) k_n0<2><<<grid, NT, dyn, st>>>(g, w);
+  else k_n0<1><<<grid, NT, dyn, st>>>(g, w);
 }
 
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t st) {
