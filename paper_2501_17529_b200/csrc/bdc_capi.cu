@@ -307,6 +307,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
   size_t o_b32 = L.add(B * (size_t)rs * g.M * 4), o_bmx = L.add(B * (size_t)rs * 4);
+  size_t o_smx = L.add(B * (size_t)g.N1 * 4);
   size_t o_lf = L.add(32), o_bs = L.add(16);
   if (!base) return L.total;
   Work& x = *w;
@@ -340,7 +341,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = single_tile_cases(T);
-  x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx);
+  x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
   x.alive = (uint8_t*)(base + o_alive); x.nct = nct; x.ntt = ntt;
   x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.nslot = nslot;
   x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);

@@ -106,7 +106,8 @@ struct Work {
   int ptop;       // cases evaluated first (the top tile by screening bound)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
   float* s32;     // (Wb, N1, T)   n0[r_c][t] (pre-outage flow of each single case), FP32
-  uint32_t* bkey; // (Wb, N1)      max_t bound(c, t) as float bits (ranking key)
+  uint32_t* bkey; // (Wb, N1)      ranking key max_t m0(t) + scale_c max_t |s(c,t)| (float bits)
+  float* smax;    // (Wb, N1)      max_t |s(c,t)|
   int* top;       // (Wb, ptop)    the ptop cases with the largest bound, ascending index
   uint8_t* done;  // (Wb, N1)      1 if the case is in top (evaluated in the first pass)
   // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j],

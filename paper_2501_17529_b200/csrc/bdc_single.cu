@@ -316,61 +316,85 @@ constexpr int SC_NC = 256, SC_RC = 16;  // static shared memory stays under 48 K
 }
 
 // RS = rank bucket >= every task's rank in the wave: W in registers, B'' terms past a
-// task's own rank are zero-filled, so the inner loop is straight-line FFMAs.
-template <int RS>
+// task's own rank are zero-filled, so the inner loop is straight-line FFMAs.  TB tasks
+// share a CTA: the D_base chunk (the shared operand) is staged and read once for all.
+template <int RS, int TB>
 __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
-  const int b = blockIdx.y;
-  if (w.status[b] != 0) return;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tb0 = blockIdx.y * TB;
+  const int tid = threadIdx.x;
   const int c0 = blockIdx.x * SC_NC, c = c0 + tid < g.N1 ? c0 + tid : -1;
-  const int rs = w.rs, rt = w.rank[b], M = g.M, N1 = g.N1, T = w.T;
+  const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
   __shared__ __align__(16) float sD[2][SC_RC][SC_NC];
-  __shared__ __align__(16) float sB[2][RS][SC_RC];
-  __shared__ float sInv[2][SC_RC];
-  __shared__ float sU[SC_NC];
-  __shared__ int sdead[RMAX];
-  const int nd = w.ndead[b];
-  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
-  __syncthreads();
-  bool ok = false;
-  int ownp = -1;
-  float wsum = 0.f;
-  double idn = 0.0;
-  float wr[RS];
-#pragma unroll
-  for (int j = 0; j < RS; ++j) wr[j] = 0.f;
-  if (c >= 0) {
-    ok = w.sc_ok[(size_t)b * N1 + c] != 0;
-    idn = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
-    const int rowc = g.sc_row[c];
-    ownp = is_dead(sdead, nd, rowc) ? -1 : g.row_mon_pos[rowc];
-#pragma unroll
-    for (int j = 0; j < RS; ++j)
-      if (j < rt) {
-        const double wv = w.Wsc[((size_t)b * N1 + c) * rs + j];
-        wr[j] = (float)wv;
-        wsum += (float)fabs(wv) * w.bmax[(size_t)b * rs + j];
-      }
+  __shared__ __align__(16) float sB[2][TB][RS][SC_RC];
+  __shared__ __align__(16) float sInv[2][TB][SC_RC];
+  __shared__ int sdead[TB][RMAX];
+  __shared__ int snd[TB], srt[TB];
+  __shared__ float sm0[TB];
+  if (tid < TB) {
+    const int b = tb0 + tid;
+    const bool on = b < w.Wb && w.status[b] == 0;
+    snd[tid] = on ? w.ndead[b] : 0;
+    srt[tid] = on ? w.rank[b] : -1;  // -1: slot idle
+    sm0[tid] = 0.f;
   }
-  const float* B32 = w.B32 + (size_t)b * rs * M;
+  __syncthreads();
+  for (int i = tid; i < TB * RMAX; i += SC_NC) {
+    const int k = i / RMAX, d = i % RMAX;
+    if (d < snd[k]) sdead[k][d] = w.dead[(size_t)(tb0 + k) * RMAX + d];
+  }
+  // max_t m0(t) of each task (ranking key)
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int k = wid; k < TB; k += SC_NC / 32) {
+      if (srt[k] < 0) continue;
+      float v = 0.f;
+      for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0[(size_t)(tb0 + k) * T + t]);
+      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) sm0[k] = v;
+    }
+  }
+  __syncthreads();
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < TB; ++k) any |= srt[k] >= 0;
+  if (!any) return;
+  float wr[TB][RS];
+#pragma unroll
+  for (int k = 0; k < TB; ++k)
+#pragma unroll
+    for (int j = 0; j < RS; ++j) wr[k][j] = 0.f;
+  if (c >= 0) {
+#pragma unroll
+    for (int k = 0; k < TB; ++k) {
+      const int b = tb0 + k;
+#pragma unroll
+      for (int j = 0; j < RS; ++j)
+        if (j < srt[k]) wr[k][j] = (float)w.Wsc[((size_t)b * N1 + c) * rs + j];
+    }
+  }
   auto issue = [&](int m0, int buf) {
     for (int idx = tid; idx < SC_RC * (SC_NC / 4); idx += SC_NC) {
       const int rr = idx / (SC_NC / 4), q = 4 * (idx % (SC_NC / 4)), m = m0 + rr;
       const bool okd = m < M && c0 + q < g.N1p;  // rows are zero-padded to N1p
       cp16(&sD[buf][rr][q], okd ? &g.D32[(size_t)m * g.N1p + c0 + q] : g.D32, okd);
     }
-    for (int idx = tid; idx < RS * SC_RC; idx += SC_NC) {
-      const int j = idx / SC_RC, rr = idx % SC_RC, m = m0 + rr;
-      const bool okb = m < M && j < rt;  // zero-fill terms past the task's rank
-      cp4(&sB[buf][j][rr], okb ? &B32[(size_t)j * M + m] : B32, okb);
+    for (int idx = tid; idx < TB * RS * SC_RC; idx += SC_NC) {
+      const int k = idx / (RS * SC_RC), j = (idx / SC_RC) % RS, rr = idx % SC_RC, m = m0 + rr;
+      const bool okb = m < M && j < srt[k];  // zero-fill terms past the task's rank
+      const float* src = w.B32 + ((size_t)(tb0 + k) * rs + j) * M + m;
+      cp4(&sB[buf][k][j][rr], okb ? src : w.B32, okb);
     }
-    if (tid < SC_RC) {
-      const int m = m0 + tid;
-      sInv[buf][tid] = (m < M && !is_dead(sdead, nd, g.mon_row[m])) ? (float)g.inv_rating[m] : 0.f;
+    for (int idx = tid; idx < TB * SC_RC; idx += SC_NC) {
+      const int k = idx / SC_RC, rr = idx % SC_RC, m = m0 + rr;
+      sInv[buf][k][rr] = (m < M && srt[k] >= 0 && !is_dead(sdead[k], snd[k], g.mon_row[m]))
+                             ? (float)g.inv_rating[m] : 0.f;
     }
     cp_commit();
   };
-  float mx = 0.f;
+  float mx[TB];
+#pragma unroll
+  for (int k = 0; k < TB; ++k) mx[k] = 0.f;
+  const int ownp = c >= 0 ? g.row_mon_pos[g.sc_row[c]] : -1;
   issue(0, 0);
   const int nchunks = (M + SC_RC - 1) / SC_RC;
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -385,65 +409,69 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
     const int ownrr = ownp - m0;
 #pragma unroll 2
     for (int r4 = 0; r4 < SC_RC; r4 += 4) {
-      float l[4];
+      float d[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) l[k] = sD[buf][r4 + k][tid];
+      for (int q = 0; q < 4; ++q) d[q] = sD[buf][r4 + q][tid];
 #pragma unroll
-      for (int j = 0; j < RS; ++j) {
-        const float4 bq = *reinterpret_cast<const float4*>(&sB[buf][j][r4]);
-        l[0] = fmaf(bq.x, wr[j], l[0]);
-        l[1] = fmaf(bq.y, wr[j], l[1]);
-        l[2] = fmaf(bq.z, wr[j], l[2]);
-        l[3] = fmaf(bq.w, wr[j], l[3]);
+      for (int k = 0; k < TB; ++k) {
+        float l0 = d[0], l1 = d[1], l2 = d[2], l3 = d[3];
+#pragma unroll
+        for (int j = 0; j < RS; ++j) {
+          const float4 bq = *reinterpret_cast<const float4*>(&sB[buf][k][j][r4]);
+          l0 = fmaf(bq.x, wr[k][j], l0);
+          l1 = fmaf(bq.y, wr[k][j], l1);
+          l2 = fmaf(bq.z, wr[k][j], l2);
+          l3 = fmaf(bq.w, wr[k][j], l3);
+        }
+        const float4 iq = *reinterpret_cast<const float4*>(&sInv[buf][k][r4]);
+        mx[k] = fmaxf(mx[k], (r4 + 0 == ownrr) ? 0.f : fabsf(l0) * iq.x);
+        mx[k] = fmaxf(mx[k], (r4 + 1 == ownrr) ? 0.f : fabsf(l1) * iq.y);
+        mx[k] = fmaxf(mx[k], (r4 + 2 == ownrr) ? 0.f : fabsf(l2) * iq.z);
+        mx[k] = fmaxf(mx[k], (r4 + 3 == ownrr) ? 0.f : fabsf(l3) * iq.w);
       }
-      const float4 iq = *reinterpret_cast<const float4*>(&sInv[buf][r4]);
-      const float v0 = fabsf(l[0]) * iq.x, v1 = fabsf(l[1]) * iq.y;
-      const float v2 = fabsf(l[2]) * iq.z, v3 = fabsf(l[3]) * iq.w;
-      mx = fmaxf(mx, (r4 + 0 == ownrr) ? 0.f : v0);
-      mx = fmaxf(mx, (r4 + 1 == ownrr) ? 0.f : v1);
-      mx = fmaxf(mx, (r4 + 2 == ownrr) ? 0.f : v2);
-      mx = fmaxf(mx, (r4 + 3 == ownrr) ? 0.f : v3);
     }
     __syncthreads();
   }
-  float U = 0.f;
-  if (c >= 0 && ok) {
-    const float gam = (float)(rt + 8) * 1.1920929e-7f;
-    U = (float)fabs(idn) * (mx + gam * ((float)g.sc_dscale[c] + wsum));
-    if (ownp >= 0) U = fmaxf(U, (float)g.inv_rating[ownp]);
-    U *= 1.f + 4e-6f;
-  }
-  sU[tid] = U;
-  __syncthreads();
-  // ranking key: warp per case
-  const float* m0v = w.m0 + (size_t)b * T;
-  for (int cc = wid; cc < SC_NC; cc += SC_NC / 32) {
-    const int cx = c0 + cc;
-    if (cx >= N1) break;
-    const float sc = sU[cc];
-    const float* sv = w.s32 + ((size_t)b * N1 + cx) * T;
-    float bm = 0.f;
-    for (int t = lane; t < T; t += 32) bm = fmaxf(bm, m0v[t] + sc * fabsf(sv[t]));
-    for (int o = 16; o; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-    if (lane == 0) {
-      w.scale[(size_t)b * N1 + cx] = sc;
-      w.bkey[(size_t)b * N1 + cx] = w.sc_ok[(size_t)b * N1 + cx] ? __float_as_uint(bm) : 0u;
+  if (c < 0) return;
+#pragma unroll
+  for (int k = 0; k < TB; ++k) {
+    const int b = tb0 + k, rt = srt[k];
+    if (rt < 0) continue;
+    const bool ok = w.sc_ok[(size_t)b * N1 + c] != 0;
+    float U = 0.f;
+    if (ok) {
+      const double idn = 1.0 / w.den[(size_t)b * N1 + c];
+      float wsum = 0.f;
+      for (int j = 0; j < rt; ++j)
+        wsum += (float)fabs(w.Wsc[((size_t)b * N1 + c) * rs + j]) * w.bmax[(size_t)b * rs + j];
+      const float gam = (float)(rt + 8) * 1.1920929e-7f;
+      U = (float)fabs(idn) * (mx[k] + gam * ((float)g.sc_dscale[c] + wsum));
+      const int rowc = g.sc_row[c];
+      if (ownp >= 0 && !is_dead(sdead[k], snd[k], rowc)) U = fmaxf(U, (float)g.inv_rating[ownp]);
+      U *= 1.f + 4e-6f;
     }
+    w.scale[(size_t)b * N1 + c] = U;
+    // ranking key for the TOP tile (ordering only; exactness rests on the per-pair bound)
+    w.bkey[(size_t)b * N1 + c] = ok ? __float_as_uint(sm0[k] + U * w.smax[(size_t)b * N1 + c]) : 0u;
   }
 }
 
 namespace {
+template <int RS, int TB>
+void launch_scale_t(const DevGrid& g, const Work& w, cudaStream_t s) {
+  const dim3 grid((g.N1 + SC_NC - 1) / SC_NC, (w.Wb + TB - 1) / TB);
+  k_scale<RS, TB><<<grid, SC_NC, 0, s>>>(g, w);
+}
 void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
-  const dim3 grid((g.N1 + SC_NC - 1) / SC_NC, w.Wb);
   const int r = w.rs;
-  if (r <= 1) k_scale<1><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 2) k_scale<2><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 3) k_scale<3><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 4) k_scale<4><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 6) k_scale<6><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 8) k_scale<8><<<grid, SC_NC, 0, s>>>(g, w);
-  else if (r <= 16) k_scale<16><<<grid, SC_NC, 0, s>>>(g, w);
-  else k_scale<32><<<grid, SC_NC, 0, s>>>(g, w);
+  if (r <= 1) launch_scale_t<1, 4>(g, w, s);
+  else if (r <= 2) launch_scale_t<2, 4>(g, w, s);
+  else if (r <= 3) launch_scale_t<3, 4>(g, w, s);
+  else if (r <= 4) launch_scale_t<4, 4>(g, w, s);
+  else if (r <= 6) launch_scale_t<6, 4>(g, w, s);
+  else if (r <= 8) launch_scale_t<8, 2>(g, w, s);
+  else if (r <= 16) launch_scale_t<16, 1>(g, w, s);
+  else launch_scale_t<32, 1>(g, w, s);
 }
 }  // namespace
 

@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   double* sY = sB + (size_t)rs * N0_ROWS;  // [rt][TCH]      y_t of the candidate chunk
   __shared__ double sF0[N0_ROWS], sScl[N0_ROWS];
   __shared__ int sLive[N0_ROWS];
+  __shared__ float sSmax[N0_ROWS];  // max_t |s(c,t)| of the CTA's single-case rows
   __shared__ int sdead[RMAX];
   __shared__ unsigned tmax[TCH];
   const int nd = w.ndead[b];
@@ -615,6 +616,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
     }
     sF0[i] = live ? g.f0[row] : 0.0;
     sScl[i] = scl;
+    sSmax[i] = 0.f;
     sLive[i] = live;
     for (int j = 0; j < rt; ++j) {
       const double bv = i < nr ? Bm[(size_t)j * R + row] : 0.0;
@@ -662,6 +664,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
         float* dst = li < M ? n0s + (size_t)li * T : s32 + (size_t)(li - M) * T;
         const bool live = sLive[i0 + i] != 0;
         const double scl = sScl[i0 + i];
+        float rmax = 0.f;
 #pragma unroll
         for (int k = 0; k < TPL; ++k) {
           const int t = tc + lane + 32 * k;
@@ -669,6 +672,11 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
           const float v = live ? (float)(acc[i][k] * scl) : 0.f;
           dst[t] = v;
           if (li < M) mx[k] = fmaxf(mx[k], fabsf(v));
+          rmax = fmaxf(rmax, fabsf(v));
+        }
+        if (li >= M) {  // warp-uniform: the row's max over this candidate chunk
+          for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+          if (lane == 0) sSmax[i0 + i] = fmaxf(sSmax[i0 + i], rmax);
         }
       }
     }
@@ -682,6 +690,8 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
       }
     __syncthreads();
   }
+  for (int i = tid; i < nr; i += NT)
+    if (r0 + i >= M) w.smax[(size_t)b * N1 + (r0 + i - M)] = sSmax[i];
 }
 
 // The ptop single cases with the largest screening bound bkey_c (the cases the
