@@ -301,7 +301,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_top = L.add(B * (size_t)PTOP_MAX * 4), o_done = L.add(B * (size_t)g.N1);
   const SweepShape sh = sweep_shape(T);
   const int nct = (g.N1 + sh.CPT * sh.TX - 1) / (sh.CPT * sh.TX), ntt = (T + sh.TPT * sh.TY - 1) / (sh.TPT * sh.TY);
-  const int nslot = 1 + (g.N1 + RCW - 1) / RCW;
+  const int nslot = RSEL_WARPS + (g.N1 + RCW - 1) / RCW;
   size_t o_alive = L.add(B * (size_t)nct * ntt * SWEEP_WARPS);
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);

@@ -43,6 +43,7 @@ inline int single_tile_cases(int T) {
 }
 constexpr int SWEEP_WARPS = 8;  // warps per sweep CTA (256 threads)
 constexpr int RCW = 128;        // single cases per CTA of the winner report sweep
+constexpr int RSEL_WARPS = 8;   // partial report lists written by the report-select kernel
 
 // Grid tables, device-resident for the session lifetime.
 struct DevGrid {
@@ -119,7 +120,7 @@ struct Work {
   // winner report: listed cases and per-slot partial top-kg lists
   int* rlist;     // (Wb, N1)      single cases the FP64 report must visit, ascending
   int* rcnt;      // (Wb)          their number
-  int nslot;      // 1 + ceil(N1 / RCW) partial lists per task
+  int nslot;      // RSEL_WARPS + ceil(N1 / RCW) partial lists per task
   int* pcase;     // (Wb, nslot, KMAX) contingency order of each partial entry
   int* ppos;      // (Wb, nslot, KMAX) monitored position
   double* pflow;  // (Wb, nslot, KMAX)

@@ -20,6 +20,7 @@ namespace {
 
 constexpr int RT = 256;
 constexpr int RW = RT / 32;
+static_assert(RW == RSEL_WARPS, "k_rsel writes one partial list per warp");
 
 __device__ __forceinline__ bool better(double r1, int p1, double r2, int p2) {
   return r1 > r2 || (r1 == r2 && p1 < p2);
@@ -105,6 +106,66 @@ __device__ void warp_merge(LaneTop<KC>& lt, int kc, WarpList& L, int kg, int cas
 }
 
 
+// Top-kg of this warp's strided subset {i = wid*32 + lane + k*RT, i < n} by
+// (value desc, index asc), kg rounds of warp argmax (no block barriers); value(i) < 0
+// excludes i.  Lane 0 writes the picks to ov/oi; returns their number.
+template <class F>
+__device__ int warp_topk(int n, int kg, F value, double* ov, int* oi) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double pv = 1e300;
+  int pi = -1, cnt = 0;
+  for (int r = 0; r < kg; ++r) {
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int i = wid * 32 + lane; i < n; i += RT) {
+      const double v = value(i);
+      if (v < 0.0 || !(v < pv || (v == pv && i > pi))) continue;
+      if (better(v, i, bv, bi)) { bv = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov2, oi2, bv, bi)) { bv = ov2; bi = oi2; }
+    }
+    if (bv < 0.0) break;
+    if (lane == 0) { ov[r] = bv; oi[r] = bi; }
+    pv = bv; pi = bi;
+    ++cnt;
+  }
+  return cnt;
+}
+
+// Merge RW warp lists (lv/li rows of stride KMAX, counts ln) into the top-kg by
+// (value desc, index asc); one warp, kg rounds.  Lane 0 writes ov/oi; returns count.
+__device__ int warp_merge_lists(const double (*lv)[KMAX], const int (*li)[KMAX], const int* ln, int kg,
+                                double* ov, int* oi) {
+  const int lane = threadIdx.x & 31;
+  double pv = 1e300;
+  int pi = -1, cnt = 0;
+  for (int r = 0; r < kg; ++r) {
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int e = lane; e < RW * KMAX; e += 32) {
+      const int wq = e / KMAX, k = e % KMAX;
+      if (k >= ln[wq]) continue;
+      const double v = lv[wq][k];
+      const int i = li[wq][k];
+      if (!(v < pv || (v == pv && i > pi))) continue;
+      if (better(v, i, bv, bi)) { bv = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov2, oi2, bv, bi)) { bv = ov2; bi = oi2; }
+    }
+    if (bv < 0.0) break;
+    if (lane == 0) { ov[r] = bv; oi[r] = bi; }
+    pv = bv; pi = bi;
+    ++cnt;
+  }
+  return cnt;
+}
+
 // Was the (single case c, candidate t) pair evaluated by the N-1 sweep, i.e. is
 // cmax[c][t] its exact FP32 maximum?  Cases of the TOP tile always are; in the
 // screened sweep it depends on the warp that owned the pair (bdc_single.cu).
@@ -158,19 +219,19 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   const double* Bm = w.Bm + (size_t)b * rs * R;
   __shared__ WarpList wl[RW];
   __shared__ int sdead[RMAX];
-  __shared__ double sred[RW];
-  __shared__ double sbr[2][RW];
-  __shared__ int sbp[2][RW];
   __shared__ double sMinv[RW][MMAX * MMAX];
   __shared__ double sY[RMAX];
-  __shared__ int sN0pos[KMAX];
-  __shared__ int wcnt[RW];
-  __shared__ int sCnt;
+  __shared__ double lv[2][RW][KMAX];  // per-warp top lists: [0] N-0 rows, [1] case maxima
+  __shared__ int li[2][RW][KMAX];
+  __shared__ int ln[2][RW];
+  __shared__ double mv[KMAX];
+  __shared__ int mi[KMAX];
+  __shared__ int wcnt[RW], woff[RW];
+  __shared__ float sTheta;
   const int nd = w.ndead[b];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   if (tid < rt) sY[tid] = w.Y[((size_t)b * rs + tid) * T + best];
   if (lane == 0) wl[wid].n = 0;
-  if (tid == 0) sCnt = 0;
   __syncthreads();
   // the winner's N-0 column, FP64, from the factors
   for (int r = tid; r < R; r += RT) {
@@ -183,53 +244,7 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   }
   __syncthreads();
 
-  double mymax = 0.0;
-  // ---- N-0 report: kg rounds of block argmax (one barrier per round) ----------------
-  {
-    double pr = 1e300;
-    int pp = -1;
-    int n0n = 0;
-    for (int round = 0; round < kg; ++round) {
-      double br = -1.0;
-      int bp = INT_MAX;
-      for (int p = tid; p < M; p += RT) {
-        const int row = g.mon_row[p];
-        const double rel = fabs(n0b[row]) * g.inv_rating[p];
-        if (round == 0) mymax = fmax(mymax, rel);
-        if (is_dead(sdead, nd, row)) continue;
-        // next entry in (rel desc, pos asc) order after the previous pick
-        if (!(rel < pr || (rel == pr && p > pp))) continue;
-        if (better(rel, p, br, bp)) { br = rel; bp = p; }
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (better(orr, op, br, bp)) { br = orr; bp = op; }
-      }
-      const int sl = round & 1;
-      if (lane == 0) { sbr[sl][wid] = br; sbp[sl][wid] = bp; }
-      __syncthreads();
-      br = sbr[sl][0]; bp = sbp[sl][0];
-      for (int i = 1; i < RW; ++i)
-        if (better(sbr[sl][i], sbp[sl][i], br, bp)) { br = sbr[sl][i]; bp = sbp[sl][i]; }
-      if (br < 0.0) break;
-      if (tid == 0) sN0pos[round] = bp;
-      pr = br; pp = bp;
-      ++n0n;
-    }
-    if (tid == 0) {
-      w.n0cnt[b] = n0n;
-      for (int i = 0; i < n0n; ++i) {
-        const int p = sN0pos[i];
-        const double f = n0b[g.mon_row[p]];
-        w.n0pos[(size_t)b * kg + i] = p;
-        w.n0flow[(size_t)b * kg + i] = f;
-        w.n0rel[(size_t)b * kg + i] = fabs(f) * g.inv_rating[p];
-      }
-    }
-  }
-
-  // ---- which contingencies can matter ------------------------------------------------------
+  // ---- per-warp candidates: N-0 report rows and the largest exact case maxima -------------
   const int N1 = g.N1, ncase = N1 + g.NM + g.NI;
   const float* cm = w.cmax + (size_t)b * ncase * T + best;
   const float m0b = w.m0[(size_t)b * T + best];
@@ -247,57 +262,85 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
     ub = m0b + w.scale[(size_t)b * N1 + ci] * fabsf(w.s32[((size_t)b * N1 + ci) * T + best]);
     return -1.f;
   };
-  float theta = -1.f;
+  double mymax = 0.0;
+  for (int p = tid; p < M; p += RT) mymax = fmax(mymax, fabs(n0b[g.mon_row[p]]) * g.inv_rating[p]);
   {
-    float pv = 3.4e38f;
-    int pi = -1, found = 0;
-    float kth = -1.f;
-    for (int round = 0; round < kg; ++round) {
-      double br = -1.0;
-      int bp = INT_MAX;
-      for (int ci = tid; ci < ncase; ci += RT) {
-        if (!feasible_case(ci)) continue;
-        float ub;
-        const float v = case_value(ci, ub);
-        if (v < 0.f) continue;  // only an upper bound is known
-        if (!(v < pv || (v == pv && ci > pi))) continue;
-        if (better(v, ci, br, bp)) { br = v; bp = ci; }
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (better(orr, op, br, bp)) { br = orr; bp = op; }
-      }
-      const int sl = round & 1;
-      if (lane == 0) { sbr[sl][wid] = br; sbp[sl][wid] = bp; }
-      __syncthreads();
-      br = sbr[sl][0]; bp = sbp[sl][0];
-      for (int i = 1; i < RW; ++i)
-        if (better(sbr[sl][i], sbp[sl][i], br, bp)) { br = sbr[sl][i]; bp = sbp[sl][i]; }
-      if (br < 0.0) break;
-      pv = (float)br; pi = bp; kth = (float)br;
-      ++found;
-    }
-    theta = found == kg ? kth - 2.f * SCREEN_EPS : -1.f;
-  }
-  // single cases to visit, ascending (the sweep kernel evaluates them in FP64)
-  int* rl = w.rlist + (size_t)b * N1;
-  for (int c0 = 0; c0 < N1; c0 += RT) {
-    const int c = c0 + tid;
-    bool take = false;
-    if (c < N1 && feasible_case(c)) {
+    const int n = warp_topk(M, kg, [&](int p) -> double {
+      const int row = g.mon_row[p];
+      return is_dead(sdead, nd, row) ? -1.0 : fabs(n0b[row]) * g.inv_rating[p];
+    }, lv[0][wid], li[0][wid]);
+    if (lane == 0) ln[0][wid] = n;
+    const int n2 = warp_topk(ncase, kg, [&](int ci) -> double {
+      if (!feasible_case(ci)) return -1.0;
       float ub;
-      case_value(c, ub);
-      take = ub >= theta;
-    }
-    int total;
-    const int pos = block_rank(take, wcnt, total);
-    if (take) rl[sCnt + pos] = c;
-    __syncthreads();
-    if (tid == 0) sCnt += total;
-    __syncthreads();
+      return (double)case_value(ci, ub);
+    }, lv[1][wid], li[1][wid]);
+    if (lane == 0) ln[1][wid] = n2;
   }
-  if (tid == 0) w.rcnt[b] = sCnt;
+  __syncthreads();
+  if (wid == 0) {
+    // N-0 report: top-kg rows by (rel desc, position asc) (_top_rows, solver.py:287-299)
+    const int n = warp_merge_lists(lv[0], li[0], ln[0], kg, mv, mi);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int p = mi[i];
+      const double f = n0b[g.mon_row[p]];
+      w.n0pos[(size_t)b * kg + i] = p;
+      w.n0flow[(size_t)b * kg + i] = f;
+      w.n0rel[(size_t)b * kg + i] = fabs(f) * g.inv_rating[p];
+    }
+    if (lane == 0) w.n0cnt[b] = n;
+  } else if (wid == 1) {
+    // Exact pruning: an entry of case c can enter the final top-kg only if c's true max
+    // loading is >= the kg-th largest true case max.  FP32 maxima are within SCREEN_EPS
+    // of FP64, so with kth = the kg-th largest exact FP32 maximum, every case whose upper
+    // bound (exact FP32 max, or the dominance bound m0 + scale_c |s(c,t)| of a pair the
+    // sweep skipped) is >= kth - 2 eps is visited; the metric's binding case is one of them.
+    __shared__ double tv[KMAX];
+    __shared__ int ti[KMAX];
+    const int n = warp_merge_lists(lv[1], li[1], ln[1], kg, tv, ti);
+    __syncwarp();
+    if (lane == 0) sTheta = n == kg ? (float)tv[kg - 1] - 2.f * SCREEN_EPS : -1.f;
+  }
+  __syncthreads();
+  const float theta = sTheta;
+  // single cases to visit, ascending: warp-contiguous segments, ordered compaction
+  {
+    const int seg = (N1 + RW - 1) / RW, s0 = wid * seg, s1 = min(N1, s0 + seg);
+    int cnt = 0;
+    for (int c0 = s0; c0 < s1; c0 += 32) {
+      const int c = c0 + lane;
+      bool take = false;
+      if (c < s1 && feasible_case(c)) {
+        float ub;
+        case_value(c, ub);
+        take = ub >= theta;
+      }
+      cnt += __popc(__ballot_sync(0xffffffffu, take));
+    }
+    if (lane == 0) wcnt[wid] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int i = 0; i < RW; ++i) { woff[i] = acc; acc += wcnt[i]; }
+      w.rcnt[b] = acc;
+    }
+    __syncthreads();
+    int* rl = w.rlist + (size_t)b * N1;
+    int off = woff[wid];
+    for (int c0 = s0; c0 < s1; c0 += 32) {
+      const int c = c0 + lane;
+      bool take = false;
+      if (c < s1 && feasible_case(c)) {
+        float ub;
+        case_value(c, ub);
+        take = ub >= theta;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (take) rl[off + __popc(bal & ((1u << lane) - 1u))] = c;
+      off += __popc(bal);
+    }
+  }
 
   // ---- multi-branch and injection cases of the report (FP64, warp per case) --------------
   LaneTop<KC> lt;
@@ -364,26 +407,17 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
     warp_merge<KC>(lt, kc, wl[wid], kg, order);
     __syncwarp();
   }
+  // each warp's list and max is one partial slot (merged by k_rmerge)
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
-  if (lane == 0) sred[wid] = mymax;
-  __syncthreads();
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int i = 0; i < RW; ++i) mx = fmax(mx, sred[i]);
-    WarpList& F = wl[0];
-    for (int i = 1; i < RW; ++i)
-      for (int e = 0; e < wl[i].n; ++e)
-        wl_insert(F, kg, wl[i].rel[e], wl[i].cs[e], wl[i].pos[e], wl[i].flow[e]);
-    const size_t o = (size_t)b * w.nslot * KMAX;
-    for (int e = 0; e < kg; ++e) {
-      const bool has = e < F.n;
-      w.pcase[o + e] = has ? F.cs[e] : INT_MAX;
-      w.ppos[o + e] = has ? F.pos[e] : INT_MAX;
-      w.pflow[o + e] = has ? F.flow[e] : 0.0;
-      w.prel[o + e] = has ? F.rel[e] : -1.0;
-    }
-    w.pmax[(size_t)b * w.nslot] = mx;
+  const size_t o = ((size_t)b * w.nslot + wid) * KMAX;
+  for (int e = lane; e < kg; e += 32) {
+    const bool has = e < wl[wid].n;
+    w.pcase[o + e] = has ? wl[wid].cs[e] : INT_MAX;
+    w.ppos[o + e] = has ? wl[wid].pos[e] : INT_MAX;
+    w.pflow[o + e] = has ? wl[wid].flow[e] : 0.0;
+    w.prel[o + e] = has ? wl[wid].rel[e] : -1.0;
   }
+  if (lane == 0) w.pmax[(size_t)b * w.nslot + wid] = mymax;
 }
 
 // --------------------------------------------------------------------------- k_rsweep
@@ -475,7 +509,7 @@ __global__ void __launch_bounds__(RCW) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if (lane == 0) wr[wid] = mymax;
   __syncthreads();
-  const int slot = 1 + tile;
+  const int slot = RSEL_WARPS + tile;
   const size_t o = ((size_t)b * w.nslot + slot) * KMAX;
   if (tid == 0) {
     double mx = 0.0;
@@ -528,7 +562,7 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
   const int b = gt >> 5, lane = gt & 31;
   if (b >= w.Wb || w.status[b] != 0) return;
   const int kg = cfg.kg;
-  const int nsl = 1 + (w.rcnt[b] + RCW - 1) / RCW;
+  const int nsl = RSEL_WARPS + (w.rcnt[b] + RCW - 1) / RCW;
   double mx = 0.0;
   for (int s = lane; s < nsl; s += 32) mx = fmax(mx, w.pmax[(size_t)b * w.nslot + s]);
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -655,7 +689,7 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
                            (int)(((size_t)RMAX * RCW + (size_t)RMAX * SRC) * sizeof(double)));
       init = true;
     }
-    k_rsweep<KC><<<dim3(w.nslot - 1, w.Wb), RCW, dyn, s>>>(g, c, w);
+    k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RCW, dyn, s>>>(g, c, w);
   }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
