@@ -178,21 +178,6 @@ __device__ __forceinline__ bool pair_evaluated(const DevGrid& g, const Work& w, 
   return w.alive[(((size_t)b * w.nct + ct) * w.ntt + tt) * SWEEP_WARPS + warp] != 0;
 }
 
-// Ordered block-wide compaction (as in bdc_update.cu).
-__device__ __forceinline__ int block_rank(bool flag, int* wcnt, int& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned bal = __ballot_sync(0xffffffffu, flag);
-  if (lane == 0) wcnt[wid] = __popc(bal);
-  __syncthreads();
-  int off = 0;
-  total = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-    if (i < wid) off += wcnt[i];
-    total += wcnt[i];
-  }
-  __syncthreads();
-  return off + __popc(bal & ((1u << lane) - 1u));
-}
 
 
 }  // namespace

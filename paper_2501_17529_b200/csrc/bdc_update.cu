@@ -23,16 +23,16 @@ namespace bdc {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 256;  // k_n0, k_topk
 constexpr int NW = NT / 32;
+constexpr int UT = 128;  // k_update: one task per CTA, small so that many tasks are in flight
+constexpr int UW = UT / 32;
 
 struct UpdShared {
   int sub[RMAX];
   unsigned bits[RMAX];
   int k, d, nd, fail, farg, nrh, nact;
-  int wcnt[NW];
-  int rh_key[RHMAX];   // row*2 + end
-  int rh_col[RHMAX];
+  int wcnt[UW];
   int dead[RMAX];
   int orow[RMAX];      // outage rows in task order
   int ofc[RMAX], otc[RMAX];  // current endpoint columns of the outaged rows
@@ -43,12 +43,9 @@ struct UpdShared {
   int srow[EMAX], sfar[EMAX];
   double ssign[EMAX], sw[EMAX];
   double den;
-  double mB[EMAX][RMAX];     // B[i][moved row]
-  double sCfar[EMAX][RMAX];  // C[i][far of stay element]
   double sCa[RMAX];          // C[i][a]
   double inner[MMAX * MMAX];
   double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
-  double oB[RMAX][RMAX];     // B[i'][outage row i]
   double ybase[RMAX];
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
   double act_sp[ACTMAX];
@@ -59,23 +56,32 @@ __device__ __forceinline__ int base_col(const DevGrid& g, const UpdShared& s, in
   return col < g.C0 ? col : g.sub_col[s.sub[col - g.C0]];
 }
 
-__device__ __forceinline__ int curcol(const UpdShared& s, int row, int end, int dflt) {
+__device__ __forceinline__ int curcol(const UpdShared& s, const int* rh_key, const int* rh_col, int row,
+                                      int end, int dflt) {
   int key = row * 2 + end, c = dflt;
   for (int i = 0; i < s.nrh; ++i)
-    if (s.rh_key[i] == key) c = s.rh_col[i];
+    if (rh_key[i] == key) c = rh_col[i];
   return c;
+}
+
+// Dynamic shared memory of k_update (bytes), sized by the wave's rank stride rs and
+// the widest substation E: moved-row B values, far-end coupler values, outage-row B
+// values and the re-homed branch ends.
+__host__ __device__ inline size_t update_dyn_bytes(int rs, int E) {
+  const int e2 = E > 2 ? E : 2;
+  return ((size_t)E * rs + (size_t)e2 * rs + (size_t)rs * rs) * sizeof(double) + 2 * (size_t)rs * E * sizeof(int);
 }
 
 // Ordered block-wide compaction helper: returns this thread's slot among the
 // flagged threads of the current chunk and the chunk total (all threads).
 __device__ __forceinline__ int block_rank(bool flag, int* wcnt, int& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned bal = __ballot_sync(0xffffffffu, flag);
   if (lane == 0) wcnt[wid] = __popc(bal);
   __syncthreads();
   int off = 0;
   total = 0;
-  for (int i = 0; i < NW; ++i) {
+  for (int i = 0; i < nw; ++i) {
     if (i < wid) off += wcnt[i];
     total += wcnt[i];
   }
@@ -89,22 +95,32 @@ __device__ void set_island(const Work& w, int b, int order) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w) {
   __shared__ UpdShared s;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int R = g.R, C0 = g.C0, rs = w.rs, Cs = w.Cs;
+  const int E = g.E > 0 ? g.E : 1, E2 = E > 2 ? E : 2;
+  extern __shared__ double udyn[];
+  double* mB = udyn;                 // [E][rs]   B[i][moved row m]
+  double* sCfar = mB + E * rs;       // [E2][rs]  C[i][far end of stay element st]
+  double* oB = sCfar + E2 * rs;      // [rs][rs]  B[i'][outage row i]
+  int* rh_key = reinterpret_cast<int*>(oB + rs * rs);  // [rs*E] row*2 + end
+  int* rh_col = rh_key + rs * E;
+#define MB(m, i) mB[(m) * rs + (i)]
+#define SCF(st, i) sCfar[(st) * rs + (i)]
+#define OB(i, ip) oB[(i) * rs + (ip)]
   double* Bm = w.Bm + (size_t)b * rs * R;
   double* Cm = w.Cm + (size_t)b * rs * Cs;
 
   if (tid == 0) {
     s.k = 0; s.d = 0; s.nd = 0; s.fail = 0; s.farg = 0; s.nrh = 0; s.nact = 0; s.nisl = 0;
   }
-  for (int i = tid; i < w.NCw; i += NT) w.isl[(size_t)b * w.NCw + i] = 0u;
+  for (int i = tid; i < w.NCw; i += UT) w.isl[(size_t)b * w.NCw + i] = 0u;
   __syncthreads();
 
   // ---- decode splits in canonical (ascending substation) order ----------------
   const uint8_t* sp = w.splits + (size_t)b * g.S * w.Ein;
-  for (int c0 = 0; c0 < g.S; c0 += NT) {
+  for (int c0 = 0; c0 < g.S; c0 += UT) {
     int si = c0 + tid;
     unsigned bits = 0;
     if (si < g.S) {
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
         int nm = 0, nst = 0;
         for (int e = 0; e < cnt; ++e) {
           int row = g.sub_elem_row[si * g.E + e];
-          int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+          int fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]), tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
           double sign; int far, end;
           if (fc == a) { sign = 1.0; far = tc; end = 0; }
           else if (tc == a) { sign = -1.0; far = fc; end = 1; }
@@ -171,25 +187,25 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     __syncthreads();
     if (s.fail) goto done;
     const int a = s.a, nm = s.nm, nst = s.nst;
-    for (int idx = tid; idx < nm * j; idx += NT) {
+    for (int idx = tid; idx < nm * j; idx += UT) {
       int m = idx / j, i = idx % j;
-      s.mB[m][i] = Bm[(size_t)i * R + s.mrow[m]];
+      MB(m, i) = Bm[(size_t)i * R + s.mrow[m]];
     }
     __syncthreads();
     // coupler row over every current column: c[col] = sum_moved sign * P_{j-1}[row, col]
     const int ncols = C0 + j;
-    for (int col = tid; col < ncols; col += NT) {
+    for (int col = tid; col < ncols; col += UT) {
       const int bc = base_col(g, s, col);
       double c = 0.0;
       for (int m = 0; m < nm; ++m) {
         double v = g.P0[(size_t)s.mrow[m] * C0 + bc];
-        for (int i = 0; i < j; ++i) v = fma(s.mB[m][i], Cm[(size_t)i * Cs + col], v);
+        for (int i = 0; i < j; ++i) v = fma(MB(m, i), Cm[(size_t)i * Cs + col], v);
         c += s.msign[m] * v;
       }
       Cm[(size_t)j * Cs + col] = c;
     }
     // the new busbar column starts as a copy of column a for every earlier term
-    for (int i = tid; i < j; i += NT) Cm[(size_t)i * Cs + C0 + j] = Cm[(size_t)i * Cs + a];
+    for (int i = tid; i < j; i += UT) Cm[(size_t)i * Cs + C0 + j] = Cm[(size_t)i * Cs + a];
     __syncthreads();
     if (tid == 0) {
       const double ca = Cm[(size_t)j * Cs + a];
@@ -199,23 +215,23 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       if (fabs(den) < ISL_TOL) { s.fail = BDC_TASK_SINGULAR_SPLIT; s.farg = j; }
       s.den = den;
     }
-    for (int idx = tid; idx < (nst + 1) * j; idx += NT) {
+    for (int idx = tid; idx < (nst + 1) * j; idx += UT) {
       int st = idx / j, i = idx % j;
-      if (st < nst) s.sCfar[st][i] = Cm[(size_t)i * Cs + s.sfar[st]];
+      if (st < nst) SCF(st, i) = Cm[(size_t)i * Cs + s.sfar[st]];
       else s.sCa[i] = Cm[(size_t)i * Cs + a];
     }
     __syncthreads();
     if (s.fail) goto done;
     {
       const double den = s.den;
-      for (int r = tid; r < R; r += NT) {
+      for (int r = tid; r < R; r += UT) {
         double pa = g.P0T[(size_t)a * R + r];
         for (int i = 0; i < j; ++i) pa = fma(Bm[(size_t)i * R + r], s.sCa[i], pa);
         double num = 0.0;
         for (int st = 0; st < nst; ++st) {
           const int bf = base_col(g, s, s.sfar[st]);
           double pf = g.P0T[(size_t)bf * R + r];
-          for (int i = 0; i < j; ++i) pf = fma(Bm[(size_t)i * R + r], s.sCfar[st][i], pf);
+          for (int i = 0; i < j; ++i) pf = fma(Bm[(size_t)i * R + r], SCF(st, i), pf);
           num += s.sw[st] * (pf - pa);
           if (r == s.srow[st]) num += s.ssign[st] * s.sw[st];
         }
@@ -224,8 +240,8 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     }
     if (tid == 0) {
       for (int m = 0; m < nm; ++m) {
-        s.rh_key[s.nrh] = s.mrow[m] * 2 + s.mend[m];
-        s.rh_col[s.nrh] = C0 + j;
+        rh_key[s.nrh] = s.mrow[m] * 2 + s.mend[m];
+        rh_col[s.nrh] = C0 + j;
         ++s.nrh;
       }
     }
@@ -243,14 +259,14 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     if (tid == 0)
       for (int i = 0; i < d; ++i) {
         int row = s.orow[i];
-        s.ofc[i] = curcol(s, row, 0, g.row_from[row]);
-        s.otc[i] = curcol(s, row, 1, g.row_to[row]);
+        s.ofc[i] = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]);
+        s.otc[i] = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
       }
     __syncthreads();
     if (cfg.method == 0) {
       // MODF: one d x d inner system against the post-split matrix (factors.py:373-425)
       // rhs[i][r] = P'[r, f'_i] - P'[r, t'_i] into B slots k+i
-      for (int r = tid; r < R; r += NT) {
+      for (int r = tid; r < R; r += UT) {
         for (int i = 0; i < d; ++i) {
           const int fc = s.ofc[i], tc = s.otc[i];
           double pf = g.P0T[(size_t)base_col(g, s, fc) * R + r];
@@ -279,14 +295,14 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
           s.fail = BDC_TASK_DETACHED; s.farg = -3;
         }
       }
-      for (int idx = tid; idx < d * k; idx += NT) {
+      for (int idx = tid; idx < d * k; idx += UT) {
         int i = idx / k, ip = idx % k;
-        s.oB[i][ip] = Bm[(size_t)ip * R + s.orow[i]];
+        OB(i, ip) = Bm[(size_t)ip * R + s.orow[i]];
       }
       __syncthreads();
       if (s.fail) goto done;
       // MODF values in place: modf[r][i] = sum_bb rhs[bb][r] inv[bb][i]; rows O -> -e_i
-      for (int r = tid; r < R; r += NT) {
+      for (int r = tid; r < R; r += UT) {
         double rhs[MMAX];
         for (int bb = 0; bb < d; ++bb) rhs[bb] = Bm[(size_t)(k + bb) * R + r];
         int own = -1;
@@ -303,10 +319,10 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       }
       // outage rows of the post-split matrix become the new coupler rows
       const int ncols = C0 + k;
-      for (int idx = tid; idx < d * ncols; idx += NT) {
+      for (int idx = tid; idx < d * ncols; idx += UT) {
         int i = idx / ncols, col = idx % ncols;
         double v = g.P0[(size_t)s.orow[i] * C0 + base_col(g, s, col)];
-        for (int ip = 0; ip < k; ++ip) v = fma(s.oB[i][ip], Cm[(size_t)ip * Cs + col], v);
+        for (int ip = 0; ip < k; ++ip) v = fma(OB(i, ip), Cm[(size_t)ip * Cs + col], v);
         Cm[(size_t)(k + i) * Cs + col] = v;
       }
       if (tid == 0) {
@@ -319,20 +335,20 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       for (int i = 0; i < d; ++i) {
         const int kk = k + i, row = s.orow[i], fc = s.ofc[i], tc = s.otc[i];
         const int bf = base_col(g, s, fc), bt = base_col(g, s, tc);
-        for (int ip = tid; ip < kk; ip += NT) {
-          s.sCfar[0][ip] = Cm[(size_t)ip * Cs + fc];
-          s.sCfar[1][ip] = Cm[(size_t)ip * Cs + tc];
-          s.oB[0][ip] = Bm[(size_t)ip * R + row];
+        for (int ip = tid; ip < kk; ip += UT) {
+          SCF(0, ip) = Cm[(size_t)ip * Cs + fc];
+          SCF(1, ip) = Cm[(size_t)ip * Cs + tc];
+          OB(0, ip) = Bm[(size_t)ip * R + row];
         }
         __syncthreads();
-        for (int r = tid; r < R; r += NT) {
+        for (int r = tid; r < R; r += UT) {
           double v = 0.0;
           if (!is_dead(s.dead, s.nd, r)) {
             double pf = g.P0T[(size_t)bf * R + r], pt = g.P0T[(size_t)bt * R + r];
             for (int ip = 0; ip < kk; ++ip) {
               double bv = Bm[(size_t)ip * R + r];
-              pf = fma(bv, s.sCfar[0][ip], pf);
-              pt = fma(bv, s.sCfar[1][ip], pt);
+              pf = fma(bv, SCF(0, ip), pf);
+              pt = fma(bv, SCF(1, ip), pt);
             }
             v = pf - pt;
           }
@@ -346,12 +362,12 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
         }
         __syncthreads();
         if (s.fail) goto done;
-        for (int r = tid; r < R; r += NT)
+        for (int r = tid; r < R; r += UT)
           Bm[(size_t)kk * R + r] = (r == row) ? -1.0 : Bm[(size_t)kk * R + r] / s.den;
         const int ncols = C0 + k;
-        for (int col = tid; col < ncols; col += NT) {
+        for (int col = tid; col < ncols; col += UT) {
           double v = g.P0[(size_t)row * C0 + base_col(g, s, col)];
-          for (int ip = 0; ip < kk; ++ip) v = fma(s.oB[0][ip], Cm[(size_t)ip * Cs + col], v);
+          for (int ip = 0; ip < kk; ++ip) v = fma(OB(0, ip), Cm[(size_t)ip * Cs + col], v);
           Cm[(size_t)kk * Cs + col] = v;
         }
         __syncthreads();
@@ -366,9 +382,9 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     const int rt = k + s.d;
     const int nd = s.nd;
     // single-branch cases: W(c,:), den_c, feasibility
-    for (int c = tid; c < g.N1; c += NT) {
+    for (int c = tid; c < g.N1; c += UT) {
       const int row = g.sc_row[c];
-      const int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+      const int fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]), tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
       double* Wc = w.Wsc + ((size_t)b * g.N1 + c) * rs;
       double diag = g.sc_delta[c];
       const bool dead = is_dead(s.dead, nd, row);
@@ -385,12 +401,12 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       if (!ok) { set_island(w, b, g.sc_order[c]); atomicAdd(&s.nisl, 1); }
     }
     // multi-branch cases: m x m inner system, SVD islanding test, inverse
-    for (int q = tid; q < g.NM; q += NT) {
+    for (int q = tid; q < g.NM; q += UT) {
       const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
       double A[MMAX * MMAX];
       for (int i = 0; i < m; ++i) {
         const int row = g.mb_row[st + i];
-        const int fc = curcol(s, row, 0, g.row_from[row]), tc = curcol(s, row, 1, g.row_to[row]);
+        const int fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]), tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
         double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
         for (int j = 0; j < rt; ++j) Wq[j] = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
       }
@@ -413,7 +429,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       if (!ok) { set_island(w, b, g.mc_order[q]); atomicAdd(&s.nisl, 1); }
     }
     // injection cases: coupler coefficients of the outaged injection's columns
-    for (int q = tid; q < g.NI; q += NT) {
+    for (int q = tid; q < g.NI; q += UT) {
       int ca, cb;
       const int sl = g.ic_slot[q];
       if (sl >= 0) {
@@ -427,7 +443,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       for (int j = 0; j < rt; ++j) { pa[j] = Cm[(size_t)j * Cs + ca]; pb[j] = Cm[(size_t)j * Cs + cb]; }
     }
     // active slots (slot at a split substation, nonzero setpoint), in slot order
-    for (int c0 = 0; c0 < g.K; c0 += NT) {
+    for (int c0 = 0; c0 < g.K; c0 += UT) {
       const int sl = c0 + tid;
       int cb = -1;
       if (sl < g.K && g.slot_sp[sl] != 0.0)
@@ -453,7 +469,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     // y_base[j] = sum_col p_base[col] C[j][col]  (every slot at home)
     {
       const int lane = tid & 31, wid = tid >> 5;
-      for (int j = wid; j < rt; j += NW) {
+      for (int j = wid; j < rt; j += UW) {
         double acc = 0.0;
         for (int col = lane; col < C0; col += 32) acc = fma(g.p_base[col], Cm[(size_t)j * Cs + col], acc);
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -464,7 +480,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
     // Y[j][t] = y_base[j] + sum_active bit(t, s) * sp_s (C[j][col_b] - C[j][col_a])
     const uint8_t* ib = w.inj + (size_t)b * w.T * g.K;
     double* Y = w.Y + (size_t)b * rs * w.T;
-    for (int idx = tid; idx < rt * w.T; idx += NT) {
+    for (int idx = tid; idx < rt * w.T; idx += UT) {
       const int j = idx / w.T, t = idx % w.T;
       double y = s.ybase[j];
       for (int a2 = 0; a2 < s.nact; ++a2)
@@ -486,7 +502,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
       if (NTM > 0) {
         float* Lo = w.Lo + (size_t)b * M * NTM;
         float* So = w.So + (size_t)b * NTM * T;
-        for (int idx = tid; idx < M * NQ; idx += NT) {
+        for (int idx = tid; idx < M * NQ; idx += UT) {
           const int p = idx / NQ, q = idx % NQ;
           const int row = g.mon_row[p];
           const double inv = g.inv_rating[p];
@@ -533,7 +549,7 @@ __global__ void __launch_bounds__(NT, 3) k_update(DevGrid g, DevCfg cfg, Work w)
           }
         }
         const uint8_t* ib = w.inj + (size_t)b * T * g.K;
-        for (int idx = tid; idx < NTM * T; idx += NT) {
+        for (int idx = tid; idx < NTM * T; idx += UT) {
           const int qj = idx / T, t = idx % T, q = qj / MT, j = qj % MT;
           float v = 0.f;
           if (q < g.NM) {
@@ -565,6 +581,9 @@ done:
     if (s.fail == BDC_TASK_DEGENERATE_SPLIT || s.fail == BDC_TASK_SINGULAR_SPLIT) applied = s.farg;
     atomicAdd(w.bsdf, (unsigned long long)applied);
   }
+#undef MB
+#undef SCF
+#undef OB
 }
 
 // ---- N-0 contraction (solver.py:575-595): n0 = f0 + B'' y_t, emitted for
@@ -762,7 +781,13 @@ __global__ void __launch_bounds__(NT) k_topk(DevGrid g, Work w) {
 }
 
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t st) {
-  k_update<<<w.Wb, NT, 0, st>>>(g, c, w);
+  const size_t dyn = update_dyn_bytes(w.rs, g.E > 0 ? g.E : 1);
+  static size_t opted = 0;
+  if (dyn > opted) {
+    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_dyn_bytes(RMAX, EMAX));
+    opted = update_dyn_bytes(RMAX, EMAX);
+  }
+  k_update<<<w.Wb, UT, dyn, st>>>(g, c, w);
 }
 
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
