@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -54,6 +55,9 @@ struct BdcSession {
   int64_t wave_cap = 0;
   size_t total_mem = 0;
   std::vector<int32_t> sub_count, slots_per_sub;  // host copies for bdc_scan_tasks
+  std::vector<double> inv_rating;                 // host copy: report loadings = |flow| / rating
+  // pinned host staging for outputs bound for pageable host memory, reused across calls
+  std::vector<std::pair<char*, size_t>> pin_free;
   // cached wave workspaces (one per concurrent call), reused across calls
   std::mutex ws_mu;
   std::vector<std::pair<char*, size_t>> ws_free;
@@ -91,6 +95,35 @@ struct WsLease {
     if (!p) return;
     std::lock_guard<std::mutex> lk(s->ws_mu);
     s->ws_free.emplace_back(p, bytes);
+  }
+};
+// Borrow pinned host memory of at least `need` bytes from the session cache.
+struct PinLease {
+  BdcSession* s;
+  char* p = nullptr;
+  size_t bytes = 0;
+  PinLease(BdcSession* s_, size_t need) : s(s_) {
+    {
+      std::lock_guard<std::mutex> lk(s->ws_mu);
+      for (size_t i = 0; i < s->pin_free.size(); ++i)
+        if (s->pin_free[i].second >= need) {
+          p = s->pin_free[i].first;
+          bytes = s->pin_free[i].second;
+          s->pin_free.erase(s->pin_free.begin() + i);
+          return;
+        }
+    }
+    if (cudaMallocHost((void**)&p, need) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return;
+    }
+    bytes = need;
+  }
+  ~PinLease() {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    s->pin_free.emplace_back(p, bytes);
   }
 };
 }  // namespace
@@ -188,6 +221,7 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   UP(ic_order, G->NI);
 #undef UP
   if (e == cudaSuccess) e = upload((const double*)inv.data(), inv.size(), &g.inv_rating, o);
+  s->inv_rating = inv;
   if (e != cudaSuccess) {
     for (void* p : o) cudaFree(p);
     delete s;
@@ -221,6 +255,7 @@ int bdc_session_destroy(BdcSession* s) {
   cudaSetDevice(s->device);
   for (void* p : s->owned) cudaFree(p);
   for (auto& f : s->ws_free) cudaFree(f.first);
+  for (auto& f : s->pin_free) cudaFreeHost(f.first);
   delete s;
   return BDC_OK;
 }
@@ -349,6 +384,22 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   return L.total;
 }
 
+// Byte offsets of one wave's outputs in a pinned staging buffer.
+struct OutLayout {
+  size_t metric, best, feasible, status, sarg, nisl, isl, n0cnt, n1cnt;
+  size_t n0pos, n0flow, n1case, n1pos, n1flow, cand;
+  size_t build(int Wb, int kg, int NCw, int T) {
+    size_t o = 0;
+    auto add = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~size_t(255); return r; };
+    const size_t B = Wb;
+    metric = add(B * 8); best = add(B * 8); feasible = add(B); status = add(B * 4); sarg = add(B * 4);
+    nisl = add(B * 4); isl = add(B * NCw * 4); n0cnt = add(B * 4); n1cnt = add(B * 4);
+    n0pos = add(B * kg * 4); n0flow = add(B * kg * 8); n1case = add(B * kg * 4); n1pos = add(B * kg * 4);
+    n1flow = add(B * kg * 8); cand = add(B * (size_t)T * 4);
+    return o;
+  }
+};
+
 struct StreamGuard {
   cudaStream_t s = nullptr;
   bool own = false;
@@ -420,6 +471,67 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   for (auto& e : ev) CK(cudaEventCreate(&e));
   const bool ondev_in = bt->inputs_on_device != 0, ondev_out = bt->outputs_on_device != 0;
   const int kg = s->cfg.kg, NCw = w.NCw;
+  // pinned staging for host outputs: two wave-sized buffers, unpacked by the host while
+  // the next wave runs; report loadings are recomputed on the host as |flow| / rating
+  // (bit-identical to the device's fabs(flow) * inv_rating), so they are not copied
+  OutLayout olay{};
+  std::unique_ptr<PinLease> pin[2];
+  cudaEvent_t wdone[2] = {nullptr, nullptr};
+  int64_t staged_b0[2] = {0, 0};
+  int staged_nb[2] = {0, 0};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 2; ++i) if (e[i]) cudaEventDestroy(e[i]); }
+  } evg{wdone};
+  if (!ondev_out) {
+    const size_t sb = olay.build((int)Wb, kg, NCw, bt->cand_metric ? T : 0);
+    for (int i = 0; i < 2; ++i) {
+      pin[i].reset(new PinLease(s, sb));
+      if (!pin[i]->p) return fail(BDC_ECUDA, "pinned staging allocation failed");
+      CK(cudaEventCreateWithFlags(&wdone[i], cudaEventDisableTiming));
+    }
+  }
+  auto unpack = [&](int slot) -> cudaError_t {
+    cudaError_t e = cudaEventSynchronize(wdone[slot]);
+    if (e != cudaSuccess) return e;
+    const char* hp = pin[slot]->p;
+    const OutLayout& O = olay;
+    const int64_t b0 = staged_b0[slot];
+    const size_t nb = (size_t)staged_nb[slot];
+    auto put = [&](void* dst, size_t off, size_t bytes_per_task) {
+      if (dst) std::memcpy((char*)dst + b0 * bytes_per_task, hp + off, nb * bytes_per_task);
+    };
+    put(bt->metric, O.metric, 8);
+    put(bt->best, O.best, 8);
+    put(bt->feasible, O.feasible, 1);
+    put(bt->status, O.status, 4);
+    put(bt->status_arg, O.sarg, 4);
+    put(bt->n_islanded, O.nisl, 4);
+    put(bt->islanded_bits, O.isl, (size_t)NCw * 4);
+    put(bt->n0_count, O.n0cnt, 4);
+    put(bt->n1_count, O.n1cnt, 4);
+    put(bt->n0_pos, O.n0pos, (size_t)kg * 4);
+    put(bt->n0_flow, O.n0flow, (size_t)kg * 8);
+    put(bt->n1_case, O.n1case, (size_t)kg * 4);
+    put(bt->n1_pos, O.n1pos, (size_t)kg * 4);
+    put(bt->n1_flow, O.n1flow, (size_t)kg * 8);
+    if (bt->cand_metric) put(bt->cand_metric, O.cand, (size_t)T * 4);
+    const double* inv = s->inv_rating.data();
+    const int M = (int)s->inv_rating.size();
+    auto rel = [&](double* dst, size_t pos_off, size_t flow_off) {
+      if (!dst) return;
+      const int32_t* pos = (const int32_t*)(hp + pos_off);
+      const double* fl = (const double*)(hp + flow_off);
+      double* d = dst + b0 * kg;
+      for (size_t i = 0; i < nb * (size_t)kg; ++i) {
+        const int p = pos[i];
+        d[i] = (p >= 0 && p < M) ? std::fabs(fl[i]) * inv[p] : 0.0;
+      }
+    };
+    rel(bt->n0_rel, O.n0pos, O.n0flow);
+    rel(bt->n1_rel, O.n1pos, O.n1flow);
+    return cudaSuccess;
+  };
   int launches = 0;
   cudaError_t err = cudaSuccess;
   for (int wv = 0; wv < nwaves && err == cudaSuccess; ++wv) {
@@ -461,37 +573,65 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     launches += kernels_per_wave(g, x);
     err = cudaGetLastError();
     if (err != cudaSuccess) break;
-    // outputs
+    // outputs: straight into device buffers, or through pinned staging for host
+    // (pageable) buffers -- the unpack of wave wv-1 overlaps the kernels of wave wv
     cudaError_t e2 = cudaSuccess;
     auto chk = [&](cudaError_t e) { if (e2 == cudaSuccess) e2 = e; };
-    chk(out_copy(bt->metric, x.metric, nb, b0, ondev_out, st));
-    chk(out_copy(bt->best, x.best, nb, b0, ondev_out, st));
-    chk(out_copy(bt->feasible, x.feasible, nb, b0, ondev_out, st));
-    chk(out_copy(bt->status, x.status, nb, b0, ondev_out, st));
-    chk(out_copy(bt->status_arg, x.sarg, nb, b0, ondev_out, st));
-    chk(out_copy(bt->n_islanded, x.nisl, nb, b0, ondev_out, st));
-    chk(out_copy(bt->islanded_bits, x.isl, (size_t)nb * NCw, b0 * NCw, ondev_out, st));
-    chk(out_copy(bt->n0_count, x.n0cnt, nb, b0, ondev_out, st));
-    chk(out_copy(bt->n1_count, x.n1cnt, nb, b0, ondev_out, st));
-    // report entries are stored with stride KMAX on device; copy with the user's stride kg
-    auto strided = [&](auto* dst, const auto* src, size_t elem) {
-      if (!dst) return;
-      chk(cudaMemcpy2DAsync(dst + b0 * kg, kg * elem, src, (size_t)kg * elem, (size_t)kg * elem, nb,
-                            ondev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    };
-    strided(bt->n0_pos, x.n0pos, 4);
-    strided(bt->n0_flow, x.n0flow, 8);
-    strided(bt->n0_rel, x.n0rel, 8);
-    strided(bt->n1_case, x.n1case, 4);
-    strided(bt->n1_pos, x.n1pos, 4);
-    strided(bt->n1_flow, x.n1flow, 8);
-    strided(bt->n1_rel, x.n1rel, 8);
-    if (bt->cand_metric)
-      chk(cudaMemcpyAsync(bt->cand_metric + b0 * T, x.m32, (size_t)nb * T * 4,
-                          ondev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (ondev_out) {
+      chk(out_copy(bt->metric, x.metric, nb, b0, true, st));
+      chk(out_copy(bt->best, x.best, nb, b0, true, st));
+      chk(out_copy(bt->feasible, x.feasible, nb, b0, true, st));
+      chk(out_copy(bt->status, x.status, nb, b0, true, st));
+      chk(out_copy(bt->status_arg, x.sarg, nb, b0, true, st));
+      chk(out_copy(bt->n_islanded, x.nisl, nb, b0, true, st));
+      chk(out_copy(bt->islanded_bits, x.isl, (size_t)nb * NCw, b0 * NCw, true, st));
+      chk(out_copy(bt->n0_count, x.n0cnt, nb, b0, true, st));
+      chk(out_copy(bt->n1_count, x.n1cnt, nb, b0, true, st));
+      // report entries: (task, kg) on device as in the user's arrays
+      auto strided = [&](auto* dst, const auto* src, size_t elem) {
+        if (!dst) return;
+        chk(cudaMemcpy2DAsync(dst + b0 * kg, kg * elem, src, (size_t)kg * elem, (size_t)kg * elem, nb,
+                              cudaMemcpyDeviceToDevice, st));
+      };
+      strided(bt->n0_pos, x.n0pos, 4);
+      strided(bt->n0_flow, x.n0flow, 8);
+      strided(bt->n0_rel, x.n0rel, 8);
+      strided(bt->n1_case, x.n1case, 4);
+      strided(bt->n1_pos, x.n1pos, 4);
+      strided(bt->n1_flow, x.n1flow, 8);
+      strided(bt->n1_rel, x.n1rel, 8);
+      if (bt->cand_metric)
+        chk(cudaMemcpyAsync(bt->cand_metric + b0 * T, x.m32, (size_t)nb * T * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      char* hp = pin[wv & 1]->p;
+      const OutLayout& O = olay;
+      chk(cudaMemcpyAsync(hp + O.metric, x.metric, (size_t)nb * 8, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.best, x.best, (size_t)nb * 8, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.feasible, x.feasible, (size_t)nb, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.status, x.status, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.sarg, x.sarg, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.nisl, x.nisl, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.isl, x.isl, (size_t)nb * NCw * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.n0cnt, x.n0cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(hp + O.n1cnt, x.n1cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+      auto strided = [&](size_t off, const void* src, size_t elem) {  // device stride is kg
+        chk(cudaMemcpyAsync(hp + off, src, (size_t)nb * kg * elem, cudaMemcpyDeviceToHost, st));
+      };
+      strided(O.n0pos, x.n0pos, 4);
+      strided(O.n0flow, x.n0flow, 8);
+      strided(O.n1case, x.n1case, 4);
+      strided(O.n1pos, x.n1pos, 4);
+      strided(O.n1flow, x.n1flow, 8);
+      if (bt->cand_metric) chk(cudaMemcpyAsync(hp + O.cand, x.m32, (size_t)nb * T * 4, cudaMemcpyDeviceToHost, st));
+      chk(cudaEventRecord(wdone[wv & 1], st));
+      staged_b0[wv & 1] = b0;
+      staged_nb[wv & 1] = nb;
+      if (wv > 0 && e2 == cudaSuccess) chk(unpack((wv - 1) & 1));
+    }
     cudaEventRecord(E[8], st);
     err = e2;
   }
+  if (!ondev_out && err == cudaSuccess) err = unpack((nwaves - 1) & 1);
   unsigned long long counters[4] = {0, 0, 0, 0};
   if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 32, cudaMemcpyDeviceToHost, st);
   cudaError_t es = cudaStreamSynchronize(st);
