@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -463,6 +464,10 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (!ws.p) return fail(BDC_ECUDA, "workspace allocation failed (" + std::to_string(bytes) + " bytes)");
   carve(g, (int)Wb, T, D, Ein, rs, ws.p, &w);
   w.screen = bt->screen ? 1 : 0;
+  {
+    const char* pt = std::getenv("BDC_PTOP");
+    if (pt && std::atoi(pt) > 0) w.ptop = std::min(w.ptop, std::atoi(pt));
+  }
   w.ranked = (w.screen && g.N1 > w.ptop) ? 1 : 0;
   CK(cudaMemsetAsync(w.lf, 0, 32, st));
 

@@ -230,6 +230,14 @@ __device__ __forceinline__ double n0_at(const DevGrid& g, const Work& w, int b, 
   return v;
 }
 
+// max(|a|, |b|, |c|) in one FMNMX3 (sm_100+ three-input max with the |.| modifier):
+// the sweeps fold two rows into an accumulator per ALU-pipe instruction.
+__device__ __forceinline__ float max3abs(float a, float b, float c) {
+  float d;
+  asm("max.abs.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // cp.async helpers (global -> shared, zero-filling when !ok).
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -97,24 +97,27 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
       __syncthreads();
       const int rend = min(ORC, M - ch * ORC);  // zero-filled rows past M are harmless
       (void)rend;
-#pragma unroll 4
-      for (int rr = 0; rr < ORC; ++rr) {
-        float n[TPT];
+      // two rows per step: FFMA2 over the row pair (same rounding as fmaf), one FMNMX3
+#pragma unroll 2
+      for (int rr = 0; rr < ORC; rr += 2) {
+        float2 n[TPT];
 #pragma unroll
-        for (int i = 0; i < TPT; ++i) n[i] = sN[(buf * ORC + rr) * TT + lane * TPT + i];
+        for (int i = 0; i < TPT; ++i)
+          n[i] = make_float2(sN[(buf * ORC + rr) * TT + lane * TPT + i], sN[(buf * ORC + rr + 1) * TT + lane * TPT + i]);
 #pragma unroll
         for (int k = 0; k < QW; ++k) {
           if (wid + OW * k >= nqb) break;  // warp-uniform
-          const float* lrow = &sL[(buf * ORC + rr) * QB * MT + (wid + OW * k) * MT];
-          float l[MT];
+          const float* lrow0 = &sL[(buf * ORC + rr) * QB * MT + (wid + OW * k) * MT];
+          const float* lrow1 = lrow0 + QB * MT;
+          float2 l[MT];
 #pragma unroll
-          for (int j = 0; j < MT; ++j) l[j] = lrow[j];
+          for (int j = 0; j < MT; ++j) l[j] = make_float2(lrow0[j], lrow1[j]);
 #pragma unroll
           for (int i = 0; i < TPT; ++i) {
-            float f = n[i];
+            float2 f = n[i];
 #pragma unroll
-            for (int j = 0; j < MT; ++j) f = fmaf(l[j], sv[k][j][i], f);
-            acc[k][i] = fmaxf(acc[k][i], fabsf(f));
+            for (int j = 0; j < MT; ++j) f = __ffma2_rn(l[j], make_float2(sv[k][j][i], sv[k][j][i]), f);
+            acc[k][i] = max3abs(acc[k][i], f.x, f.y);
           }
         }
       }

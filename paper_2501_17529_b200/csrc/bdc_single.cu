@@ -242,18 +242,33 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
     if (warp_alive) {
       const int rend = min(RC, M - ch * RC);
       if (rend == RC) {
-#pragma unroll 4
-        for (int rr = 0; rr < RC; ++rr) {
-          float l[CPT], n[TPT];
+        // two rows x two candidates per step: FFMA2 (packed FP32 FMA, same rounding as
+        // fmaf) and one FMNMX3 (|.| on every input) per accumulator
+        static_assert(TPT % 2 == 0, "candidate pairs");
+#pragma unroll 2
+        for (int rr = 0; rr < RC; rr += 2) {
+          float2 l2[2][CPT], n2[2][TPT / 2];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) l[i] = sL[rr][tx * CPT + i];
+          for (int h = 0; h < 2; ++h) {
 #pragma unroll
-          for (int jj = 0; jj < TPT; ++jj) n[jj] = SN(buf, rr, ty * TPT + jj);
+            for (int i = 0; i < CPT; ++i) {
+              const float lv = sL[rr + h][tx * CPT + i];
+              l2[h][i] = make_float2(lv, lv);
+            }
+#pragma unroll
+            for (int p = 0; p < TPT / 2; ++p)
+              n2[h][p] = *reinterpret_cast<const float2*>(&SN(buf, rr + h, ty * TPT + 2 * p));
+          }
 #pragma unroll
           for (int i = 0; i < CPT; ++i)
 #pragma unroll
-            for (int jj = 0; jj < TPT; ++jj)
-              acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
+            for (int p = 0; p < TPT / 2; ++p) {
+              const float2 sp = make_float2(sv[i][2 * p], sv[i][2 * p + 1]);
+              const float2 f0 = __ffma2_rn(l2[0][i], sp, n2[0][p]);
+              const float2 f1 = __ffma2_rn(l2[1][i], sp, n2[1][p]);
+              acc[i][2 * p] = max3abs(acc[i][2 * p], f0.x, f1.x);
+              acc[i][2 * p + 1] = max3abs(acc[i][2 * p + 1], f0.y, f1.y);
+            }
         }
       } else {
         for (int rr = 0; rr < rend; ++rr) {

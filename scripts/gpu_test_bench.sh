@@ -4,7 +4,7 @@
 set -u
 CFGS=${1:-g1k}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q ${2:+-k "$2"} 2>&1 | tail -15
+[ "${2:-}" = skip ] || timeout 900 python -m pytest tests -m gpu -x -q ${2:+-k "$2"} 2>&1 | tail -15
 for C in $CFGS; do
   timeout 600 python bench.py --config $C --no-cpu --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_$C.json
   python - "$C" <<'PY'

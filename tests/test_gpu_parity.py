@@ -220,3 +220,28 @@ def test_dominance_screen_is_exact(name, sessions):
             a, c = np.maximum(a, pen), np.maximum(c, pen)
         assert np.array_equal(a, c), b
     assert on.n1_pairs <= off.n1_pairs
+
+
+@pytest.mark.parametrize("name", ["fixture_b", "g118"])
+def test_wave_split_is_invisible(name, sessions):
+    """Splitting a batch into many waves (workspace reuse, double-buffered host
+    staging) gives bit-identical results to a single wave."""
+    case = next(c for c in CASES if c["name"] == name)
+    sess = sessions(case)
+    arr, _ = load_case(name)
+    eng = sess.engine
+    args = (arr["splits"], arr["disconnections"], arr["injection_sets"])
+    try:
+        eng.set_wave(0)
+        one = eng.solve(*args, want_candidates=True)
+        eng.set_wave(3)
+        many = eng.solve(*args, want_candidates=True)
+    finally:
+        eng.set_wave(0)
+    assert many.waves > 2 and one.waves == 1
+    assert np.array_equal(one.best, many.best)
+    assert np.array_equal(one.metric, many.metric, equal_nan=True)
+    assert np.array_equal(one.feasible, many.feasible)
+    assert np.array_equal(one.cand_metric, many.cand_metric)
+    assert one.reports() == many.reports()
+    assert one.loadflows == many.loadflows and one.n1_pairs == many.n1_pairs
