@@ -332,13 +332,13 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_n0c = L.add(B * 4), o_n0p = L.add(B * KMAX * 4), o_n0f = L.add(B * KMAX * 8), o_n0r = L.add(B * KMAX * 8);
   size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
   size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
-  size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)g.N1 * 4);
+  size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)SB * g.N1 * 4);
+  size_t o_m0b = L.add(B * (size_t)SB * T * 4);
+  const int TW = (T + 31) / 32;
+  size_t o_live = L.add(B * (size_t)g.N1 * TW * 4), o_q = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 8);
   size_t o_s32 = L.add(B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
-  size_t o_top = L.add(B * (size_t)PTOP_MAX * 4), o_done = L.add(B * (size_t)g.N1);
-  const SweepShape sh = sweep_shape(T);
-  const int nct = (g.N1 + sh.CPT * sh.TX - 1) / (sh.CPT * sh.TX), ntt = (T + sh.TPT * sh.TY - 1) / (sh.TPT * sh.TY);
+  size_t o_top = L.add(B * (size_t)TOPC * 4), o_done = L.add(B * (size_t)g.N1);
   const int nslot = RSEL_WARPS + (g.N1 + RCW - 1) / RCW;
-  size_t o_alive = L.add(B * (size_t)nct * ntt * SWEEP_WARPS);
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
@@ -372,13 +372,15 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.lf = (unsigned long long*)(base + o_lf);
   x.bsdf = x.lf + 1;
   x.pairs = x.lf + 2;
-  (void)o_bs;
+  x.qcount = (unsigned*)(base + o_bs);  // k_pairs queue length, zeroed per wave
   x.m0 = (float*)(base + o_m0); x.scale = (float*)(base + o_sc);
   x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
-  x.ptop = single_tile_cases(T);
+  x.ptop = TOPC;
+  x.m0b = (float*)(base + o_m0b);
+  x.live = (uint32_t*)(base + o_live); x.TW = TW;
+  x.queue = (int2*)(base + o_q);
   x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
-  x.alive = (uint8_t*)(base + o_alive); x.nct = nct; x.ntt = ntt;
   x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.nslot = nslot;
   x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);
   x.pflow = (double*)(base + o_pf); x.prel = (double*)(base + o_pr); x.pmax = (double*)(base + o_pm);
@@ -558,6 +560,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (!bt->t_count) x.tcount = nullptr;
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.m0b, 0, (size_t)nb * SB * T * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);

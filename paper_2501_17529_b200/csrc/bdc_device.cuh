@@ -21,27 +21,19 @@ constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors
 // path's observed error is ~1e-6 (tests: <= 1e-5 enforced), so 1e-3 is a
 // >= 100x safety factor; a wider margin only costs report time.
 constexpr float SCREEN_EPS = 1e-3f;
-constexpr int PTOP_MAX = 256;             // largest case tile of the single-branch sweep
-
-// Thread layout of the single-branch sweep for T candidates (bdc_single.cu): a CTA of
-// TX*TY = 256 threads covers NC = CPT*TX cases x TT = TPT*TY candidates; thread
-// (tx, ty) = tid % TX, tid / TX owns CPT cases x TPT candidates.  The winner report
-// uses the same map to find the warp that evaluated a (case, candidate) pair.
-struct SweepShape {
-  int CPT, TPT, TX, TY;
-};
-__host__ __device__ inline SweepShape sweep_shape(int T) {
-  if (T >= 96) return {2, 16, 32, 8};  // 64 cases x 128 candidates
-  if (T >= 48) return {2, 8, 32, 8};   // 64 x 64
-  if (T >= 24) return {4, 4, 32, 8};   // 128 x 32
-  if (T >= 12) return {4, 4, 64, 4};   // 256 x 16
-  return {4, 2, 64, 4};                // 256 x 8
+// Single-branch N-1 stage with the exact dominance screen (bdc_single.cu):
+//   TOPC  cases evaluated first for every candidate (the top of the screening ranking);
+//   SB    row blocks of the screening bound |F(r,c,t)| <= max_b (m0_b(t) + scale_bc |s(c,t)|):
+//         per-block maxima over monitored rows pair large N-0 rows and large LODF rows
+//         only when they fall in the same block, which is much tighter than one block.
+constexpr int TOPC = 16;
+constexpr int SB = 4;
+// Rows per screening block: a multiple of 16 (the k_scale row chunk, also a multiple of
+// the k_n0 row group), so a chunk never straddles two blocks; block of position m = m / MB.
+__host__ __device__ inline int screen_block_rows(int M) {
+  const int per = (M + SB - 1) / SB;
+  return ((per + 15) / 16) * 16 > 0 ? ((per + 15) / 16) * 16 : 16;
 }
-inline int single_tile_cases(int T) {
-  const SweepShape s = sweep_shape(T);
-  return s.CPT * s.TX;
-}
-constexpr int SWEEP_WARPS = 8;  // warps per sweep CTA (256 threads)
 constexpr int RCW = 128;        // single cases per CTA of the winner report sweep
 constexpr int RSEL_WARPS = 8;   // partial report lists written by the report-select kernel
 
@@ -93,18 +85,20 @@ struct Work {
   double* Y;      // (Wb, rs, T)   y_t = C''^T p_t
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
-  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate), valid
-                  //                   where evaluated (see alive); other cases always
-  uint8_t* alive; // (Wb, nct, ntt, SWEEP_WARPS) 1 if that warp of the screened sweep
-                  //                   evaluated its pairs (else they were dominated)
-  int nct, ntt;   // case / candidate tiles of the sweep
+  float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate); for single
+                  //                   cases valid where evaluated (TOP case or live bit set)
+  uint32_t* live; // (Wb, N1, TW)  bit t of case c: pair evaluated by k_pairs (bound failed)
+  int TW;         // 32-bit words per case of the live bitmap (ceil(T / 32))
+  int2* queue;    // (Wb * N1)     (task, case) items with at least one live candidate
+  unsigned* qcount;  // items in the queue (device counter, reset per wave)
+  float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
-  float* scale;   // (Wb, N1)      FP32 upper bound of max_r |LODF(r,c)|/rating_r (dominance screen)
+  float* scale;   // (Wb, SB, N1)  FP32 upper bound of max_{r in block} |LODF(r,c)|/rating_r
   float* B32;     // (Wb, rs, M)   FP32 B'' on monitored rows (screening bound only)
   float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
   int screen;     // 1 = exact dominance screen on
-  int ptop;       // cases evaluated first (the top tile by screening bound)
+  int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
   float* s32;     // (Wb, N1, T)   n0[r_c][t] (pre-outage flow of each single case), FP32
   uint32_t* bkey; // (Wb, N1)      ranking key max_t m0(t) + scale_c max_t |s(c,t)| (float bits)
@@ -271,5 +265,6 @@ void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s);
 int kernels_per_wave(const DevGrid& g, const Work& w);
+int single_launches(const DevGrid& g, const Work& w);
 
 }  // namespace bdc

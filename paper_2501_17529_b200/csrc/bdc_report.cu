@@ -166,19 +166,23 @@ __device__ int warp_merge_lists(const double (*lv)[KMAX], const int (*li)[KMAX],
   return cnt;
 }
 
-// Was the (single case c, candidate t) pair evaluated by the N-1 sweep, i.e. is
-// cmax[c][t] its exact FP32 maximum?  Cases of the TOP tile always are; in the
-// screened sweep it depends on the warp that owned the pair (bdc_single.cu).
+// Was the (single case c, candidate t) pair evaluated by the N-1 stage, i.e. is
+// cmax[c][t] its exact FP32 maximum?  TOP cases always are, the others iff the screen
+// found the pair live (bdc_single.cu).
 __device__ __forceinline__ bool pair_evaluated(const DevGrid& g, const Work& w, int b, int c, int t) {
   if (w.ranked ? w.done[(size_t)b * g.N1 + c] != 0 : c < w.ptop) return true;
-  const SweepShape sh = sweep_shape(w.T);
-  const int NC = sh.CPT * sh.TX, TT = sh.TPT * sh.TY;
-  const int ct = c / NC, tx = (c % NC) / sh.CPT, tt = t / TT, ty = (t % TT) / sh.TPT;
-  const int warp = (ty * sh.TX + tx) >> 5;
-  return w.alive[(((size_t)b * w.nct + ct) * w.ntt + tt) * SWEEP_WARPS + warp] != 0;
+  return (w.live[((size_t)b * g.N1 + c) * w.TW + (t >> 5)] >> (t & 31)) & 1u;
 }
 
-
+// The dominance bound of a skipped pair: max_b (m0_b(t) + scale_bc |s(c,t)|).
+__device__ __forceinline__ float pair_bound(const DevGrid& g, const Work& w, int b, int c, int t) {
+  const float as = fabsf(w.s32[((size_t)b * g.N1 + c) * w.T + t]);
+  float ub = 0.f;
+#pragma unroll
+  for (int blk = 0; blk < SB; ++blk)
+    ub = fmaxf(ub, w.m0b[((size_t)b * SB + blk) * w.T + t] + w.scale[((size_t)b * SB + blk) * g.N1 + c] * as);
+  return ub;
+}
 
 }  // namespace
 
@@ -232,7 +236,6 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   // ---- per-warp candidates: N-0 report rows and the largest exact case maxima -------------
   const int N1 = g.N1, ncase = N1 + g.NM + g.NI;
   const float* cm = w.cmax + (size_t)b * ncase * T + best;
-  const float m0b = w.m0[(size_t)b * T + best];
   auto feasible_case = [&](int ci) -> bool {
     if (ci < N1) return w.sc_ok[(size_t)b * N1 + ci] != 0;
     if (ci < N1 + g.NM) return w.mc_ok[(size_t)b * g.NM + (ci - N1)] != 0;
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
       ub = cm[(size_t)ci * T];
       return ub;
     }
-    ub = m0b + w.scale[(size_t)b * N1 + ci] * fabsf(w.s32[((size_t)b * N1 + ci) * T + best]);
+    ub = pair_bound(g, w, b, ci, best);
     return -1.f;
   };
   double mymax = 0.0;
@@ -697,10 +700,9 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
 
 int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
-  // update, N-0, select, report select + merge (+ single: [scale, top-k,] top tile, screened
-  // sweep, report sweep) (+ other)
-  return 5 + (single ? 2 + (g.N1 > w.ptop ? 1 : 0) + (w.ranked ? 2 : 0) : 0) +
-         (g.NM + g.NI > 0 && g.M > 0);
+  // update, N-0, select, report select + merge (+ single: the N-1 stage's launches and
+  // the report sweep) (+ other)
+  return 5 + (single ? single_launches(g, w) + 1 : 0) + (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

@@ -1,37 +1,39 @@
 // bdc_single.cu -- the single-branch N-1 stage (the hot path).
 //
-// Forms LODF columns on the fly from the shared base D_base and the task's
-// rank-r factors, L = (D_base + B'' W^T) / den (solver.py:474-485), in FP64,
-// rounded once to FP32 and scaled by 1/rating; monitored rows stream through
-// shared memory in chunks (cp.async double buffer of D_base, B'' rows and
-// n0/rating); every (case, candidate) pair of a tile is evaluated as
-// F = n0 + L n0[r_c] (solver.py:612-613), |F|/rating, max over rows, and the
-// per-candidate max is folded into the metric (solver.py:625-631).  The
-// (case x candidate x branch) tensor never leaves registers.
+// Every (case, candidate) pair needs max_r |n0(r,t) + L(r,c) s(c,t)| / rating_r with
+// L = (D_base + B'' W^T) / den the LODF column of case c on the updated topology
+// (solver.py:474-485, 612-613, 625-631).  LODF columns are formed on the fly in FP64
+// from the shared base D_base and the task's rank-r factors, rounded once to FP32 and
+// scaled by 1/rating; the (case x candidate x branch) tensor never leaves registers.
 //
 // Exact dominance screen (the reference's metric_first, solver.py:798-822):
-//   k_scale      an upper bound scale_c of max_r |L'(r,c)| per case and the ranking
-//                key max_t(m0(t) + scale_c |s(c,t)|);
-//   pass TOP     the ptop cases with the largest key (k_topk) are evaluated first,
-//                for every candidate -- the reference likewise visits likely-binding
-//                cases first;
-//   pass SCREEN  every other tile; a pair whose bound cannot exceed the running
-//                metric of its candidate cannot change it and is skipped, per CTA
-//                tile and per warp.  Evaluated pairs store their exact FP32 max in
-//                cmax; the alive map records which warps evaluated, so the winner
-//                report re-derives the bound of skipped pairs.
+//   k_scale  per case and screening row block b an upper bound scale_bc of
+//            max_{r in b} |L'(r,c)|, and the ranking key of the case;
+//   k_topk   the TOPC cases with the largest key (bdc_update.cu);
+//   k_top    those cases for every candidate (dense tile, FFMA2 + FMNMX3): they fix a
+//            good lower bound lb(t) of every candidate's metric, as the reference's
+//            visit order (descending bound) does;
+//   k_live   every other pair is bounded by |F| <= max_b (m0_b(t) + scale_bc |s(c,t)|);
+//            a pair whose bound cannot exceed lb(t) cannot change the metric and is
+//            skipped; the others get a bit in the live map and their case is queued;
+//   k_pairs  the queued cases, exactly, for their live candidates only.
+// Every evaluated pair uses the same FP32 expression fabsf(fmaf(L', s, n0')) in every
+// kernel, so a metric never depends on which kernel evaluated the binding pair.
 #include "bdc_device.cuh"
 
 namespace bdc {
 
-enum { PASS_SCREEN = 0, PASS_TOP = 1 };
-
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB, int PASS>
-__global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, Work w) {
+// ---------------------------------------------------------------------------- k_top
+// The TOP tile: NC = CPT*TX cases (the task's ranked list, or the first cases when the
+// screen is off / N1 <= TOPC) x TT = TPT*TY candidates per CTA, thread (tx, ty) owns
+// CPT cases x TPT candidates.  Monitored rows stream through shared memory in chunks of
+// RC (cp.async double buffer of D_base columns, B'' rows and n0/rating).
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+__global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Work w) {
   constexpr int NTH = TX * TY, NC = CPT * TX, TT = TPT * TY;
   const int b = blockIdx.z;
   if (w.status[b] != 0) return;
-  const int c0 = blockIdx.x * NC, t0 = blockIdx.y * TT;
+  const int t0 = blockIdx.y * TT;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   const int rs = w.rs, rt = w.rank[b], T = w.T, M = g.M, N1 = g.N1, R = g.R;
   // dynamic: [sW rs*NC f64][sBb 2*rs*RC f64][sN 2*RC*TT f32][sD 2*RC*NC f32]
@@ -42,7 +44,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
   float* sDp = sNp + 2 * RC * TT;
 #define SN(bf, r_, t_) sNp[((bf) * RC + (r_)) * TT + (t_)]
 #define SD(bf, r_, c_) sDp[((bf) * RC + (r_)) * NC + (c_)]
-  __shared__ int sCase[NC];        // case index of each tile column, -1 = none / skip
+  __shared__ int sCase[NC];        // case index of each tile column, -1 = none
   __shared__ double sInvDen[NC];
   __shared__ int sRowC[NC];
   __shared__ double sInv[2][RC];
@@ -55,17 +57,11 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
   const float* s32 = w.s32 + (size_t)b * N1 * T;
   float* cm = w.cmax + (size_t)b * (N1 + g.NM + g.NI) * T;
   const bool vecN = TT % 4 == 0 && (T % 4) == 0 && (t0 % 4) == 0;
-  // contiguous tile columns allow 16-byte D_base copies; the TOP tile gathers
-  const bool vecD = PASS != PASS_TOP;
 
-  // cases of the TOP tile: ranked by screening key, or simply the first ptop cases
-  auto done_c = [&](int c) -> bool { return w.ranked ? w.done[(size_t)b * N1 + c] != 0 : c < w.ptop; };
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   for (int cc = tid; cc < NC; cc += NTH) {
-    int c = -1;
-    if constexpr (PASS == PASS_TOP)
-      c = w.ranked ? (cc < w.ptop ? w.top[(size_t)b * w.ptop + cc] : -1) : (cc < min(w.ptop, N1) ? cc : -1);
-    else c = c0 + cc < N1 ? c0 + cc : -1;
+    const int c = w.ranked ? (cc < w.ptop ? w.top[(size_t)b * w.ptop + cc] : -1)
+                           : (cc < min(w.ptop, N1) ? cc : -1);
     sCase[cc] = c;
     const bool ok = c >= 0 && w.sc_ok[(size_t)b * N1 + c];
     sInvDen[cc] = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
@@ -77,8 +73,9 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
     sW[j * NC + cc] = c >= 0 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
   }
 
-  // s(c,t) = n0[r_c][t] (FP32, from the update kernel) and the accumulators
+  // s(c,t) = n0[r_c][t] (FP32, from k_n0) and the accumulators
   float acc[CPT][TPT], sv[CPT][TPT];
+  int cnt = 0;
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = sCase[tx * CPT + i];
@@ -87,61 +84,12 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
       const int t = t0 + ty * TPT + jj;
       sv[i][jj] = (c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
       acc[i][jj] = 0.f;
+      cnt += c >= 0 && t < T;
     }
   }
-  bool warp_alive = true;
-  if constexpr (PASS == PASS_SCREEN) {
-    // |F| <= m0(t) + scale_c |s(c,t)| (update kernel): a pair whose bound cannot
-    // exceed a lower bound of its candidate's final metric -- the running metric
-    // (N-0, multi/injection cases, the TOP pass) and, for tasks with islanded cases,
-    // the penalty floor -- cannot change the metric.  Cases already evaluated by the
-    // TOP pass are skipped outright.
-    bool live[CPT];
-    float scl[CPT];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const int cc = tx * CPT + i, c = sCase[cc];
-      live[i] = c >= 0 && !done_c(c);
-      scl[i] = (w.screen && live[i]) ? w.scale[(size_t)b * N1 + c] : 0.f;
-      if (w.screen) live[i] = live[i] && sInvDen[cc] != 0.0;
-    }
-    bool need = false;
-    if (w.screen) {
-      const float pen = w.nisl[b] > 0 ? (float)cfg.penalty : 0.f;
-#pragma unroll
-      for (int jj = 0; jj < TPT; ++jj) {
-        const int t = t0 + ty * TPT + jj;
-        if (t >= T) continue;
-        const float lb = fmaxf(__uint_as_float(w.m32[(size_t)b * T + t]), pen);
-        const float m0 = w.m0[(size_t)b * T + t];
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) need |= live[i] && (m0 + scl[i] * fabsf(sv[i][jj])) > lb;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) need |= live[i];
-    }
-    warp_alive = __any_sync(0xffffffffu, need);
-    // which warps evaluated their pairs: the winner report takes exact maxima from
-    // alive warps and re-derives the dominance bound for the others
-    if ((tid & 31) == 0)
-      w.alive[(((size_t)b * w.nct + blockIdx.x) * w.ntt + blockIdx.y) * SWEEP_WARPS + (tid >> 5)] = warp_alive;
-    const bool block_alive = __syncthreads_or(need);
-    if (!block_alive) return;  // no cp.async in flight yet
-  }
-  if (warp_alive) {
-    // evaluated (case, candidate) pairs, for the roofline accounting
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const int c = sCase[tx * CPT + i];
-      if (c < 0 || (PASS == PASS_SCREEN && done_c(c))) continue;
-#pragma unroll
-      for (int jj = 0; jj < TPT; ++jj) cnt += (t0 + ty * TPT + jj) < T;
-    }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((tid & 31) == 0 && cnt) atomicAdd(w.pairs, (unsigned long long)cnt);
-  }
+  // evaluated (case, candidate) pairs, for the roofline accounting
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((tid & 31) == 0 && cnt) atomicAdd(w.pairs, (unsigned long long)cnt);
 
   // ---- stage one row chunk (async): row ids + 1/rating, B'' rows, n0/rating, D_base
   auto issue = [&](int m0, int buf) {
@@ -179,18 +127,10 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
         cp4(&SN(buf, rr, tt), ok ? &n0s[(size_t)m * T + t] : n0s, ok);
       }
     }
-    if (vecD) {
-      for (int idx = tid; idx < RC * (NC / 4); idx += NTH) {
-        const int rr = idx / (NC / 4), q = idx % (NC / 4), m = m0 + rr, c = c0 + 4 * q;
-        const bool ok = m < M && c < g.N1p;  // rows are zero-padded to N1p
-        cp16(&SD(buf, rr, 4 * q), ok ? &g.D32[(size_t)m * g.N1p + c] : g.D32, ok);
-      }
-    } else {
-      for (int idx = tid; idx < RC * NC; idx += NTH) {
-        const int rr = idx / NC, cc = idx % NC, m = m0 + rr, c = sCase[cc];
-        const bool ok = m < M && c >= 0;
-        cp4(&SD(buf, rr, cc), ok ? &g.D32[(size_t)m * g.N1p + c] : g.D32, ok);
-      }
+    for (int idx = tid; idx < RC * NC; idx += NTH) {
+      const int rr = idx / NC, cc = idx % NC, m = m0 + rr, c = sCase[cc];
+      const bool ok = m < M && c >= 0;
+      cp4(&SD(buf, rr, cc), ok ? &g.D32[(size_t)m * g.N1p + c] : g.D32, ok);
     }
     cp_commit();
   };
@@ -211,24 +151,25 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
     // j-outer register accumulation (W[j][cc] once, B rows broadcast from smem).
     {
       constexpr int RG = NTH / NC;   // row groups
-      constexpr int RPT = RC / RG;   // rows per thread (multiple of 8)
-      static_assert(RPT % 8 == 0, "row tile");
+      constexpr int RPT = RC / RG;   // rows per thread
+      constexpr int KB = RPT < 8 ? RPT : 8;
+      static_assert(RPT % KB == 0, "row tile");
       const int cc = tid % NC, rg = tid / NC;
       const double idn = sInvDen[cc];
       const int rowc = sRowC[cc];
 #pragma unroll
-      for (int kb = 0; kb < RPT; kb += 8) {
-        double v[8];
+      for (int kb = 0; kb < RPT; kb += KB) {
+        double v[KB];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = (double)SD(buf, rg + (kb + k) * RG, cc);
+        for (int k = 0; k < KB; ++k) v[k] = (double)SD(buf, rg + (kb + k) * RG, cc);
         for (int j = 0; j < rt; ++j) {
           const double wj = sW[j * NC + cc];
           const double* Bj = &sBb[(buf * rs + j) * RC + rg];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = fma(Bj[(kb + k) * RG], wj, v[k]);
+          for (int k = 0; k < KB; ++k) v[k] = fma(Bj[(kb + k) * RG], wj, v[k]);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KB; ++k) {
           const int rr = rg + (kb + k) * RG;
           const int row = sRow[buf][rr];
           const double sc = idn * sInv[buf][rr];
@@ -239,62 +180,59 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
       }
     }
     __syncthreads();
-    if (warp_alive) {
-      const int rend = min(RC, M - ch * RC);
-      if (rend == RC) {
-        // two rows x two candidates per step: FFMA2 (packed FP32 FMA, same rounding as
-        // fmaf) and one FMNMX3 (|.| on every input) per accumulator
-        static_assert(TPT % 2 == 0, "candidate pairs");
+    const int rend = min(RC, M - ch * RC);
+    if (rend == RC) {
+      // two rows x two candidates per step: FFMA2 (packed FP32 FMA, same rounding as
+      // fmaf) and one FMNMX3 (|.| on every input) per accumulator
+      static_assert(TPT % 2 == 0, "candidate pairs");
 #pragma unroll 2
-        for (int rr = 0; rr < RC; rr += 2) {
-          float2 l2[2][CPT], n2[2][TPT / 2];
+      for (int rr = 0; rr < RC; rr += 2) {
+        float2 l2[2][CPT], n2[2][TPT / 2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) {
-              const float lv = sL[rr + h][tx * CPT + i];
-              l2[h][i] = make_float2(lv, lv);
-            }
-#pragma unroll
-            for (int p = 0; p < TPT / 2; ++p)
-              n2[h][p] = *reinterpret_cast<const float2*>(&SN(buf, rr + h, ty * TPT + 2 * p));
+          for (int i = 0; i < CPT; ++i) {
+            const float lv = sL[rr + h][tx * CPT + i];
+            l2[h][i] = make_float2(lv, lv);
           }
 #pragma unroll
-          for (int i = 0; i < CPT; ++i)
-#pragma unroll
-            for (int p = 0; p < TPT / 2; ++p) {
-              const float2 sp = make_float2(sv[i][2 * p], sv[i][2 * p + 1]);
-              const float2 f0 = __ffma2_rn(l2[0][i], sp, n2[0][p]);
-              const float2 f1 = __ffma2_rn(l2[1][i], sp, n2[1][p]);
-              acc[i][2 * p] = max3abs(acc[i][2 * p], f0.x, f1.x);
-              acc[i][2 * p + 1] = max3abs(acc[i][2 * p + 1], f0.y, f1.y);
-            }
+          for (int p = 0; p < TPT / 2; ++p)
+            n2[h][p] = *reinterpret_cast<const float2*>(&SN(buf, rr + h, ty * TPT + 2 * p));
         }
-      } else {
-        for (int rr = 0; rr < rend; ++rr) {
-          float l[CPT], n[TPT];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) l[i] = sL[rr][tx * CPT + i];
+        for (int i = 0; i < CPT; ++i)
 #pragma unroll
-          for (int jj = 0; jj < TPT; ++jj) n[jj] = SN(buf, rr, ty * TPT + jj);
+          for (int p = 0; p < TPT / 2; ++p) {
+            const float2 sp = make_float2(sv[i][2 * p], sv[i][2 * p + 1]);
+            const float2 f0 = __ffma2_rn(l2[0][i], sp, n2[0][p]);
+            const float2 f1 = __ffma2_rn(l2[1][i], sp, n2[1][p]);
+            acc[i][2 * p] = max3abs(acc[i][2 * p], f0.x, f1.x);
+            acc[i][2 * p + 1] = max3abs(acc[i][2 * p + 1], f0.y, f1.y);
+          }
+      }
+    } else {
+      for (int rr = 0; rr < rend; ++rr) {
+        float l[CPT], n[TPT];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i)
+        for (int i = 0; i < CPT; ++i) l[i] = sL[rr][tx * CPT + i];
 #pragma unroll
-            for (int jj = 0; jj < TPT; ++jj)
-              acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
-        }
+        for (int jj = 0; jj < TPT; ++jj) n[jj] = SN(buf, rr, ty * TPT + jj);
+#pragma unroll
+        for (int i = 0; i < CPT; ++i)
+#pragma unroll
+          for (int jj = 0; jj < TPT; ++jj)
+            acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
       }
     }
     __syncthreads();
   }
 
-  if (!warp_alive) return;
   // exact per-(case, candidate) maxima for the winner report; the per-candidate max
   // over the tile's cases goes into the running metric
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = sCase[tx * CPT + i];
-    if (c < 0 || (PASS == PASS_SCREEN && done_c(c))) continue;
+    if (c < 0) continue;
 #pragma unroll
     for (int jj = 0; jj < TPT; ++jj) {
       const int t = t0 + ty * TPT + jj;
@@ -317,13 +255,14 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_single(DevGrid g, DevCfg cfg, 
 }
 
 // ---------------------------------------------------------------------------- k_scale
-// Per-case screening scale: an upper bound of max_r |L'(r,c)| over the monitored rows
-// (L' = the FP32 LODF/rating values the sweep multiplies), from an FP32 evaluation
-// L~ = D_base + sum_j B''_j W_j with a rigorous rounding term:
+// Per-case screening scales: for every screening row block b (bdc_device.cuh) an upper
+// bound of max_{r in b} |L'(r,c)| over the monitored rows (L' = the FP32 LODF/rating
+// values the sweeps multiply), from an FP32 evaluation L~ = D_base + sum_j B''_j W_j
+// with a rigorous rounding term:
 //     |L - L~| <= gamma (|D| + sum_j |B''_j| |W_j|),  gamma = (rt + 8) 2^-23,
 // bounded per case by sc_dscale_c + sum_j |W_cj| max_r |B''(r,j)|/rating_r.  The own
 // row contributes 1/rating (L' = -1/rating there), disconnected rows nothing.  Then the
-// ranking key bkey_c = max_t (m0(t) + scale_c |s(c,t)|) (solver.py:634-639, 815).
+// ranking key bkey_c = max_b (max_t m0_b(t) + scale_bc max_t |s(c,t)|) (solver.py:815).
 // One thread per case, monitored-row chunks of D_base and B'' through a cp.async
 // double buffer; 4 rows of B'' per 16-byte shared load.
 namespace {
@@ -339,33 +278,34 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * SC_NC, c = c0 + tid < g.N1 ? c0 + tid : -1;
   const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
+  const int MB = screen_block_rows(M);
   __shared__ __align__(16) float sD[2][SC_RC][SC_NC];
   __shared__ __align__(16) float sB[2][TB][RS][SC_RC];
   __shared__ __align__(16) float sInv[2][TB][SC_RC];
   __shared__ int sdead[TB][RMAX];
   __shared__ int snd[TB], srt[TB];
-  __shared__ float sm0[TB];
+  __shared__ float sm0[TB][SB];
   if (tid < TB) {
     const int b = tb0 + tid;
     const bool on = b < w.Wb && w.status[b] == 0;
     snd[tid] = on ? w.ndead[b] : 0;
     srt[tid] = on ? w.rank[b] : -1;  // -1: slot idle
-    sm0[tid] = 0.f;
   }
   __syncthreads();
   for (int i = tid; i < TB * RMAX; i += SC_NC) {
     const int k = i / RMAX, d = i % RMAX;
     if (d < snd[k]) sdead[k][d] = w.dead[(size_t)(tb0 + k) * RMAX + d];
   }
-  // max_t m0(t) of each task (ranking key)
+  // max_t m0_b(t) of each task and block (ranking key)
   {
     const int lane = tid & 31, wid = tid >> 5;
-    for (int k = wid; k < TB; k += SC_NC / 32) {
-      if (srt[k] < 0) continue;
+    for (int kb = wid; kb < TB * SB; kb += SC_NC / 32) {
+      const int k = kb / SB, blk = kb % SB;
       float v = 0.f;
-      for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0[(size_t)(tb0 + k) * T + t]);
+      if (srt[k] >= 0)
+        for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0b[((size_t)(tb0 + k) * SB + blk) * T + t]);
       for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) sm0[k] = v;
+      if (lane == 0) sm0[k][blk] = v;
     }
   }
   __syncthreads();
@@ -378,15 +318,48 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
   for (int k = 0; k < TB; ++k)
 #pragma unroll
     for (int j = 0; j < RS; ++j) wr[k][j] = 0.f;
+  // per task: |1/den| and the rounding term of the FP32 evaluation (0 if infeasible)
+  float aid[TB], rnd[TB], keyv[TB], mx[TB];
+#pragma unroll
+  for (int k = 0; k < TB; ++k) { aid[k] = 0.f; rnd[k] = 0.f; keyv[k] = 0.f; mx[k] = 0.f; }
   if (c >= 0) {
 #pragma unroll
     for (int k = 0; k < TB; ++k) {
-      const int b = tb0 + k;
+      const int b = tb0 + k, rt = srt[k];
 #pragma unroll
       for (int j = 0; j < RS; ++j)
-        if (j < srt[k]) wr[k][j] = (float)w.Wsc[((size_t)b * N1 + c) * rs + j];
+        if (j < rt) wr[k][j] = (float)w.Wsc[((size_t)b * N1 + c) * rs + j];
+      if (rt >= 0 && w.sc_ok[(size_t)b * N1 + c]) {
+        float wsum = 0.f;
+        for (int j = 0; j < rt; ++j)
+          wsum += (float)fabs(w.Wsc[((size_t)b * N1 + c) * rs + j]) * w.bmax[(size_t)b * rs + j];
+        const float gam = (float)(rt + 8) * 1.1920929e-7f;
+        aid[k] = (float)fabs(1.0 / w.den[(size_t)b * N1 + c]);
+        rnd[k] = gam * ((float)g.sc_dscale[c] + wsum);
+      }
     }
   }
+  const int rowc = c >= 0 ? g.sc_row[c] : -1;
+  const int ownp = c >= 0 ? g.row_mon_pos[rowc] : -1;
+  // block maxima -> scale_bc (written for every block, 0 for infeasible cases)
+  auto finish_block = [&](int blk) {
+    if (c < 0) return;
+#pragma unroll
+    for (int k = 0; k < TB; ++k) {
+      const int b = tb0 + k;
+      if (srt[k] < 0) continue;
+      float U = 0.f;
+      if (aid[k] != 0.f) {
+        U = aid[k] * (mx[k] + rnd[k]);
+        if (ownp >= 0 && ownp / MB == blk && !is_dead(sdead[k], snd[k], rowc))
+          U = fmaxf(U, (float)g.inv_rating[ownp]);
+        U *= 1.f + 4e-6f;
+      }
+      w.scale[((size_t)b * SB + blk) * N1 + c] = U;
+      keyv[k] = fmaxf(keyv[k], sm0[k][blk] + U * w.smax[(size_t)b * N1 + c]);
+      mx[k] = 0.f;
+    }
+  };
   auto issue = [&](int m0, int buf) {
     for (int idx = tid; idx < SC_RC * (SC_NC / 4); idx += SC_NC) {
       const int rr = idx / (SC_NC / 4), q = 4 * (idx % (SC_NC / 4)), m = m0 + rr;
@@ -406,12 +379,9 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
     }
     cp_commit();
   };
-  float mx[TB];
-#pragma unroll
-  for (int k = 0; k < TB; ++k) mx[k] = 0.f;
-  const int ownp = c >= 0 ? g.row_mon_pos[g.sc_row[c]] : -1;
   issue(0, 0);
   const int nchunks = (M + SC_RC - 1) / SC_RC;
+  int nblk = 0;  // blocks finished
   for (int ch = 0; ch < nchunks; ++ch) {
     const int buf = ch & 1, m0 = ch * SC_RC;
     if (ch + 1 < nchunks) {
@@ -445,29 +415,155 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
         mx[k] = fmaxf(mx[k], (r4 + 3 == ownrr) ? 0.f : fabsf(l3) * iq.w);
       }
     }
+    // a block ends at a multiple of MB (a multiple of SC_RC) or at the last row
+    if ((m0 + SC_RC) % MB == 0 || ch + 1 == nchunks) finish_block(nblk++);
     __syncthreads();
   }
+  for (; nblk < SB; ++nblk) finish_block(nblk);  // empty blocks (small M)
   if (c < 0) return;
 #pragma unroll
   for (int k = 0; k < TB; ++k) {
-    const int b = tb0 + k, rt = srt[k];
-    if (rt < 0) continue;
-    const bool ok = w.sc_ok[(size_t)b * N1 + c] != 0;
-    float U = 0.f;
-    if (ok) {
-      const double idn = 1.0 / w.den[(size_t)b * N1 + c];
-      float wsum = 0.f;
-      for (int j = 0; j < rt; ++j)
-        wsum += (float)fabs(w.Wsc[((size_t)b * N1 + c) * rs + j]) * w.bmax[(size_t)b * rs + j];
-      const float gam = (float)(rt + 8) * 1.1920929e-7f;
-      U = (float)fabs(idn) * (mx[k] + gam * ((float)g.sc_dscale[c] + wsum));
-      const int rowc = g.sc_row[c];
-      if (ownp >= 0 && !is_dead(sdead[k], snd[k], rowc)) U = fmaxf(U, (float)g.inv_rating[ownp]);
-      U *= 1.f + 4e-6f;
+    const int b = tb0 + k;
+    if (srt[k] < 0) continue;
+    w.bkey[(size_t)b * N1 + c] = aid[k] != 0.f ? __float_as_uint(keyv[k]) : 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------- k_live
+// The screen proper, pair by pair: for a case outside the TOP tile, candidate t is live
+// iff max_b (m0_b(t) + scale_bc |s(c,t)|) > lb(t) = max(running metric, penalty floor)
+// (every TOP case, multi/injection case and the N-0 flows are already in m32).  A
+// skipped pair is provably dominated: it cannot change the metric (solver.py:809-812).
+// With the screen off every pair of a feasible case is live.  Writes the live map
+// (read by the winner report) and queues cases with live candidates for k_pairs.
+// CTA = (task, LC cases), warp per case, lanes over candidates; the block bounds and
+// lb of the task are staged once per CTA.
+namespace {
+constexpr int LC = 64;         // cases per k_live CTA
+constexpr int LV_TMAX = 1024;  // candidates staged in shared memory (larger T: global reads)
+}
+__global__ void __launch_bounds__(256) k_live(DevGrid g, DevCfg cfg, Work w) {
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (w.status[b] != 0) return;
+  const int T = w.T, N1 = g.N1, TW = w.TW;
+  __shared__ float sLb[LV_TMAX];
+  __shared__ float sM0[SB][LV_TMAX];
+  const bool staged = T <= LV_TMAX;
+  const float pen = w.nisl[b] > 0 ? (float)cfg.penalty : 0.f;
+  const float* m32 = reinterpret_cast<const float*>(w.m32) + (size_t)b * T;
+  const float* m0b = w.m0b + (size_t)b * SB * T;
+  if (staged && w.screen) {
+    for (int t = tid; t < T; t += 256) {
+      sLb[t] = fmaxf(m32[t], pen);
+#pragma unroll
+      for (int blk = 0; blk < SB; ++blk) sM0[blk][t] = m0b[(size_t)blk * T + t];
     }
-    w.scale[(size_t)b * N1 + c] = U;
-    // ranking key for the TOP tile (ordering only; exactness rests on the per-pair bound)
-    w.bkey[(size_t)b * N1 + c] = ok ? __float_as_uint(sm0[k] + U * w.smax[(size_t)b * N1 + c]) : 0u;
+  }
+  __syncthreads();
+  for (int c = blockIdx.x * LC + wid; c < min(N1, (blockIdx.x + 1) * LC); c += 8) {
+    uint32_t* lw = w.live + ((size_t)b * N1 + c) * TW;
+    const bool done = w.ranked ? w.done[(size_t)b * N1 + c] != 0 : c < w.ptop;
+    const bool ok = w.sc_ok[(size_t)b * N1 + c] != 0;
+    if (done || !ok) {
+      for (int tw = lane; tw < TW; tw += 32) lw[tw] = 0u;
+      continue;
+    }
+    float scl[SB];
+#pragma unroll
+    for (int blk = 0; blk < SB; ++blk) scl[blk] = w.screen ? w.scale[((size_t)b * SB + blk) * N1 + c] : 0.f;
+    const float* sc = w.s32 + ((size_t)b * N1 + c) * T;
+    int nlive = 0;
+    for (int tw = 0; tw < TW; ++tw) {
+      const int t = tw * 32 + lane;
+      bool live = t < T;
+      if (live && w.screen) {
+        const float as = fabsf(sc[t]);
+        float bound = 0.f;
+#pragma unroll
+        for (int blk = 0; blk < SB; ++blk)
+          bound = fmaxf(bound, (staged ? sM0[blk][t] : m0b[(size_t)blk * T + t]) + scl[blk] * as);
+        live = bound > (staged ? sLb[t] : fmaxf(m32[t], pen));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, live);
+      if (lane == 0) lw[tw] = word;
+      nlive += __popc(word);
+    }
+    if (lane == 0 && nlive) {
+      const unsigned q = atomicAdd(w.qcount, 1u);
+      w.queue[q] = make_int2(b, c);
+      atomicAdd(w.pairs, (unsigned long long)nlive);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- k_pairs
+// The queued (task, case) items: a warp per item, lanes over the 32 candidates of a
+// live word, monitored rows in chunks of PR: each lane forms PR/32 LODF entries in FP64
+// (the same expression and rounding as k_top) into the warp's shared slice, then every
+// lane streams the chunk for its candidate (n0/rating reads coalesced across lanes).
+// Persistent grid; the item count is read on the device.
+namespace {
+constexpr int PR = 128;  // rows per chunk
+constexpr int PW = 8;    // warps per CTA
+}
+__global__ void __launch_bounds__(PW * 32) k_pairs(DevGrid g, Work w) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ float sL[PW][PR];
+  __shared__ double sWc[PW][RMAX];
+  const unsigned nq = *w.qcount;
+  const int M = g.M, N1 = g.N1, R = g.R, T = w.T, TW = w.TW, rs = w.rs;
+  for (unsigned it = blockIdx.x * PW + wid; it < nq; it += gridDim.x * PW) {
+    const int2 bc = w.queue[it];
+    const int b = bc.x, c = bc.y;
+    const int rt = w.rank[b], nd = w.ndead[b];
+    const int* dead = w.dead + (size_t)b * RMAX;
+    const double* Bm = w.Bm + (size_t)b * rs * R;
+    const float* n0s = w.n0s + (size_t)b * M * T;
+    const double idn = 1.0 / w.den[(size_t)b * N1 + c];  // queued cases are feasible
+    const int rowc = g.sc_row[c];
+    for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+    __syncwarp();
+    const uint32_t* lw = w.live + ((size_t)b * N1 + c) * TW;
+    float* cm = w.cmax + (size_t)b * (N1 + g.NM + g.NI) * T + (size_t)c * T;
+    for (int tw = 0; tw < TW; ++tw) {
+      const uint32_t word = lw[tw];
+      if (word == 0u) continue;
+      const int t = tw * 32 + lane;
+      const bool mine = (word >> lane) & 1u;
+      const float s = mine ? w.s32[((size_t)b * N1 + c) * T + t] : 0.f;
+      float acc = 0.f;
+      for (int m0 = 0; m0 < M; m0 += PR) {
+#pragma unroll
+        for (int q = 0; q < PR / 32; ++q) {
+          const int m = m0 + lane + 32 * q;
+          float lv = 0.f;
+          if (m < M) {
+            const int row = g.mon_row[m];
+            if (!is_dead(dead, nd, row)) {
+              const double inv = g.inv_rating[m];
+              if (row == rowc) {
+                lv = (float)(-inv);
+              } else {
+                double v = (double)g.D32[(size_t)m * g.N1p + c];
+                for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], sWc[wid][j], v);
+                lv = (float)(v * (idn * inv));
+              }
+            }
+          }
+          sL[wid][lane + 32 * q] = lv;
+        }
+        __syncwarp();
+        const int rend = min(PR, M - m0);
+        if (mine)
+          for (int rr = 0; rr < rend; ++rr)
+            acc = fmaxf(acc, fabsf(fmaf(sL[wid][rr], s, n0s[(size_t)(m0 + rr) * T + t])));
+        __syncwarp();
+      }
+      if (mine) {
+        cm[t] = acc;
+        atomic_max_pos(&w.m32[(size_t)b * T + t], acc);
+      }
+    }
   }
 }
 
@@ -488,13 +584,11 @@ void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
   else if (r <= 16) launch_scale_t<16, 1>(g, w, s);
   else launch_scale_t<32, 1>(g, w, s);
 }
-}  // namespace
 
-namespace {
-
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB, int PASS>
-void launch_single_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   constexpr int NC = CPT * TX, TT = TPT * TY;
+  static_assert(NC == TOPC, "TOP tile = TOPC cases");
   const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
                      (2 * (size_t)RC * TT + 2 * (size_t)RC * NC) * sizeof(float);
   static int max_dyn = -1;
@@ -504,38 +598,41 @@ void launch_single_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_single<CPT, TPT, TX, TY, RC, MINB, PASS>);
+    cudaFuncGetAttributes(&fa, k_top<CPT, TPT, TX, TY, RC, MINB>);
     max_dyn = optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_single<CPT, TPT, TX, TY, RC, MINB, PASS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaFuncSetAttribute(k_top<CPT, TPT, TX, TY, RC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
-  const int ctiles = PASS == PASS_TOP ? 1 : (g.N1 + NC - 1) / NC;
-  dim3 grid(ctiles, (w.T + TT - 1) / TT, w.Wb);
-  k_single<CPT, TPT, TX, TY, RC, MINB, PASS><<<grid, TX * TY, dyn, s>>>(g, c, w);
+  dim3 grid(1, (w.T + TT - 1) / TT, w.Wb);
+  k_top<CPT, TPT, TX, TY, RC, MINB><<<grid, TX * TY, dyn, s>>>(g, c, w);
 }
 
-template <int PASS>
-void launch_pass(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  // must match sweep_shape(T) (bdc_device.cuh): the report decodes the alive map with it
-  const SweepShape sh = sweep_shape(w.T);
-  if (sh.TPT == 16) launch_single_t<2, 16, 32, 8, 32, 2, PASS>(g, c, w, s);      // 64 cases x 128 candidates
-  else if (sh.TPT == 8) launch_single_t<2, 8, 32, 8, 32, 3, PASS>(g, c, w, s);   // 64 x 64
-  else if (sh.TX == 32) launch_single_t<4, 4, 32, 8, 32, 3, PASS>(g, c, w, s);   // 128 x 32
-  else if (sh.TPT == 4) launch_single_t<4, 4, 64, 4, 32, 3, PASS>(g, c, w, s);   // 256 x 16
-  else launch_single_t<4, 2, 64, 4, 32, 3, PASS>(g, c, w, s);                    // 256 x 8
+void launch_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  if (w.T >= 96) launch_top_t<1, 8, 16, 16, 64, 2>(g, c, w, s);       // 16 cases x 128 candidates
+  else if (w.T >= 48) launch_top_t<1, 4, 16, 16, 64, 2>(g, c, w, s);  // 16 x 64
+  else launch_top_t<1, 2, 16, 16, 64, 2>(g, c, w, s);                 // 16 x 32
 }
-
 }  // namespace
 
 void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   if (g.N1 == 0 || g.M == 0) return;
   if (w.ranked) {
-    // per-case scale bound and ranking key, then the top tile by key
+    // per-case block scales and ranking key, then the TOP tile by key
     launch_scale(g, w, s);
     launch_topk(g, w, s);
   }
-  launch_pass<PASS_TOP>(g, c, w, s);
-  if (g.N1 > w.ptop) launch_pass<PASS_SCREEN>(g, c, w, s);
+  launch_top(g, c, w, s);
+  if (g.N1 > w.ptop) {
+    k_live<<<dim3((g.N1 + LC - 1) / LC, w.Wb), 256, 0, s>>>(g, c, w);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    k_pairs<<<nsm * 4, PW * 32, 0, s>>>(g, w);
+  }
+}
+
+int single_launches(const DevGrid& g, const Work& w) {
+  if (g.N1 == 0 || g.M == 0) return 0;
+  return (w.ranked ? 2 : 0) + 1 + (g.N1 > w.ptop ? 2 : 0);
 }
 
 }  // namespace bdc

@@ -616,6 +616,8 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   __shared__ float sSmax[N0_ROWS];  // max_t |s(c,t)| of the CTA's single-case rows
   __shared__ int sdead[RMAX];
   __shared__ unsigned tmax[TCH];
+  __shared__ unsigned tmaxb[SB][TCH];  // per screening row block
+  const int MB = screen_block_rows(M);
   const int nd = w.ndead[b];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   __syncthreads();
@@ -651,6 +653,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   }
   for (int tc = 0; tc < T; tc += TCH) {
     for (int i = tid; i < TCH; i += NT) tmax[i] = 0u;
+    for (int i = tid; i < SB * TCH; i += NT) (&tmaxb[0][0])[i] = 0u;
     for (int idx = tid; idx < rt * TCH; idx += NT) {
       const int j = idx / TCH, t = tc + idx % TCH;
       sY[idx] = t < T ? Y[(size_t)j * T + t] : 0.0;
@@ -676,6 +679,9 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
 #pragma unroll
           for (int k = 0; k < TPL; ++k) acc[i][k] = fma(bv[i], yv[k], acc[i][k]);
       }
+      float gm[TPL];  // this row group's max per candidate (one screening block: MB % RG == 0)
+#pragma unroll
+      for (int k = 0; k < TPL; ++k) gm[k] = 0.f;
 #pragma unroll
       for (int i = 0; i < RG; ++i) {
         const int li = r0 + i0 + i;
@@ -690,7 +696,10 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
           if (t >= T) continue;
           const float v = live ? (float)(acc[i][k] * scl) : 0.f;
           dst[t] = v;
-          if (li < M) mx[k] = fmaxf(mx[k], fabsf(v));
+          if (li < M) {
+            mx[k] = fmaxf(mx[k], fabsf(v));
+            gm[k] = fmaxf(gm[k], fabsf(v));
+          }
           rmax = fmaxf(rmax, fabsf(v));
         }
         if (li >= M) {  // warp-uniform: the row's max over this candidate chunk
@@ -698,15 +707,25 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
           if (lane == 0) sSmax[i0 + i] = fmaxf(sSmax[i0 + i], rmax);
         }
       }
+      if (r0 + i0 < M) {
+        const int blk = (r0 + i0) / MB;
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) atomicMax(&tmaxb[blk][lane + 32 * k], __float_as_uint(gm[k]));
+      }
     }
 #pragma unroll
     for (int k = 0; k < TPL; ++k) atomicMax(&tmax[lane + 32 * k], __float_as_uint(mx[k]));
     __syncthreads();
-    if (r0 < M)  // CTAs with monitored rows fold their per-candidate max into m0 / m32
+    if (r0 < M) {  // CTAs with monitored rows fold their per-candidate max into m0 / m32
       for (int i = tid; i < min(TCH, T - tc); i += NT) {
         atomicMax(&w.m32[(size_t)b * T + tc + i], tmax[i]);
         atomicMax(reinterpret_cast<unsigned*>(&w.m0[(size_t)b * T + tc + i]), tmax[i]);
       }
+      const int blo = r0 / MB, bhi = (min(r0 + nr, M) - 1) / MB;
+      for (int blk = blo; blk <= bhi; ++blk)
+        for (int i = tid; i < min(TCH, T - tc); i += NT)
+          atomicMax(reinterpret_cast<unsigned*>(&w.m0b[((size_t)b * SB + blk) * T + tc + i]), tmaxb[blk][i]);
+    }
     __syncthreads();
   }
   for (int i = tid; i < nr; i += NT)
