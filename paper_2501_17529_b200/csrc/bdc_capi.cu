@@ -216,6 +216,13 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   UP(mc_order, G->NM);
   UP(mb_row, G->NMB);
   UP(Dm64, (size_t)G->NMB * G->R);
+  // D_base on monitored rows, case-major, for the winner report's coalesced sweeps
+  if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
+    std::vector<double> dm((size_t)G->N1 * G->M);
+    for (int c = 0; c < G->N1; ++c)
+      for (int p = 0; p < G->M; ++p) dm[(size_t)c * G->M + p] = G->D64[(size_t)c * G->R + G->mon_row[p]];
+    e = upload(dm.data(), dm.size(), &g.DM64, o);
+  }
   UP(ic_slot, G->NI);
   UP(ic_col, G->NI);
   UP(ic_sp, G->NI);
@@ -324,7 +331,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_Wm = L.add(B * g.NMB * rs * 8), o_mi = L.add(B * g.NM * MMAX * MMAX * 8), o_mo = L.add(B * g.NM);
   size_t o_ca = L.add(B * g.NI * rs * 8), o_cb = L.add(B * g.NI * rs * 8);
   size_t o_Y = L.add(B * rs * T * 8), o_n0s = L.add(B * g.M * T * 4);
-  size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8);
+  size_t o_m32 = L.add(B * T * 4), o_n0b = L.add(B * g.R * 8), o_n0m = L.add(B * g.M * 8);
+  size_t o_bmon = L.add(B * (size_t)rs * g.M * 8);
   size_t o_cmax = L.add(B * (size_t)(g.N1 + g.NM + g.NI) * T * 4);
   const size_t NTERM = ((size_t)g.NM + g.NI) * g.MT;
   size_t o_Lo = L.add(B * (size_t)g.M * NTERM * 4), o_So = L.add(B * NTERM * T * 4);
@@ -334,12 +342,13 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
   size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)SB * g.N1 * 4);
   size_t o_m0b = L.add(B * (size_t)SB * T * 4);
-  const int TW = (T + 31) / 32;
-  size_t o_live = L.add(B * (size_t)g.N1 * TW * 4), o_q = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 8);
+  const size_t nitems = B * (size_t)((g.N1 + TOPC - 1) / TOPC) * (size_t)((T + top_tile_cands(T) - 1) / top_tile_cands(T));
+  size_t o_ll = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_lc = L.add(B * 4);
+  size_t o_q = L.add((nitems > 0 ? nitems : 1) * 8);
   size_t o_s32 = L.add(B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
   size_t o_top = L.add(B * (size_t)TOPC * 4), o_done = L.add(B * (size_t)g.N1);
   const int nslot = RSEL_WARPS + (g.N1 + RCW - 1) / RCW;
-  size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4);
+  size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4), o_th = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
   size_t o_b32 = L.add(B * (size_t)rs * g.M * 4), o_bmx = L.add(B * (size_t)rs * 4);
@@ -360,7 +369,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.Wm = (double*)(base + o_Wm); x.minv = (double*)(base + o_mi); x.mc_ok = (uint8_t*)(base + o_mo);
   x.cia = (double*)(base + o_ca); x.cib = (double*)(base + o_cb);
   x.Y = (double*)(base + o_Y); x.n0s = (float*)(base + o_n0s);
-  x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b);
+  x.m32 = (uint32_t*)(base + o_m32); x.n0b = (double*)(base + o_n0b); x.n0m = (double*)(base + o_n0m);
+  x.Bmon = (double*)(base + o_bmon);
   x.cmax = (float*)(base + o_cmax);
   x.Lo = (float*)(base + o_Lo); x.So = (float*)(base + o_So); x.NTERM = (int)NTERM;
   x.metric = (double*)(base + o_met); x.best = (int64_t*)(base + o_best); x.feasible = (uint8_t*)(base + o_fe);
@@ -378,10 +388,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = TOPC;
   x.m0b = (float*)(base + o_m0b);
-  x.live = (uint32_t*)(base + o_live); x.TW = TW;
+  x.llist = (int*)(base + o_ll); x.lcnt = (int*)(base + o_lc);
   x.queue = (int2*)(base + o_q);
   x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
-  x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.nslot = nslot;
+  x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.theta = (float*)(base + o_th); x.nslot = nslot;
   x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);
   x.pflow = (double*)(base + o_pf); x.prel = (double*)(base + o_pr); x.pmax = (double*)(base + o_pm);
   return L.total;
@@ -562,6 +572,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0b, 0, (size_t)nb * SB * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.lcnt, 0, (size_t)nb * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);

@@ -28,13 +28,15 @@ constexpr float SCREEN_EPS = 1e-3f;
 //         only when they fall in the same block, which is much tighter than one block.
 constexpr int TOPC = 16;
 constexpr int SB = 4;
+// Candidates per TOP-tile CTA (bdc_single.cu launch_top).
+__host__ __device__ inline int top_tile_cands(int T) { return T >= 96 ? 128 : (T >= 48 ? 64 : 32); }
 // Rows per screening block: a multiple of 16 (the k_scale row chunk, also a multiple of
 // the k_n0 row group), so a chunk never straddles two blocks; block of position m = m / MB.
 __host__ __device__ inline int screen_block_rows(int M) {
   const int per = (M + SB - 1) / SB;
   return ((per + 15) / 16) * 16 > 0 ? ((per + 15) / 16) * 16 : 16;
 }
-constexpr int RCW = 128;        // single cases per CTA of the winner report sweep
+constexpr int RCW = 64;         // single cases per CTA of the winner report sweep (8 per warp)
 constexpr int RSEL_WARPS = 8;   // partial report lists written by the report-select kernel
 
 // Grid tables, device-resident for the session lifetime.
@@ -44,6 +46,7 @@ struct DevGrid {
   int MT;   // correction-term slots per multi/injection case (max branches, pow2 >= 2)
   const double *P0, *P0T, *f0, *p_base, *rating, *inv_rating, *sub_elem_b, *slot_sp;
   const double *sc_delta, *sc_dscale, *D64, *Dm64, *ic_sp;
+  const double* DM64;  // (N1, M) D_base on monitored rows, case-major (winner report)
   const float* D32;
   const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;
   const int *sub_elem_row, *slot_sub, *slot_col, *sc_row, *sc_order, *mc_start, *mc_order;
@@ -86,10 +89,11 @@ struct Work {
   float* n0s;     // (Wb, M, T)    N-0 flows / rating on monitored rows, FP32
   uint32_t* m32;  // (Wb, T)       FP32 screening metric (float bits, >= 0)
   float* cmax;    // (Wb, N1+NM+NI, T) FP32 max |F|/rating per (case, candidate); for single
-                  //                   cases valid where evaluated (TOP case or live bit set)
-  uint32_t* live; // (Wb, N1, TW)  bit t of case c: pair evaluated by k_pairs (bound failed)
-  int TW;         // 32-bit words per case of the live bitmap (ceil(T / 32))
-  int2* queue;    // (Wb * N1)     (task, case) items with at least one live candidate
+                  //                   cases valid where evaluated (done[c] != 0, or c < ptop
+                  //                   when the cases are not ranked)
+  int* llist;     // (Wb, N1)      live single cases of each task (screen failed), any order
+  int* lcnt;      // (Wb)          their number
+  int2* queue;    // (Wb * ceil(N1/TOPC) * candidate tiles)  k_pairs items (task, group<<16 | tile)
   unsigned* qcount;  // items in the queue (device counter, reset per wave)
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
@@ -104,16 +108,20 @@ struct Work {
   uint32_t* bkey; // (Wb, N1)      ranking key max_t m0(t) + scale_c max_t |s(c,t)| (float bits)
   float* smax;    // (Wb, N1)      max_t |s(c,t)|
   int* top;       // (Wb, ptop)    the ptop cases with the largest bound, ascending index
-  uint8_t* done;  // (Wb, N1)      1 if the case is in top (evaluated in the first pass)
+  uint8_t* done;  // (Wb, N1)      1: TOP case (k_topk), 2: live case (k_live); both evaluated
+                  //               for every candidate
   // multi-branch / injection cases as correction terms: F = n0 + sum_j Lo[j] So[j],
   // MT term slots per case q (multi: one per outaged branch, injection: 2), zero-padded
   float* Lo;      // (Wb, M, NQ, MT)  correction columns / rating on monitored rows
   float* So;      // (Wb, NQ, MT, T)  per-candidate multipliers
   int NTERM;      // NQ * MT, NQ = NM + NI
   double* n0b;    // (Wb, R)       winner's N-0 column (report scratch)
+  double* n0m;    // (Wb, M)       the same on monitored positions
+  double* Bmon;   // (Wb, rs, M)   B'' on monitored positions, FP64 (winner report)
   // winner report: listed cases and per-slot partial top-kg lists
   int* rlist;     // (Wb, N1)      single cases the FP64 report must visit, ascending
   int* rcnt;      // (Wb)          their number
+  float* theta;   // (Wb)          report floor: kg-th largest exact case max - 2 eps (or -1)
   int nslot;      // RSEL_WARPS + ceil(N1 / RCW) partial lists per task
   int* pcase;     // (Wb, nslot, KMAX) contingency order of each partial entry
   int* ppos;      // (Wb, nslot, KMAX) monitored position

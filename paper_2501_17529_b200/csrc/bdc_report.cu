@@ -167,11 +167,12 @@ __device__ int warp_merge_lists(const double (*lv)[KMAX], const int (*li)[KMAX],
 }
 
 // Was the (single case c, candidate t) pair evaluated by the N-1 stage, i.e. is
-// cmax[c][t] its exact FP32 maximum?  TOP cases always are, the others iff the screen
-// found the pair live (bdc_single.cu).
+// cmax[c][t] its exact FP32 maximum?  TOP cases and live cases were evaluated for every
+// candidate (bdc_single.cu); the others are dominated.
 __device__ __forceinline__ bool pair_evaluated(const DevGrid& g, const Work& w, int b, int c, int t) {
-  if (w.ranked ? w.done[(size_t)b * g.N1 + c] != 0 : c < w.ptop) return true;
-  return (w.live[((size_t)b * g.N1 + c) * w.TW + (t >> 5)] >> (t & 31)) & 1u;
+  (void)t;
+  if (!w.ranked && c < w.ptop) return true;
+  return g.N1 > w.ptop && w.done[(size_t)b * g.N1 + c] != 0;
 }
 
 // The dominance bound of a skipped pair: max_b (m0_b(t) + scale_bc |s(c,t)|).
@@ -230,6 +231,8 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
       for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + r], sY[j], v);
     }
     n0b[r] = v;
+    const int p = g.row_mon_pos[r];
+    if (p >= 0) w.n0m[(size_t)b * M + p] = v;
   }
   __syncthreads();
 
@@ -292,6 +295,7 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   }
   __syncthreads();
   const float theta = sTheta;
+  if (tid == 0) w.theta[b] = theta;
   // single cases to visit, ascending: warp-contiguous segments, ordered compaction
   {
     const int seg = (N1 + RW - 1) / RW, s0 = wid * seg, s1 = min(N1, s0 + seg);
@@ -342,7 +346,9 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
       order = g.ic_order[q];
     }
     lt.clear();
-    const double thresh = warp_thresh(wl[wid], kg);
+    // entries below theta cannot reach the final top-kg (it holds the kg largest case
+    // maxima, all >= theta): a floor for the lane lists
+    const double thresh = fmax(warp_thresh(wl[wid], kg), (double)theta);
     if (kind == 1) {
       const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
       for (int i = lane; i < m * m; i += 32) sMinv[wid][i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
@@ -410,135 +416,112 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
 
 // --------------------------------------------------------------------------- k_rsweep
 // Winner report, part 2: the listed single cases in FP64 for the winning candidate,
-// RCW cases per CTA, one case per thread; monitored-row chunks of B'' rows, the N-0
-// column and 1/rating are staged in shared memory once for all the CTA's cases.
-// Each thread keeps its case's stable top-kc (rel desc, position asc; solver.py:287-299)
-// and max; the CTA merges them into its partial top-kg by (rel desc, case order,
-// position) (_merge_entries, solver.py:302-318).
-namespace {
-constexpr int SRC = 64;  // monitored rows per chunk
-}
-
+// RCW cases per CTA, a warp per case with lanes over monitored rows (coalesced reads of
+// D_base, B'', the N-0 column and 1/rating).  Each lane keeps its rows' stable top-kc
+// (rel desc, position asc; solver.py:287-299), merged per case into the warp's top-kg by
+// (rel desc, case order, position) (_merge_entries, solver.py:302-318); the CTA merges
+// its warps' lists into one partial slot.
 template <int KC>
-__global__ void __launch_bounds__(RCW) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
   const int n = w.rcnt[b];
   if (tile * RCW >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int R = g.R, M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kg = cfg.kg;
-  extern __shared__ __align__(16) unsigned char rsm[];
-  double* sW = reinterpret_cast<double*>(rsm);  // [rt][RCW]
-  double* sB = sW + (size_t)rs * RCW;           // [rt][SRC]
-  __shared__ double sN0[SRC], sInv[SRC];
-  __shared__ int sRow[SRC];
-  __shared__ int sdead[RMAX];
-  __shared__ double wr[RCW / 32];
-  __shared__ int wo[RCW / 32], wp[RCW / 32], wsrc[RCW / 32];
-  __shared__ int pick_src;
+  const int M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kc = cfg.kc, kg = cfg.kg;
+  __shared__ WarpList wl[RW];
+  __shared__ double sWc[RW][RMAX];
+  __shared__ double wmax[RW];
+  __shared__ int sdeadp[RMAX];  // monitored positions of the disconnected rows (-1: unmonitored)
   const int nd = w.ndead[b];
-  if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
-  const int li = tile * RCW + tid;
-  const int c = li < n ? w.rlist[(size_t)b * N1 + li] : -1;
-  const double* n0b = w.n0b + (size_t)b * R;
-  const double* Bm = w.Bm + (size_t)b * rs * R;
-  int rowc = -1, order = INT_MAX;
-  double idn = 0.0, sc = 0.0;
-  if (c >= 0) {
-    rowc = g.sc_row[c];
-    order = g.sc_order[c];
-    idn = 1.0 / w.den[(size_t)b * N1 + c];
-    sc = n0b[rowc];
-    for (int j = 0; j < rt; ++j) sW[j * RCW + tid] = w.Wsc[((size_t)b * N1 + c) * rs + j];
-  }
-  const double* Dc = g.D64 + (size_t)(c >= 0 ? c : 0) * R;
-  LaneTop<KC> lt;
-  lt.clear();
+  if (tid < nd) sdeadp[tid] = g.row_mon_pos[w.dead[(size_t)b * RMAX + tid]];
+  if (lane == 0) wl[wid].n = 0;
+  __syncthreads();
+  const double* n0m = w.n0m + (size_t)b * M;
+  const double* Bmon = w.Bmon + (size_t)b * rs * M;
+  // the final top-kg holds the kg largest case maxima, all >= theta (k_rsel): entries
+  // below it are never reported, so they never enter a list
+  const double floor_rel = (double)w.theta[b];
   double mymax = 0.0;
-  __syncthreads();
-  for (int m0 = 0; m0 < M; m0 += SRC) {
-    for (int rr = tid; rr < SRC; rr += RCW) {
-      const int m = m0 + rr;
-      int row = -1;
-      if (m < M) {
-        row = g.mon_row[m];
-        if (is_dead(sdead, nd, row)) row = -1;
+  LaneTop<KC> lt;
+  constexpr int U = 4;  // rows per lane per step: independent loads in flight
+  const int end = min(n, (tile + 1) * RCW);
+  for (int li = tile * RCW + wid; li < end; li += RW) {
+    const int c = w.rlist[(size_t)b * N1 + li];
+    const int rowc = g.sc_row[c], order = g.sc_order[c], ownp = g.row_mon_pos[rowc];
+    const double idn = 1.0 / w.den[(size_t)b * N1 + c];
+    const double sc = w.n0b[(size_t)b * g.R + rowc];
+    for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+    __syncwarp();
+    const double* Dc = g.DM64 + (size_t)c * M;
+    const double thresh = fmax(warp_thresh(wl[wid], kg), floor_rel);
+    lt.clear();
+    for (int p0 = lane; p0 < M; p0 += 32 * U) {
+      double dv[U], nv[U], iv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + 32 * u;
+        const bool ok = p < M;
+        dv[u] = ok ? __ldg(&Dc[p]) : 0.0;
+        nv[u] = ok ? n0m[p] : 0.0;
+        iv[u] = ok ? __ldg(&g.inv_rating[p]) : 0.0;
       }
-      sRow[rr] = row;
-      sN0[rr] = row >= 0 ? n0b[row] : 0.0;
-      sInv[rr] = m < M ? g.inv_rating[m] : 0.0;
-    }
-    for (int idx = tid; idx < rt * SRC; idx += RCW) {
-      const int j = idx / SRC, rr = idx % SRC, m = m0 + rr;
-      sB[j * SRC + rr] = m < M ? Bm[(size_t)j * R + g.mon_row[m]] : 0.0;
-    }
-    __syncthreads();
-    if (c >= 0) {
-      const int rend = min(SRC, M - m0);
-      for (int rr = 0; rr < rend; ++rr) {
-        const int row = sRow[rr];
-        if (row < 0) continue;  // disconnected: flow exactly 0, neither metric nor report
-        double f;
-        if (row == rowc) {
-          f = sN0[rr] + (-1.0) * sc;
-        } else {
-          double dv = __ldg(&Dc[row]);
-          for (int j = 0; j < rt; ++j) dv = fma(sB[j * SRC + rr], sW[j * RCW + tid], dv);
-          f = sN0[rr] + (dv * idn) * sc;
+      for (int j = 0; j < rt; ++j) {
+        const double wj = sWc[wid][j];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = p0 + 32 * u;
+          if (p < M) dv[u] = fma(Bmon[(size_t)j * M + p], wj, dv[u]);
         }
-        const double rel = fabs(f) * sInv[rr];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + 32 * u;
+        if (p >= M || is_dead(sdeadp, nd, p)) continue;  // disconnected: flow exactly 0
+        const double f = (p == ownp) ? nv[u] + (-1.0) * sc : nv[u] + (dv[u] * idn) * sc;
+        const double rel = fabs(f) * iv[u];
         mymax = fmax(mymax, rel);
-        if (row != rowc) lt.insert(rel, m0 + rr, f);
+        if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
       }
     }
-    __syncthreads();
+    warp_merge<KC>(lt, kc, wl[wid], kg, order);
+    __syncwarp();
   }
-  // CTA max and the partial top-kg: kg rounds of block argmax over the thread heads
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
-  if (lane == 0) wr[wid] = mymax;
+  if (lane == 0) wmax[wid] = mymax;
   __syncthreads();
+  if (wid != 0) return;
+  // warp 0: the CTA's partial top-kg, kg rounds of argmax over the RW sorted warp lists
   const int slot = RSEL_WARPS + tile;
   const size_t o = ((size_t)b * w.nslot + slot) * KMAX;
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int i = 0; i < RCW / 32; ++i) mx = fmax(mx, wr[i]);
-    w.pmax[(size_t)b * w.nslot + slot] = mx;
-  }
-  __syncthreads();
+  double mx = lane < RW ? wmax[lane] : 0.0;
+  for (int k = 16; k; k >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, k));
+  if (lane == 0) w.pmax[(size_t)b * w.nslot + slot] = mx;
+  int hd = 0;  // lane l < RW: next entry of warp list l
   for (int e = 0; e < kg; ++e) {
-    double r = c >= 0 ? lt.rel[0] : -1.0;
-    int ord = c >= 0 && r >= 0.0 ? order : INT_MAX, p = lt.pos[0], src = tid;
-    for (int off = 16; off; off >>= 1) {
-      const double orr = __shfl_xor_sync(0xffffffffu, r, off);
-      const int oo = __shfl_xor_sync(0xffffffffu, ord, off);
-      const int op = __shfl_xor_sync(0xffffffffu, p, off);
-      const int os = __shfl_xor_sync(0xffffffffu, src, off);
-      if (better3(orr, oo, op, r, ord, p)) { r = orr; ord = oo; p = op; src = os; }
+    double r = -1.0;
+    int ord = INT_MAX, p = INT_MAX, src = lane;
+    if (lane < RW && hd < wl[lane].n) { r = wl[lane].rel[hd]; ord = wl[lane].cs[hd]; p = wl[lane].pos[hd]; }
+    for (int k = 16; k; k >>= 1) {
+      const double orr = __shfl_xor_sync(0xffffffffu, r, k);
+      const int oo = __shfl_xor_sync(0xffffffffu, ord, k);
+      const int op = __shfl_xor_sync(0xffffffffu, p, k);
+      const int os = __shfl_xor_sync(0xffffffffu, src, k);
+      if (better3(orr, oo, op, r, ord, p) || (orr == r && oo == ord && op == p && os < src)) {
+        r = orr; ord = oo; p = op; src = os;
+      }
     }
-    if (lane == 0) { wr[wid] = r; wo[wid] = ord; wp[wid] = p; wsrc[wid] = src; }
-    __syncthreads();
-    if (tid == 0) {
-      int k = 0;
-      for (int i = 1; i < RCW / 32; ++i)
-        if (better3(wr[i], wo[i], wp[i], wr[k], wo[k], wp[k])) k = i;
-      pick_src = wr[k] >= 0.0 ? wsrc[k] : -1;
-      w.prel[o + e] = wr[k] >= 0.0 ? wr[k] : -1.0;
-      w.pcase[o + e] = wr[k] >= 0.0 ? wo[k] : INT_MAX;
-      w.ppos[o + e] = wr[k] >= 0.0 ? wp[k] : INT_MAX;
+    if (lane == src && r >= 0.0) {
+      w.prel[o + e] = r; w.pcase[o + e] = ord; w.ppos[o + e] = p; w.pflow[o + e] = wl[lane].flow[hd];
+      ++hd;
     }
-    __syncthreads();
-    const int ps = pick_src;
-    if (ps < 0) {
-      for (int e2 = e + 1 + tid; e2 < kg; e2 += RCW) {
+    if (r < 0.0) {
+      for (int e2 = e + lane; e2 < kg; e2 += 32) {
         w.prel[o + e2] = -1.0; w.pcase[o + e2] = INT_MAX; w.ppos[o + e2] = INT_MAX;
       }
       break;
     }
-    if (tid == ps) {
-      w.pflow[o + e] = lt.flow[0];
-      lt.pop();
-    }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -669,16 +652,7 @@ namespace {
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
-  if (g.N1 > 0 && g.M > 0) {
-    const size_t dyn = ((size_t)w.rs * RCW + (size_t)w.rs * SRC) * sizeof(double);
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_rsweep<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(((size_t)RMAX * RCW + (size_t)RMAX * SRC) * sizeof(double)));
-      init = true;
-    }
-    k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RCW, dyn, s>>>(g, c, w);
-  }
+  if (g.N1 > 0 && g.M > 0) k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RT, 0, s>>>(g, c, w);
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
 }

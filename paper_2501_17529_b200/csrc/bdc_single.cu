@@ -14,9 +14,9 @@
 //            good lower bound lb(t) of every candidate's metric, as the reference's
 //            visit order (descending bound) does;
 //   k_live   every other pair is bounded by |F| <= max_b (m0_b(t) + scale_bc |s(c,t)|);
-//            a pair whose bound cannot exceed lb(t) cannot change the metric and is
-//            skipped; the others get a bit in the live map and their case is queued;
-//   k_pairs  the queued cases, exactly, for their live candidates only.
+//            a pair whose bound cannot exceed lb(t) cannot change the metric; a case
+//            with any pair above its bound is live and queued in groups of TOPC;
+//   k_pairs  the live groups, as TOP tiles (every candidate of a live case).
 // Every evaluated pair uses the same FP32 expression fabsf(fmaf(L', s, n0')) in every
 // kernel, so a metric never depends on which kernel evaluated the binding pair.
 #include "bdc_device.cuh"
@@ -28,12 +28,11 @@ namespace bdc {
 // screen is off / N1 <= TOPC) x TT = TPT*TY candidates per CTA, thread (tx, ty) owns
 // CPT cases x TPT candidates.  Monitored rows stream through shared memory in chunks of
 // RC (cp.async double buffer of D_base columns, B'' rows and n0/rating).
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
-__global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Work w) {
+// One tile: task b, cases list[0..nlist) (entries < 0 are empty; list == nullptr means
+// cases 0..nlist-1), candidates t0..t0+TT.  Ends with the block synchronised.
+template <int CPT, int TPT, int TX, int TY, int RC>
+__device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b, const int* list, int nlist, int t0) {
   constexpr int NTH = TX * TY, NC = CPT * TX, TT = TPT * TY;
-  const int b = blockIdx.z;
-  if (w.status[b] != 0) return;
-  const int t0 = blockIdx.y * TT;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   const int rs = w.rs, rt = w.rank[b], T = w.T, M = g.M, N1 = g.N1, R = g.R;
   // dynamic: [sW rs*NC f64][sBb 2*rs*RC f64][sN 2*RC*TT f32][sD 2*RC*NC f32]
@@ -60,8 +59,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Wor
 
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   for (int cc = tid; cc < NC; cc += NTH) {
-    const int c = w.ranked ? (cc < w.ptop ? w.top[(size_t)b * w.ptop + cc] : -1)
-                           : (cc < min(w.ptop, N1) ? cc : -1);
+    const int c = cc < nlist ? (list ? list[cc] : cc) : -1;
     sCase[cc] = c;
     const bool ok = c >= 0 && w.sc_ok[(size_t)b * N1 + c];
     sInvDen[cc] = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
@@ -250,8 +248,30 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Wor
     const int t = t0 + ty * TPT + jj;
     if ((tx % GW) == 0 && t < T) atomic_max_pos(&w.m32[(size_t)b * T + t], v);
   }
+  __syncthreads();  // the caller may reuse the shared buffers for the next tile
 #undef SN
 #undef SD
+}
+
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+__global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Work w) {
+  const int b = blockIdx.z;
+  if (w.status[b] != 0) return;
+  const int* list = w.ranked ? w.top + (size_t)b * w.ptop : nullptr;
+  const int nlist = w.ranked ? w.ptop : min(w.ptop, g.N1);
+  top_tile<CPT, TPT, TX, TY, RC>(g, w, b, list, nlist, blockIdx.y * (TPT * TY));
+}
+
+// Live cases, TOPC per item, every candidate tile: persistent over the queue.
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+__global__ void __launch_bounds__(TX* TY, MINB) k_pairs(DevGrid g, DevCfg cfg, Work w) {
+  const unsigned nq = *w.qcount;
+  for (unsigned it = blockIdx.x; it < nq; it += gridDim.x) {
+    const int2 q = w.queue[it];
+    const int b = q.x, grp = q.y >> 16, tt = q.y & 0xffff;
+    const int n = min(TOPC, w.lcnt[b] - grp * TOPC);
+    top_tile<CPT, TPT, TX, TY, RC>(g, w, b, w.llist + (size_t)b * g.N1 + grp * TOPC, n, tt * (TPT * TY));
+  }
 }
 
 // ---------------------------------------------------------------------------- k_scale
@@ -434,18 +454,19 @@ __global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
 // iff max_b (m0_b(t) + scale_bc |s(c,t)|) > lb(t) = max(running metric, penalty floor)
 // (every TOP case, multi/injection case and the N-0 flows are already in m32).  A
 // skipped pair is provably dominated: it cannot change the metric (solver.py:809-812).
-// With the screen off every pair of a feasible case is live.  Writes the live map
-// (read by the winner report) and queues cases with live candidates for k_pairs.
-// CTA = (task, LC cases), warp per case, lanes over candidates; the block bounds and
-// lb of the task are staged once per CTA.
+// A case with any live candidate is evaluated for all of them (k_pairs): done[c] = 2 and
+// listed in llist (k_queue then queues the lists in groups of TOPC x candidate tiles).
+// With the screen off every feasible case is live.  CTA = (task, LC cases), a warp per
+// 32 cases: lanes load the cases' flags and block scales (coalesced), then the warp walks
+// its cases with lanes over candidates; lb and the block N-0 maxima are staged per CTA.
 namespace {
-constexpr int LC = 64;         // cases per k_live CTA
+constexpr int LC = 128;        // cases per k_live CTA (4 warps x 32)
 constexpr int LV_TMAX = 1024;  // candidates staged in shared memory (larger T: global reads)
 }
-__global__ void __launch_bounds__(256) k_live(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (w.status[b] != 0) return;
-  const int T = w.T, N1 = g.N1, TW = w.TW;
+  const int T = w.T, N1 = g.N1;
   __shared__ float sLb[LV_TMAX];
   __shared__ float sM0[SB][LV_TMAX];
   const bool staged = T <= LV_TMAX;
@@ -453,118 +474,75 @@ __global__ void __launch_bounds__(256) k_live(DevGrid g, DevCfg cfg, Work w) {
   const float* m32 = reinterpret_cast<const float*>(w.m32) + (size_t)b * T;
   const float* m0b = w.m0b + (size_t)b * SB * T;
   if (staged && w.screen) {
-    for (int t = tid; t < T; t += 256) {
+    for (int t = tid; t < T; t += LC) {
       sLb[t] = fmaxf(m32[t], pen);
 #pragma unroll
       for (int blk = 0; blk < SB; ++blk) sM0[blk][t] = m0b[(size_t)blk * T + t];
     }
   }
   __syncthreads();
-  for (int c = blockIdx.x * LC + wid; c < min(N1, (blockIdx.x + 1) * LC); c += 8) {
-    uint32_t* lw = w.live + ((size_t)b * N1 + c) * TW;
-    const bool done = w.ranked ? w.done[(size_t)b * N1 + c] != 0 : c < w.ptop;
-    const bool ok = w.sc_ok[(size_t)b * N1 + c] != 0;
-    if (done || !ok) {
-      for (int tw = lane; tw < TW; tw += 32) lw[tw] = 0u;
-      continue;
-    }
-    float scl[SB];
+  uint8_t* done = w.done + (size_t)b * N1;
+  const int cl = blockIdx.x * LC + wid * 32 + lane;  // this lane's case
+  bool cand = false;
+  float scl[SB];
 #pragma unroll
-    for (int blk = 0; blk < SB; ++blk) scl[blk] = w.screen ? w.scale[((size_t)b * SB + blk) * N1 + c] : 0.f;
+  for (int blk = 0; blk < SB; ++blk) scl[blk] = 0.f;
+  if (cl < N1) {
+    const bool top = w.ranked ? done[cl] != 0 : cl < w.ptop;
+    cand = !top && w.sc_ok[(size_t)b * N1 + cl] != 0;
+    if (cand && w.screen)
+#pragma unroll
+      for (int blk = 0; blk < SB; ++blk) scl[blk] = w.scale[((size_t)b * SB + blk) * N1 + cl];
+  }
+  bool mylive = cand && !w.screen;
+  unsigned todo = __ballot_sync(0xffffffffu, cand && w.screen);
+  while (todo) {
+    const int k = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int c = blockIdx.x * LC + wid * 32 + k;
+    float sk[SB];
+#pragma unroll
+    for (int blk = 0; blk < SB; ++blk) sk[blk] = __shfl_sync(0xffffffffu, scl[blk], k);
     const float* sc = w.s32 + ((size_t)b * N1 + c) * T;
-    int nlive = 0;
-    for (int tw = 0; tw < TW; ++tw) {
-      const int t = tw * 32 + lane;
-      bool live = t < T;
-      if (live && w.screen) {
+    bool live = false;
+    for (int t0 = 0; t0 < T && !live; t0 += 32) {
+      const int t = t0 + lane;
+      bool lt = false;
+      if (t < T) {
         const float as = fabsf(sc[t]);
         float bound = 0.f;
 #pragma unroll
         for (int blk = 0; blk < SB; ++blk)
-          bound = fmaxf(bound, (staged ? sM0[blk][t] : m0b[(size_t)blk * T + t]) + scl[blk] * as);
-        live = bound > (staged ? sLb[t] : fmaxf(m32[t], pen));
+          bound = fmaxf(bound, (staged ? sM0[blk][t] : m0b[(size_t)blk * T + t]) + sk[blk] * as);
+        lt = bound > (staged ? sLb[t] : fmaxf(m32[t], pen));
       }
-      const uint32_t word = __ballot_sync(0xffffffffu, live);
-      if (lane == 0) lw[tw] = word;
-      nlive += __popc(word);
+      live = __any_sync(0xffffffffu, lt);
     }
-    if (lane == 0 && nlive) {
-      const unsigned q = atomicAdd(w.qcount, 1u);
-      w.queue[q] = make_int2(b, c);
-      atomicAdd(w.pairs, (unsigned long long)nlive);
-    }
+    if (lane == k) mylive = live;
+  }
+  if (cl < N1 && (cand || !w.ranked)) {
+    // TOP cases keep done = 1 (k_topk); unranked tasks have no k_topk pass
+    if (!(w.ranked ? false : cl < w.ptop)) done[cl] = mylive ? 2 : 0;
+  }
+  const unsigned lb = __ballot_sync(0xffffffffu, mylive);
+  if (lb) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&w.lcnt[b], __popc(lb));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (mylive) w.llist[(size_t)b * N1 + base + __popc(lb & ((1u << lane) - 1u))] = cl;
   }
 }
 
-// --------------------------------------------------------------------------- k_pairs
-// The queued (task, case) items: a warp per item, lanes over the 32 candidates of a
-// live word, monitored rows in chunks of PR: each lane forms PR/32 LODF entries in FP64
-// (the same expression and rounding as k_top) into the warp's shared slice, then every
-// lane streams the chunk for its candidate (n0/rating reads coalesced across lanes).
-// Persistent grid; the item count is read on the device.
-namespace {
-constexpr int PR = 128;  // rows per chunk
-constexpr int PW = 8;    // warps per CTA
-}
-__global__ void __launch_bounds__(PW * 32) k_pairs(DevGrid g, Work w) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __shared__ float sL[PW][PR];
-  __shared__ double sWc[PW][RMAX];
-  const unsigned nq = *w.qcount;
-  const int M = g.M, N1 = g.N1, R = g.R, T = w.T, TW = w.TW, rs = w.rs;
-  for (unsigned it = blockIdx.x * PW + wid; it < nq; it += gridDim.x * PW) {
-    const int2 bc = w.queue[it];
-    const int b = bc.x, c = bc.y;
-    const int rt = w.rank[b], nd = w.ndead[b];
-    const int* dead = w.dead + (size_t)b * RMAX;
-    const double* Bm = w.Bm + (size_t)b * rs * R;
-    const float* n0s = w.n0s + (size_t)b * M * T;
-    const double idn = 1.0 / w.den[(size_t)b * N1 + c];  // queued cases are feasible
-    const int rowc = g.sc_row[c];
-    for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
-    __syncwarp();
-    const uint32_t* lw = w.live + ((size_t)b * N1 + c) * TW;
-    float* cm = w.cmax + (size_t)b * (N1 + g.NM + g.NI) * T + (size_t)c * T;
-    for (int tw = 0; tw < TW; ++tw) {
-      const uint32_t word = lw[tw];
-      if (word == 0u) continue;
-      const int t = tw * 32 + lane;
-      const bool mine = (word >> lane) & 1u;
-      const float s = mine ? w.s32[((size_t)b * N1 + c) * T + t] : 0.f;
-      float acc = 0.f;
-      for (int m0 = 0; m0 < M; m0 += PR) {
-#pragma unroll
-        for (int q = 0; q < PR / 32; ++q) {
-          const int m = m0 + lane + 32 * q;
-          float lv = 0.f;
-          if (m < M) {
-            const int row = g.mon_row[m];
-            if (!is_dead(dead, nd, row)) {
-              const double inv = g.inv_rating[m];
-              if (row == rowc) {
-                lv = (float)(-inv);
-              } else {
-                double v = (double)g.D32[(size_t)m * g.N1p + c];
-                for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], sWc[wid][j], v);
-                lv = (float)(v * (idn * inv));
-              }
-            }
-          }
-          sL[wid][lane + 32 * q] = lv;
-        }
-        __syncwarp();
-        const int rend = min(PR, M - m0);
-        if (mine)
-          for (int rr = 0; rr < rend; ++rr)
-            acc = fmaxf(acc, fabsf(fmaf(sL[wid][rr], s, n0s[(size_t)(m0 + rr) * T + t])));
-        __syncwarp();
-      }
-      if (mine) {
-        cm[t] = acc;
-        atomic_max_pos(&w.m32[(size_t)b * T + t], acc);
-      }
-    }
-  }
+// Queue the live lists: per task, groups of TOPC cases x candidate tiles (k_pairs counts
+// the evaluated pairs as it goes).
+__global__ void k_queue(DevGrid g, Work w) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= w.Wb || w.status[b] != 0) return;
+  const int n = w.lcnt[b];
+  if (n == 0) return;
+  const int TT = top_tile_cands(w.T), ntt = (w.T + TT - 1) / TT, ng = (n + TOPC - 1) / TOPC;
+  const unsigned q0 = atomicAdd(w.qcount, (unsigned)(ng * ntt));
+  for (int i = 0; i < ng * ntt; ++i) w.queue[q0 + i] = make_int2(b, ((i / ntt) << 16) | (i % ntt));
 }
 
 namespace {
@@ -606,10 +584,37 @@ void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t
   k_top<CPT, TPT, TX, TY, RC, MINB><<<grid, TX * TY, dyn, s>>>(g, c, w);
 }
 
+template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+void launch_pairs_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  constexpr int NC = CPT * TX, TT = TPT * TY;
+  const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
+                     (2 * (size_t)RC * TT + 2 * (size_t)RC * NC) * sizeof(float);
+  static int max_dyn = -1, per_sm = 1, nsm = 148;
+  if (max_dyn < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_pairs<CPT, TPT, TX, TY, RC, MINB>);
+    max_dyn = optin - (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(k_pairs<CPT, TPT, TX, TY, RC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+  }
+  // persistent: as many CTAs as fit at once for this rank stride's shared memory
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pairs<CPT, TPT, TX, TY, RC, MINB>, TX * TY, dyn);
+  k_pairs<CPT, TPT, TX, TY, RC, MINB><<<nsm * (per_sm > 0 ? per_sm : 1), TX * TY, dyn, s>>>(g, c, w);
+}
+
+// tile shapes: 16 cases x top_tile_cands(T) candidates (bdc_device.cuh)
 void launch_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   if (w.T >= 96) launch_top_t<1, 8, 16, 16, 64, 2>(g, c, w, s);       // 16 cases x 128 candidates
   else if (w.T >= 48) launch_top_t<1, 4, 16, 16, 64, 2>(g, c, w, s);  // 16 x 64
   else launch_top_t<1, 2, 16, 16, 64, 2>(g, c, w, s);                 // 16 x 32
+}
+void launch_pairs(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  if (w.T >= 96) launch_pairs_t<1, 8, 16, 16, 64, 2>(g, c, w, s);
+  else if (w.T >= 48) launch_pairs_t<1, 4, 16, 16, 64, 2>(g, c, w, s);
+  else launch_pairs_t<1, 2, 16, 16, 64, 2>(g, c, w, s);
 }
 }  // namespace
 
@@ -622,17 +627,15 @@ void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   }
   launch_top(g, c, w, s);
   if (g.N1 > w.ptop) {
-    k_live<<<dim3((g.N1 + LC - 1) / LC, w.Wb), 256, 0, s>>>(g, c, w);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    k_pairs<<<nsm * 4, PW * 32, 0, s>>>(g, w);
+    k_live<<<dim3((g.N1 + LC - 1) / LC, w.Wb), LC, 0, s>>>(g, c, w);
+    k_queue<<<(w.Wb + 255) / 256, 256, 0, s>>>(g, w);
+    launch_pairs(g, c, w, s);
   }
 }
 
 int single_launches(const DevGrid& g, const Work& w) {
   if (g.N1 == 0 || g.M == 0) return 0;
-  return (w.ranked ? 2 : 0) + 1 + (g.N1 > w.ptop ? 2 : 0);
+  return (w.ranked ? 2 : 0) + 1 + (g.N1 > w.ptop ? 3 : 0);
 }
 
 }  // namespace bdc
