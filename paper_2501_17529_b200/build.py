@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["bdc_update.cu", "bdc_single.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_capi.cu"]
+SOURCES = ["bdc_update.cu", "bdc_single.cu", "bdc_scale.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_capi.cu"]
 TARGET = os.path.join(HERE, "libbdc.so")
 FLAGS = [
     "-std=c++17",

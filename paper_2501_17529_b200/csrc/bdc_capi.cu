@@ -216,6 +216,16 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   UP(mc_order, G->NM);
   UP(mb_row, G->NMB);
   UP(Dm64, (size_t)G->NMB * G->R);
+  // D_base / rating on monitored rows, case-major, FP32, rows padded to a multiple of 4
+  // (16-byte cp.async of the tensor-core screening kernel)
+  g.Mp = (G->M + 3) & ~3;
+  if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
+    std::vector<float> ds((size_t)G->N1 * g.Mp, 0.f);
+    for (int c = 0; c < G->N1; ++c)
+      for (int p = 0; p < G->M; ++p)
+        ds[(size_t)c * g.Mp + p] = (float)(G->D64[(size_t)c * G->R + G->mon_row[p]] * (1.0 / G->rating[p]));
+    e = upload(ds.data(), ds.size(), &g.DsT, o);
+  }
   // D_base on monitored rows, case-major, for the winner report's coalesced sweeps
   if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
     std::vector<double> dm((size_t)G->N1 * G->M);

@@ -30,11 +30,11 @@ constexpr int TOPC = 16;
 constexpr int SB = 4;
 // Candidates per TOP-tile CTA (bdc_single.cu launch_top).
 __host__ __device__ inline int top_tile_cands(int T) { return T >= 96 ? 128 : (T >= 48 ? 64 : 32); }
-// Rows per screening block: a multiple of 16 (the k_scale row chunk, also a multiple of
-// the k_n0 row group), so a chunk never straddles two blocks; block of position m = m / MB.
+// Rows per screening block: a multiple of 32 (the k_scale epilogue's row half, also a
+// multiple of the k_n0 row group), so neither straddles two blocks; block of m = m / MB.
 __host__ __device__ inline int screen_block_rows(int M) {
   const int per = (M + SB - 1) / SB;
-  return ((per + 15) / 16) * 16 > 0 ? ((per + 15) / 16) * 16 : 16;
+  return ((per + 31) / 32) * 32 > 0 ? ((per + 31) / 32) * 32 : 32;
 }
 constexpr int RCW = 64;         // single cases per CTA of the winner report sweep (8 per warp)
 constexpr int RSEL_WARPS = 8;   // partial report lists written by the report-select kernel
@@ -47,6 +47,8 @@ struct DevGrid {
   const double *P0, *P0T, *f0, *p_base, *rating, *inv_rating, *sub_elem_b, *slot_sp;
   const double *sc_delta, *sc_dscale, *D64, *Dm64, *ic_sp;
   const double* DM64;  // (N1, M) D_base on monitored rows, case-major (winner report)
+  const float* DsT;    // (N1, Mp) D_base / rating on monitored rows, case-major, FP32 (k_scale)
+  int Mp;              // M rounded up to a multiple of 4
   const float* D32;
   const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;
   const int *sub_elem_row, *slot_sub, *slot_col, *sc_row, *sc_order, *mc_start, *mc_order;
@@ -98,7 +100,7 @@ struct Work {
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
   float* scale;   // (Wb, SB, N1)  FP32 upper bound of max_{r in block} |LODF(r,c)|/rating_r
-  float* B32;     // (Wb, rs, M)   FP32 B'' on monitored rows (screening bound only)
+  float* B32;     // (Wb, rs, M)   FP32 B''/rating on monitored rows, 0 on dead rows (k_scale)
   float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
   int screen;     // 1 = exact dominance screen on
@@ -267,6 +269,7 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);

@@ -1,0 +1,370 @@
+// bdc_scale.cu -- the screening scales of the single-branch N-1 stage on the tcgen05
+// tensor cores.
+//
+// For every task, single case c and screening row block b (bdc_device.cuh) the
+// dominance screen needs an upper bound of
+//     max_{r in b} |L'(r,c)|,   L'(r,c) = L(r,c) / rating_r = (D'(r,c) + sum_j B'(r,j) W(c,j)) / den_c
+// with D' = D_base / rating (a session table, case-major) and B' = B'' / rating (dead
+// rows zeroed, written per task by k_n0).  The rank-r product sum_j B'(r,j) W(c,j) is a
+// (cases x K) . (K x rows) GEMM per task, K = rank padded to 8: it runs as
+// tcgen05.mma.kind::tf32 (M = 128 cases, N = 64 rows, K = 8 per instruction) into a
+// TMEM accumulator, and the epilogue reads it back with tcgen05.ld (thread = case,
+// columns = rows), adds D' from shared memory and folds max |.| per case and row block
+// with FMNMX3 -- the reduction over rows never leaves the thread.
+//
+// Rigour: operands are rounded to TF32 (cvt.rna, relative error <= 2^-11 each), so the
+// product terms carry <= 2^-10 relative error, accumulated and added in FP32.  The bound
+//     |L~ - L| <= 2^-9 sum_j |W_cj| max_r |B'(r,j)| + (rt + 8) 2^-23 (max_r |D'(r,c)| + sum_j ...)
+// is added before scaling by 1/|den_c| (the FP32 CUDA-core version needed only the
+// second term).  The own row contributes 1/rating (L' = -1/rating there), dead rows
+// nothing; both are masked out of the accumulated maxima.
+//
+// CTA = 128 cases x TB tasks (the D' tile staged once per row chunk serves all TB
+// tasks); one elected thread issues the MMAs and commits them to an mbarrier.
+#include "bdc_device.cuh"
+
+#include <algorithm>
+
+namespace bdc {
+
+namespace {
+
+constexpr int SM_CASES = 128;  // UMMA M
+constexpr int SM_ROWS = 64;    // UMMA N: monitored rows per chunk
+constexpr int SD_LD = SM_ROWS + 4;  // padded row length of the staged D' tile (floats)
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// K-major, no-swizzle canonical layout: 8-row x 16-byte core matrices; the two 16-byte
+// K halves of a row group at +128 B (LBO), consecutive row groups at +256 B (SBO).
+__device__ __forceinline__ int core_off(int row, int k) {  // byte offset of element (row, k), k < 8
+  return (row >> 3) * 256 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4;
+}
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  const uint32_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)((128 >> 4) & 0x3FFF) << 16;  // leading byte offset (K direction)
+  d |= (uint64_t)((256 >> 4) & 0x3FFF) << 32;  // stride byte offset (M/N direction)
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
+  return d;                                    // base offset 0, SWIZZLE_NONE
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = SM_ROWS
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(SM_ROWS >> 3) << 17) |
+                            ((uint32_t)(SM_CASES >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc ? 1 : 0));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace
+
+// TB tasks per CTA, KB = K blocks of 8 rank terms (rank stride rs <= 8 KB).  256 threads:
+// warp w reads TMEM lanes 32 (w % 4) .. +31 (the CTA's cases), warpgroup w / 4 takes one
+// 32-row half of every 64-row chunk.  The D' tile and the B operands of chunk ch + 1 are
+// in flight (cp.async, double buffer) while chunk ch is multiplied and reduced.
+template <int TB, int KB>
+__global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w) {
+  constexpr int NT = 2 * SM_CASES;
+  constexpr int TCOLS = TB * SM_ROWS;  // TMEM columns: one accumulator per task
+  constexpr int NCOLS = TCOLS <= 32 ? 32 : (TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : 256));
+  constexpr int ABYTES = SM_CASES * 32, BBYTES = SM_ROWS * 32;  // one K block of A / B
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, wg = wid >> 2;
+  const int ci = (wid & 3) * 32 + lane;  // this thread's case within the tile (= TMEM lane)
+  const int c0 = blockIdx.x * SM_CASES, c = c0 + ci;
+  const int tb0 = blockIdx.y * TB;
+  const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
+  const int MB = screen_block_rows(M);
+  extern __shared__ __align__(1024) unsigned char ssm[];
+  unsigned char* sA = ssm;                            // [TB][KB] A tiles
+  unsigned char* sBt = sA + TB * KB * ABYTES;         // [2][TB][KB] B tiles
+  float* sD = reinterpret_cast<float*>(sBt + 2 * TB * KB * BBYTES);  // [2][128 cases][SD_LD]
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  __shared__ int sdead[TB][RMAX];
+  __shared__ int snd[TB], srt[TB];
+  __shared__ float sm0[TB][SB];
+
+  if (wid == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "n"(NCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  if (tid < TB) {
+    const int b = tb0 + tid;
+    const bool on = b < w.Wb && w.status[b] == 0;
+    snd[tid] = on ? w.ndead[b] : 0;
+    srt[tid] = on ? w.rank[b] : -1;  // -1: slot idle
+  }
+  __syncthreads();
+  for (int i = tid; i < TB * RMAX; i += NT) {
+    const int k = i / RMAX, d = i % RMAX;
+    if (d < snd[k]) sdead[k][d] = g.row_mon_pos[w.dead[(size_t)(tb0 + k) * RMAX + d]];  // -1: unmonitored
+  }
+  // max_t m0_b(t) of each task and block (ranking key)
+  for (int kb = wid; kb < TB * SB; kb += NT / 32) {
+    const int k = kb / SB, blk = kb % SB;
+    float v = 0.f;
+    if (srt[k] >= 0)
+      for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0b[((size_t)(tb0 + k) * SB + blk) * T + t]);
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sm0[k][blk] = v;
+  }
+  // A operands (warpgroup 0): W(c, j) of every task, TF32 (cvt.rna), zero past the rank
+  if (wg == 0) {
+#pragma unroll
+    for (int k = 0; k < TB; ++k) {
+      const int b = tb0 + k, rt = srt[k];
+      const bool ok = c < N1 && rt >= 0 && w.sc_ok[(size_t)b * N1 + c];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = kb * 8 + jj;
+          const float wv = (ok && j < rt) ? (float)w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.f;
+          *reinterpret_cast<uint32_t*>(sA + (k * KB + kb) * ABYTES + core_off(ci, jj)) = to_tf32(wv);
+        }
+    }
+  }
+  // own rows: the computed own-row value is |1 - den_c| / rating (D''(r_c, c) = 1 - den_c);
+  // its true |L'| = 1/rating enters the bound at the end.  Scaled by 1/|den_c| the computed
+  // value only loosens the bound when |1 - den_c| > |den_c|: masked out in that case only.
+  const int ownp = c < N1 ? g.row_mon_pos[g.sc_row[c]] : -1;
+  bool ownloose = false;
+#pragma unroll
+  for (int k = 0; k < TB; ++k)
+    if (c < N1 && srt[k] >= 0 && w.sc_ok[(size_t)(tb0 + k) * N1 + c]) {
+      const double den = w.den[(size_t)(tb0 + k) * N1 + c];
+      ownloose |= fabs(1.0 - den) > 0.999 * fabs(den);
+    }
+
+  // stage chunk ch into buffer bf: D' tile (cp16) and B operands (cp4 into the core-matrix
+  // layout; fp32 bits, which the tf32 MMA truncates: <= 2^-10 relative)
+  auto issue = [&](int ch, int bf) {
+    const int m0 = ch * SM_ROWS;
+    float* D = sD + bf * SM_CASES * SD_LD;
+    for (int idx = tid; idx < SM_CASES * (SM_ROWS / 4); idx += NT) {
+      const int i = idx / (SM_ROWS / 4), q = 4 * (idx % (SM_ROWS / 4));
+      const bool ok = c0 + i < N1 && m0 + q < g.Mp;
+      cp16(&D[i * SD_LD + q], ok ? &g.DsT[(size_t)(c0 + i) * g.Mp + m0 + q] : g.DsT, ok);
+    }
+    unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
+    for (int idx = tid; idx < TB * KB * 8 * SM_ROWS; idx += NT) {
+      const int r = idx % SM_ROWS, jj = (idx / SM_ROWS) % 8, kb = (idx / (SM_ROWS * 8)) % KB, k = idx / (SM_ROWS * 8 * KB);
+      const int j = kb * 8 + jj, m = m0 + r;
+      const bool ok = srt[k] >= 0 && j < srt[k] && m < M;
+      cp4(Bt + (k * KB + kb) * BBYTES + core_off(r, jj), ok ? &w.B32[((size_t)(tb0 + k) * rs + j) * M + m] : w.B32, ok);
+    }
+    cp_commit();
+  };
+
+  const int nchunks = (M + SM_ROWS - 1) / SM_ROWS;
+  float mx[TB], mxb[TB][SB];  // running max of the current block; finished blocks
+#pragma unroll
+  for (int k = 0; k < TB; ++k) {
+    mx[k] = 0.f;
+#pragma unroll
+    for (int bb = 0; bb < SB; ++bb) mxb[k][bb] = 0.f;
+  }
+  int curblk = -1;
+  auto flush = [&]() {
+#pragma unroll
+    for (int k = 0; k < TB; ++k) {
+#pragma unroll
+      for (int bb = 0; bb < SB; ++bb)
+        if (bb == curblk) mxb[k][bb] = fmaxf(mxb[k][bb], mx[k]);
+      mx[k] = 0.f;
+    }
+  };
+  issue(0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tbase = tmem_base;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int bf = ch & 1;
+    if (ch + 1 < nchunks) {
+      issue(ch + 1, bf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (tid == 0) {
+      const unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
+#pragma unroll
+      for (int k = 0; k < TB; ++k)
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb)
+          mma_tf32(tbase + k * SM_ROWS, smem_desc(sA + (k * KB + kb) * ABYTES),
+                   smem_desc(Bt + (k * KB + kb) * BBYTES), kb > 0);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&mbar))
+                   : "memory");
+    }
+    mbar_wait(&mbar, ch & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // epilogue: this warpgroup's 32-row half (a screening block holds whole halves)
+    const int r0 = ch * SM_ROWS + wg * 32;
+    if (r0 < M) {
+      const int blk = r0 / MB;
+      if (blk != curblk) {
+        flush();
+        curblk = blk;
+      }
+      const float* D = sD + bf * SM_CASES * SD_LD + ci * SD_LD + wg * 32;
+      float dv[32];
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(&D[q]);
+        dv[q] = v4.x; dv[q + 1] = v4.y; dv[q + 2] = v4.z; dv[q + 3] = v4.w;
+      }
+      const int ownq = ownp - r0;
+      const bool ownin = ownloose && ownq >= 0 && ownq < 32;
+      const bool anyown = __any_sync(0xffffffffu, ownin);
+#pragma unroll
+      for (int k = 0; k < TB; ++k) {
+        float acc[32];
+        tmem_ld32(tbase + ((uint32_t)((wid & 3) * 32) << 16) + k * SM_ROWS + wg * 32, acc);
+        if (srt[k] < 0) continue;
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) {
+          const float2 a2 = __fadd2_rn(make_float2(acc[q], acc[q + 1]), make_float2(dv[q], dv[q + 1]));
+          acc[q] = a2.x; acc[q + 1] = a2.y;
+        }
+        // dead rows of the task -> excluded (their flow is exactly 0)
+        for (int d = 0; d < snd[k]; ++d) {
+          const int dq = sdead[k][d] - r0;
+          if (dq >= 0 && dq < 32) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) acc[q] = (q == dq) ? 0.f : acc[q];
+          }
+        }
+        if (anyown) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) acc[q] = (ownin && q == ownq) ? 0.f : acc[q];
+        }
+        float m = mx[k];
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) m = max3abs(m, acc[q], acc[q + 1]);
+        mx[k] = m;
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();  // TMEM and this chunk's buffers are free again
+  }
+  flush();
+  __syncthreads();
+  if (wid == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(NCOLS));
+  // warpgroup 1 hands its block maxima over through the (now free) D' buffer
+  float* sMx = sD;  // [SB][TB][128]
+  if (wg == 1)
+#pragma unroll
+    for (int k = 0; k < TB; ++k)
+#pragma unroll
+      for (int bb = 0; bb < SB; ++bb) sMx[(bb * TB + k) * SM_CASES + ci] = mxb[k][bb];
+  __syncthreads();
+  if (wg != 0 || c >= N1) return;
+  // warpgroup 0: combine the two halves' block maxima, scale, bound, ranking key
+#pragma unroll
+  for (int k = 0; k < TB; ++k) {
+    const int b = tb0 + k, rt = srt[k];
+    if (rt < 0) continue;
+    const bool ok = w.sc_ok[(size_t)b * N1 + c] != 0;
+    float aid = 0.f, rnd = 0.f;
+    if (ok) {
+      float wsum = 0.f;
+      for (int j = 0; j < rt; ++j)
+        wsum += (float)fabs(w.Wsc[((size_t)b * N1 + c) * rs + j]) * w.bmax[(size_t)b * rs + j];
+      aid = (float)fabs(1.0 / w.den[(size_t)b * N1 + c]);
+      const float gam = (float)(rt + 8) * 1.1920929e-7f;
+      rnd = 0.001953125f * wsum + gam * ((float)g.sc_dscale[c] + wsum);  // 2^-9: tf32 products
+    }
+    bool owndead = false;
+    for (int d = 0; d < snd[k]; ++d) owndead |= sdead[k][d] == ownp;
+    float keyv = 0.f;
+    const float smx = w.smax[(size_t)b * N1 + c];
+    for (int blk = 0; blk < SB; ++blk) {
+      float U = 0.f;
+      if (ok) {
+        float mb = 0.f;
+#pragma unroll
+        for (int bb = 0; bb < SB; ++bb)
+          if (bb == blk) mb = mxb[k][bb];
+        mb = fmaxf(mb, sMx[(blk * TB + k) * SM_CASES + ci]);
+        U = aid * (mb + rnd);
+        if (ownp >= 0 && ownp / MB == blk && !owndead) U = fmaxf(U, (float)g.inv_rating[ownp]);
+        U *= 1.f + 4e-6f;
+      }
+      w.scale[((size_t)b * SB + blk) * N1 + c] = U;
+      keyv = fmaxf(keyv, sm0[k][blk] + U * smx);
+    }
+    w.bkey[(size_t)b * N1 + c] = ok ? __float_as_uint(keyv) : 0u;
+  }
+}
+
+namespace {
+template <int TB, int KB>
+void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
+  size_t dyn = (size_t)TB * KB * (SM_CASES + 2 * SM_ROWS) * 32 + 2 * (size_t)SM_CASES * SD_LD * 4;
+  static_assert(SB * 4 * SM_CASES <= 2 * SM_CASES * SD_LD, "block maxima fit the D' buffer");
+  // at most 512 / NCOLS CTAs per SM fit their TMEM columns: size the shared memory so
+  // that no more are resident (a CTA spinning in tcgen05.alloc would hold an SM slot)
+  const int ncols = TB * SM_ROWS <= 64 ? 64 : (TB * SM_ROWS <= 128 ? 128 : 256);
+  dyn = std::max(dyn, (size_t)(220 * 1024) / (size_t)(512 / ncols));
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_scale_tc<TB, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    init = true;
+  }
+  const dim3 grid((g.N1 + SM_CASES - 1) / SM_CASES, (w.Wb + TB - 1) / TB);
+  k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, w);
+}
+}  // namespace
+
+void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
+  if (w.rs <= 8) launch_scale_tc_t<4, 1>(g, w, s);
+  else if (w.rs <= 16) launch_scale_tc_t<2, 2>(g, w, s);
+  else launch_scale_tc_t<1, 4>(g, w, s);
+}
+
+}  // namespace bdc

@@ -8,7 +8,8 @@
 //
 // Exact dominance screen (the reference's metric_first, solver.py:798-822):
 //   k_scale  per case and screening row block b an upper bound scale_bc of
-//            max_{r in b} |L'(r,c)|, and the ranking key of the case;
+//            max_{r in b} |L'(r,c)|, and the ranking key of the case (tcgen05,
+//            bdc_scale.cu);
 //   k_topk   the TOPC cases with the largest key (bdc_update.cu);
 //   k_top    those cases for every candidate (dense tile, FFMA2 + FMNMX3): they fix a
 //            good lower bound lb(t) of every candidate's metric, as the reference's
@@ -274,180 +275,7 @@ __global__ void __launch_bounds__(TX* TY, MINB) k_pairs(DevGrid g, DevCfg cfg, W
   }
 }
 
-// ---------------------------------------------------------------------------- k_scale
-// Per-case screening scales: for every screening row block b (bdc_device.cuh) an upper
-// bound of max_{r in b} |L'(r,c)| over the monitored rows (L' = the FP32 LODF/rating
-// values the sweeps multiply), from an FP32 evaluation L~ = D_base + sum_j B''_j W_j
-// with a rigorous rounding term:
-//     |L - L~| <= gamma (|D| + sum_j |B''_j| |W_j|),  gamma = (rt + 8) 2^-23,
-// bounded per case by sc_dscale_c + sum_j |W_cj| max_r |B''(r,j)|/rating_r.  The own
-// row contributes 1/rating (L' = -1/rating there), disconnected rows nothing.  Then the
-// ranking key bkey_c = max_b (max_t m0_b(t) + scale_bc max_t |s(c,t)|) (solver.py:815).
-// One thread per case, monitored-row chunks of D_base and B'' through a cp.async
-// double buffer; 4 rows of B'' per 16-byte shared load.
-namespace {
-constexpr int SC_NC = 256, SC_RC = 16;  // static shared memory stays under 48 KB
-}
-
-// RS = rank bucket >= every task's rank in the wave: W in registers, B'' terms past a
-// task's own rank are zero-filled, so the inner loop is straight-line FFMAs.  TB tasks
-// share a CTA: the D_base chunk (the shared operand) is staged and read once for all.
-template <int RS, int TB>
-__global__ void __launch_bounds__(SC_NC, 2) k_scale(DevGrid g, Work w) {
-  const int tb0 = blockIdx.y * TB;
-  const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * SC_NC, c = c0 + tid < g.N1 ? c0 + tid : -1;
-  const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
-  const int MB = screen_block_rows(M);
-  __shared__ __align__(16) float sD[2][SC_RC][SC_NC];
-  __shared__ __align__(16) float sB[2][TB][RS][SC_RC];
-  __shared__ __align__(16) float sInv[2][TB][SC_RC];
-  __shared__ int sdead[TB][RMAX];
-  __shared__ int snd[TB], srt[TB];
-  __shared__ float sm0[TB][SB];
-  if (tid < TB) {
-    const int b = tb0 + tid;
-    const bool on = b < w.Wb && w.status[b] == 0;
-    snd[tid] = on ? w.ndead[b] : 0;
-    srt[tid] = on ? w.rank[b] : -1;  // -1: slot idle
-  }
-  __syncthreads();
-  for (int i = tid; i < TB * RMAX; i += SC_NC) {
-    const int k = i / RMAX, d = i % RMAX;
-    if (d < snd[k]) sdead[k][d] = w.dead[(size_t)(tb0 + k) * RMAX + d];
-  }
-  // max_t m0_b(t) of each task and block (ranking key)
-  {
-    const int lane = tid & 31, wid = tid >> 5;
-    for (int kb = wid; kb < TB * SB; kb += SC_NC / 32) {
-      const int k = kb / SB, blk = kb % SB;
-      float v = 0.f;
-      if (srt[k] >= 0)
-        for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0b[((size_t)(tb0 + k) * SB + blk) * T + t]);
-      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) sm0[k][blk] = v;
-    }
-  }
-  __syncthreads();
-  bool any = false;
-#pragma unroll
-  for (int k = 0; k < TB; ++k) any |= srt[k] >= 0;
-  if (!any) return;
-  float wr[TB][RS];
-#pragma unroll
-  for (int k = 0; k < TB; ++k)
-#pragma unroll
-    for (int j = 0; j < RS; ++j) wr[k][j] = 0.f;
-  // per task: |1/den| and the rounding term of the FP32 evaluation (0 if infeasible)
-  float aid[TB], rnd[TB], keyv[TB], mx[TB];
-#pragma unroll
-  for (int k = 0; k < TB; ++k) { aid[k] = 0.f; rnd[k] = 0.f; keyv[k] = 0.f; mx[k] = 0.f; }
-  if (c >= 0) {
-#pragma unroll
-    for (int k = 0; k < TB; ++k) {
-      const int b = tb0 + k, rt = srt[k];
-#pragma unroll
-      for (int j = 0; j < RS; ++j)
-        if (j < rt) wr[k][j] = (float)w.Wsc[((size_t)b * N1 + c) * rs + j];
-      if (rt >= 0 && w.sc_ok[(size_t)b * N1 + c]) {
-        float wsum = 0.f;
-        for (int j = 0; j < rt; ++j)
-          wsum += (float)fabs(w.Wsc[((size_t)b * N1 + c) * rs + j]) * w.bmax[(size_t)b * rs + j];
-        const float gam = (float)(rt + 8) * 1.1920929e-7f;
-        aid[k] = (float)fabs(1.0 / w.den[(size_t)b * N1 + c]);
-        rnd[k] = gam * ((float)g.sc_dscale[c] + wsum);
-      }
-    }
-  }
-  const int rowc = c >= 0 ? g.sc_row[c] : -1;
-  const int ownp = c >= 0 ? g.row_mon_pos[rowc] : -1;
-  // block maxima -> scale_bc (written for every block, 0 for infeasible cases)
-  auto finish_block = [&](int blk) {
-    if (c < 0) return;
-#pragma unroll
-    for (int k = 0; k < TB; ++k) {
-      const int b = tb0 + k;
-      if (srt[k] < 0) continue;
-      float U = 0.f;
-      if (aid[k] != 0.f) {
-        U = aid[k] * (mx[k] + rnd[k]);
-        if (ownp >= 0 && ownp / MB == blk && !is_dead(sdead[k], snd[k], rowc))
-          U = fmaxf(U, (float)g.inv_rating[ownp]);
-        U *= 1.f + 4e-6f;
-      }
-      w.scale[((size_t)b * SB + blk) * N1 + c] = U;
-      keyv[k] = fmaxf(keyv[k], sm0[k][blk] + U * w.smax[(size_t)b * N1 + c]);
-      mx[k] = 0.f;
-    }
-  };
-  auto issue = [&](int m0, int buf) {
-    for (int idx = tid; idx < SC_RC * (SC_NC / 4); idx += SC_NC) {
-      const int rr = idx / (SC_NC / 4), q = 4 * (idx % (SC_NC / 4)), m = m0 + rr;
-      const bool okd = m < M && c0 + q < g.N1p;  // rows are zero-padded to N1p
-      cp16(&sD[buf][rr][q], okd ? &g.D32[(size_t)m * g.N1p + c0 + q] : g.D32, okd);
-    }
-    for (int idx = tid; idx < TB * RS * SC_RC; idx += SC_NC) {
-      const int k = idx / (RS * SC_RC), j = (idx / SC_RC) % RS, rr = idx % SC_RC, m = m0 + rr;
-      const bool okb = m < M && j < srt[k];  // zero-fill terms past the task's rank
-      const float* src = w.B32 + ((size_t)(tb0 + k) * rs + j) * M + m;
-      cp4(&sB[buf][k][j][rr], okb ? src : w.B32, okb);
-    }
-    for (int idx = tid; idx < TB * SC_RC; idx += SC_NC) {
-      const int k = idx / SC_RC, rr = idx % SC_RC, m = m0 + rr;
-      sInv[buf][k][rr] = (m < M && srt[k] >= 0 && !is_dead(sdead[k], snd[k], g.mon_row[m]))
-                             ? (float)g.inv_rating[m] : 0.f;
-    }
-    cp_commit();
-  };
-  issue(0, 0);
-  const int nchunks = (M + SC_RC - 1) / SC_RC;
-  int nblk = 0;  // blocks finished
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1, m0 = ch * SC_RC;
-    if (ch + 1 < nchunks) {
-      issue(m0 + SC_RC, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const int ownrr = ownp - m0;
-#pragma unroll 2
-    for (int r4 = 0; r4 < SC_RC; r4 += 4) {
-      float d[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) d[q] = sD[buf][r4 + q][tid];
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        float l0 = d[0], l1 = d[1], l2 = d[2], l3 = d[3];
-#pragma unroll
-        for (int j = 0; j < RS; ++j) {
-          const float4 bq = *reinterpret_cast<const float4*>(&sB[buf][k][j][r4]);
-          l0 = fmaf(bq.x, wr[k][j], l0);
-          l1 = fmaf(bq.y, wr[k][j], l1);
-          l2 = fmaf(bq.z, wr[k][j], l2);
-          l3 = fmaf(bq.w, wr[k][j], l3);
-        }
-        const float4 iq = *reinterpret_cast<const float4*>(&sInv[buf][k][r4]);
-        mx[k] = fmaxf(mx[k], (r4 + 0 == ownrr) ? 0.f : fabsf(l0) * iq.x);
-        mx[k] = fmaxf(mx[k], (r4 + 1 == ownrr) ? 0.f : fabsf(l1) * iq.y);
-        mx[k] = fmaxf(mx[k], (r4 + 2 == ownrr) ? 0.f : fabsf(l2) * iq.z);
-        mx[k] = fmaxf(mx[k], (r4 + 3 == ownrr) ? 0.f : fabsf(l3) * iq.w);
-      }
-    }
-    // a block ends at a multiple of MB (a multiple of SC_RC) or at the last row
-    if ((m0 + SC_RC) % MB == 0 || ch + 1 == nchunks) finish_block(nblk++);
-    __syncthreads();
-  }
-  for (; nblk < SB; ++nblk) finish_block(nblk);  // empty blocks (small M)
-  if (c < 0) return;
-#pragma unroll
-  for (int k = 0; k < TB; ++k) {
-    const int b = tb0 + k;
-    if (srt[k] < 0) continue;
-    w.bkey[(size_t)b * N1 + c] = aid[k] != 0.f ? __float_as_uint(keyv[k]) : 0u;
-  }
-}
+// k_scale (the per-case, per-block screening scales) runs on the tensor cores: bdc_scale.cu.
 
 // ---------------------------------------------------------------------------- k_live
 // The screen proper, pair by pair: for a case outside the TOP tile, candidate t is live
@@ -473,12 +301,30 @@ __global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
   const float pen = w.nisl[b] > 0 ? (float)cfg.penalty : 0.f;
   const float* m32 = reinterpret_cast<const float*>(w.m32) + (size_t)b * T;
   const float* m0b = w.m0b + (size_t)b * SB * T;
-  if (staged && w.screen) {
-    for (int t = tid; t < T; t += LC) {
-      sLb[t] = fmaxf(m32[t], pen);
+  // case-level reject: max_b (max_t m0_b + scale_bc max_t |s(c,t)|) <= min_t lb(t)
+  // bounds every pair of the case, so it is dominated without reading s(c, .)
+  __shared__ unsigned sLbMin, sM0Max[SB];
+  if (tid == 0) sLbMin = 0x7f800000u;
+  if (tid < SB) sM0Max[tid] = 0u;
+  __syncthreads();
+  if (w.screen) {
+    float lmin = __int_as_float(0x7f800000), mm[SB];
 #pragma unroll
-      for (int blk = 0; blk < SB; ++blk) sM0[blk][t] = m0b[(size_t)blk * T + t];
+    for (int blk = 0; blk < SB; ++blk) mm[blk] = 0.f;
+    for (int t = tid; t < T; t += LC) {
+      const float lbt = fmaxf(m32[t], pen);
+      lmin = fminf(lmin, lbt);
+      if (staged) sLb[t] = lbt;
+#pragma unroll
+      for (int blk = 0; blk < SB; ++blk) {
+        const float v = m0b[(size_t)blk * T + t];
+        mm[blk] = fmaxf(mm[blk], v);
+        if (staged) sM0[blk][t] = v;
+      }
     }
+    atomicMin(&sLbMin, __float_as_uint(lmin));
+#pragma unroll
+    for (int blk = 0; blk < SB; ++blk) atomicMax(&sM0Max[blk], __float_as_uint(mm[blk]));
   }
   __syncthreads();
   uint8_t* done = w.done + (size_t)b * N1;
@@ -490,9 +336,16 @@ __global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
   if (cl < N1) {
     const bool top = w.ranked ? done[cl] != 0 : cl < w.ptop;
     cand = !top && w.sc_ok[(size_t)b * N1 + cl] != 0;
-    if (cand && w.screen)
+    if (cand && w.screen) {
+      const float smx = w.smax[(size_t)b * N1 + cl];
+      float coarse = 0.f;
 #pragma unroll
-      for (int blk = 0; blk < SB; ++blk) scl[blk] = w.scale[((size_t)b * SB + blk) * N1 + cl];
+      for (int blk = 0; blk < SB; ++blk) {
+        scl[blk] = w.scale[((size_t)b * SB + blk) * N1 + cl];
+        coarse = fmaxf(coarse, __uint_as_float(sM0Max[blk]) + scl[blk] * smx);
+      }
+      if (coarse <= __uint_as_float(sLbMin)) cand = false;
+    }
   }
   bool mylive = cand && !w.screen;
   unsigned todo = __ballot_sync(0xffffffffu, cand && w.screen);
@@ -546,23 +399,6 @@ __global__ void k_queue(DevGrid g, Work w) {
 }
 
 namespace {
-template <int RS, int TB>
-void launch_scale_t(const DevGrid& g, const Work& w, cudaStream_t s) {
-  const dim3 grid((g.N1 + SC_NC - 1) / SC_NC, (w.Wb + TB - 1) / TB);
-  k_scale<RS, TB><<<grid, SC_NC, 0, s>>>(g, w);
-}
-void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
-  const int r = w.rs;
-  if (r <= 1) launch_scale_t<1, 4>(g, w, s);
-  else if (r <= 2) launch_scale_t<2, 4>(g, w, s);
-  else if (r <= 3) launch_scale_t<3, 4>(g, w, s);
-  else if (r <= 4) launch_scale_t<4, 4>(g, w, s);
-  else if (r <= 6) launch_scale_t<6, 4>(g, w, s);
-  else if (r <= 8) launch_scale_t<8, 2>(g, w, s);
-  else if (r <= 16) launch_scale_t<16, 1>(g, w, s);
-  else launch_scale_t<32, 1>(g, w, s);
-}
-
 template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
 void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   constexpr int NC = CPT * TX, TT = TPT * TY;
