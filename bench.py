@@ -293,6 +293,7 @@ def run_ours(args):
     clocks.start()
     elapsed_ms = 0.0
     pairs_eval = 0
+    report_cases = 0
     lf_total = 0
     stage = [0.0] * 8
     launches = 0
@@ -312,6 +313,7 @@ def run_ours(args):
         launches += nl
         waves = wv
         pairs_eval += eng.last_pairs
+        report_cases += eng.last_report_cases
     torch.cuda.synchronize()
     clk = clocks.stop()
     if ws > 1:
@@ -435,6 +437,7 @@ def run_ours(args):
             "pairs_total": pairs,
             "pairs_evaluated": evaluated,
             "skipped_frac": (1.0 - evaluated / pairs) if pairs else 0.0,
+            "report_cases_per_task": report_cases / args.steps / max(1, B),
             "note": "exact dominance screen of the reference's metric_first mode (solver.py:798-822); "
             "the metric is unchanged, skipped pairs are provably dominated",
         },

@@ -146,6 +146,8 @@ typedef struct {
   int64_t* n1_pairs;         /* (1) optional: (single case, candidate) pairs the N-1
                                 kernel evaluated; the rest were skipped by the exact
                                 dominance screen (solver.py:798-822) */
+  int64_t* report_cases;     /* (1) optional: single cases the FP64 winner report revisited
+                                (summed over tasks) */
   int32_t screen;            /* 0 = brute force every pair, 1 = exact dominance screen */
   /* timing (filled by the engine; milliseconds of device time per stage, summed over waves) */
   float stage_ms[8];

@@ -389,6 +389,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.n1cnt = (int*)(base + o_n1c); x.n1case = (int*)(base + o_n1k); x.n1pos = (int*)(base + o_n1p);
   x.n1flow = (double*)(base + o_n1f); x.n1rel = (double*)(base + o_n1r);
   // counters, one 32-byte block zeroed per call: [0] loadflows [1] bsdf [2] evaluated pairs
+  // [3] single cases revisited by the winner report
   x.lf = (unsigned long long*)(base + o_lf);
   x.bsdf = x.lf + 1;
   x.pairs = x.lf + 2;
@@ -682,6 +683,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (bt->loadflows) *bt->loadflows = (int64_t)counters[0];
   if (bt->bsdf_applications) *bt->bsdf_applications = (int64_t)counters[1];
   if (bt->n1_pairs) *bt->n1_pairs = (int64_t)counters[2];
+  if (bt->report_cases) *bt->report_cases = (int64_t)counters[3];
   bt->waves = nwaves;
   bt->kernel_launches = launches;
   return BDC_OK;

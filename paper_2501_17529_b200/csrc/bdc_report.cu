@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
       int acc = 0;
       for (int i = 0; i < RW; ++i) { woff[i] = acc; acc += wcnt[i]; }
       w.rcnt[b] = acc;
+      atomicAdd(w.lf + 3, (unsigned long long)acc);
     }
     __syncthreads();
     int* rl = w.rlist + (size_t)b * N1;
@@ -415,12 +416,17 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
 }
 
 // --------------------------------------------------------------------------- k_rsweep
-// Winner report, part 2: the listed single cases in FP64 for the winning candidate,
-// RCW cases per CTA, a warp per case with lanes over monitored rows (coalesced reads of
-// D_base, B'', the N-0 column and 1/rating).  Each lane keeps its rows' stable top-kc
-// (rel desc, position asc; solver.py:287-299), merged per case into the warp's top-kg by
-// (rel desc, case order, position) (_merge_entries, solver.py:302-318); the CTA merges
-// its warps' lists into one partial slot.
+// Winner report, part 2: the listed single cases in FP64 for the winning candidate, RCW
+// cases per CTA in groups of RW (a warp per case, lanes over monitored rows).  The rows
+// stream in chunks of SRC through a cp.async double buffer holding the task's B'' rows,
+// N-0 column and 1/rating for the chunk -- shared by the group's RW cases -- while each
+// warp reads its case's D_base column (coalesced).  Each lane keeps its rows' stable
+// top-kc (rel desc, position asc; solver.py:287-299), merged per case into the warp's
+// top-kg by (rel desc, case order, position) (_merge_entries, solver.py:302-318); the
+// CTA merges its warps' lists into one partial slot.
+namespace {
+constexpr int SRC = 128;  // monitored rows per chunk (4 per lane)
+}
 template <int KC>
 __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.y, tile = blockIdx.x;
@@ -429,6 +435,10 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   if (tile * RCW >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kc = cfg.kc, kg = cfg.kg;
+  extern __shared__ __align__(16) double rsm[];
+  double* sB = rsm;                  // [2][rt][SRC] B'' on the chunk's monitored rows
+  double* sN = sB + 2 * rs * SRC;    // [2][SRC] N-0 column
+  double* sI = sN + 2 * SRC;         // [2][SRC] 1 / rating
   __shared__ WarpList wl[RW];
   __shared__ double sWc[RW][RMAX];
   __shared__ double wmax[RW];
@@ -436,55 +446,78 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   const int nd = w.ndead[b];
   if (tid < nd) sdeadp[tid] = g.row_mon_pos[w.dead[(size_t)b * RMAX + tid]];
   if (lane == 0) wl[wid].n = 0;
-  __syncthreads();
   const double* n0m = w.n0m + (size_t)b * M;
   const double* Bmon = w.Bmon + (size_t)b * rs * M;
-  // the final top-kg holds the kg largest case maxima, all >= theta (k_rsel): entries
-  // below it are never reported, so they never enter a list
-  const double floor_rel = (double)w.theta[b];
+  const double floor_rel = (double)w.theta[b];  // entries below theta are never reported
   double mymax = 0.0;
   LaneTop<KC> lt;
-  constexpr int U = 4;  // rows per lane per step: independent loads in flight
+  auto issue = [&](int m0, int bf) {
+    for (int idx = tid; idx < rt * SRC; idx += RT) {
+      const int j = idx / SRC, r = idx % SRC, m = m0 + r;
+      cp8(&sB[(bf * rs + j) * SRC + r], m < M ? &Bmon[(size_t)j * M + m] : Bmon, m < M);
+    }
+    for (int r = tid; r < SRC; r += RT) {
+      const int m = m0 + r;
+      cp8(&sN[bf * SRC + r], m < M ? &n0m[m] : n0m, m < M);
+      cp8(&sI[bf * SRC + r], m < M ? &g.inv_rating[m] : g.inv_rating, m < M);
+    }
+    cp_commit();
+  };
+  const int nchunks = (M + SRC - 1) / SRC;
   const int end = min(n, (tile + 1) * RCW);
-  for (int li = tile * RCW + wid; li < end; li += RW) {
-    const int c = w.rlist[(size_t)b * N1 + li];
-    const int rowc = g.sc_row[c], order = g.sc_order[c], ownp = g.row_mon_pos[rowc];
-    const double idn = 1.0 / w.den[(size_t)b * N1 + c];
-    const double sc = w.n0b[(size_t)b * g.R + rowc];
-    for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
-    __syncwarp();
-    const double* Dc = g.DM64 + (size_t)c * M;
-    const double thresh = fmax(warp_thresh(wl[wid], kg), floor_rel);
+  for (int g0 = tile * RCW; g0 < end; g0 += RW) {
+    const int li = g0 + wid;
+    const int c = li < end ? w.rlist[(size_t)b * N1 + li] : -1;
+    int ownp = -1, order = INT_MAX;
+    double idn = 0.0, sc = 0.0;
+    if (c >= 0) {
+      const int rowc = g.sc_row[c];
+      ownp = g.row_mon_pos[rowc];
+      order = g.sc_order[c];
+      idn = 1.0 / w.den[(size_t)b * N1 + c];
+      sc = w.n0b[(size_t)b * g.R + rowc];
+      for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+    }
+    const double* Dc = g.DM64 + (size_t)(c >= 0 ? c : 0) * M;
     lt.clear();
-    for (int p0 = lane; p0 < M; p0 += 32 * U) {
-      double dv[U], nv[U], iv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = p0 + 32 * u;
-        const bool ok = p < M;
-        dv[u] = ok ? __ldg(&Dc[p]) : 0.0;
-        nv[u] = ok ? n0m[p] : 0.0;
-        iv[u] = ok ? __ldg(&g.inv_rating[p]) : 0.0;
+    __syncthreads();  // sWc written; the previous group's chunk buffers are free
+    const double thresh = fmax(warp_thresh(wl[wid], kg), floor_rel);
+    issue(0, 0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int bf = ch & 1, m0 = ch * SRC;
+      if (ch + 1 < nchunks) {
+        issue(m0 + SRC, bf ^ 1);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
       }
-      for (int j = 0; j < rt; ++j) {
-        const double wj = sWc[wid][j];
+      __syncthreads();
+      if (c >= 0) {
+        double dv[SRC / 32];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int p = p0 + 32 * u;
-          if (p < M) dv[u] = fma(Bmon[(size_t)j * M + p], wj, dv[u]);
+        for (int u = 0; u < SRC / 32; ++u) {
+          const int p = m0 + lane + 32 * u;
+          dv[u] = p < M ? __ldg(&Dc[p]) : 0.0;
+        }
+        for (int j = 0; j < rt; ++j) {
+          const double wj = sWc[wid][j];
+#pragma unroll
+          for (int u = 0; u < SRC / 32; ++u) dv[u] = fma(sB[(bf * rs + j) * SRC + lane + 32 * u], wj, dv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < SRC / 32; ++u) {
+          const int r = lane + 32 * u, p = m0 + r;
+          if (p >= M || is_dead(sdeadp, nd, p)) continue;  // disconnected: flow exactly 0
+          const double nv = sN[bf * SRC + r];
+          const double f = (p == ownp) ? nv + (-1.0) * sc : nv + (dv[u] * idn) * sc;
+          const double rel = fabs(f) * sI[bf * SRC + r];
+          mymax = fmax(mymax, rel);
+          if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = p0 + 32 * u;
-        if (p >= M || is_dead(sdeadp, nd, p)) continue;  // disconnected: flow exactly 0
-        const double f = (p == ownp) ? nv[u] + (-1.0) * sc : nv[u] + (dv[u] * idn) * sc;
-        const double rel = fabs(f) * iv[u];
-        mymax = fmax(mymax, rel);
-        if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
-      }
+      __syncthreads();
     }
-    warp_merge<KC>(lt, kc, wl[wid], kg, order);
+    if (c >= 0) warp_merge<KC>(lt, kc, wl[wid], kg, order);
     __syncwarp();
   }
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
@@ -652,7 +685,16 @@ namespace {
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
-  if (g.N1 > 0 && g.M > 0) k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RT, 0, s>>>(g, c, w);
+  if (g.N1 > 0 && g.M > 0) {
+    const size_t dyn = (2 * (size_t)w.rs * SRC + 4 * (size_t)SRC) * sizeof(double);
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_rsweep<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((2 * (size_t)RMAX * SRC + 4 * (size_t)SRC) * sizeof(double)));
+      init = true;
+    }
+    k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RT, dyn, s>>>(g, c, w);
+  }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
 }

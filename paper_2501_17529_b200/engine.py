@@ -101,6 +101,7 @@ class _Batch(ctypes.Structure):
         ("loadflows", _P),
         ("bsdf_applications", _P),
         ("n1_pairs", _P),
+        ("report_cases", _P),
         ("screen", ctypes.c_int32),
         ("stage_ms", ctypes.c_float * 8),
         ("waves", ctypes.c_int32),
@@ -387,13 +388,16 @@ class Engine:
             setattr(bt, name, ctypes.c_void_p(t.data_ptr()))
         lf = loadflows if loadflows is not None else np.zeros(1, dtype=np.int64)
         pairs = np.zeros(1, dtype=np.int64)
+        rcases = np.zeros(1, dtype=np.int64)
         bt.loadflows = _ptr(lf)
         bt.n1_pairs = _ptr(pairs)
+        bt.report_cases = _ptr(rcases)
         bt.screen = int(self.screen)
         rc = self.lib.bdc_solve(self.handle, ctypes.byref(bt))
         if rc != 0:
             raise EngineUnavailable(f"bdc_solve failed ({rc}): {_err(self.lib)}")
         self.last_pairs = int(pairs[0])
+        self.last_report_cases = int(rcases[0])
         return [float(x) for x in bt.stage_ms], int(bt.waves), int(bt.kernel_launches), int(lf[0])
 
     def probe_flows(self, splits_row: np.ndarray, discos_row: np.ndarray, inj_rows: np.ndarray):

@@ -15,6 +15,6 @@ try:
 except Exception as e:
     print(c, "FAILED", open(f"gpurun_out/bench_{c}.json").read()[-2000:]); sys.exit()
 st = {k: round(v, 2) for k, v in d["stage_ms_per_step"].items()}
-print(c, f"value={d['value']:.3e} e2e={d['e2e']['value']:.3e} ms/step={d['ms_per_step']:.2f} frac={d['roofline']['frac']:.3f} skip={d['screen']['skipped_frac']:.3f}", st)
+print(c, f"value={d['value']:.3e} e2e={d['e2e']['value']:.3e} ms/step={d['ms_per_step']:.2f} frac={d['roofline']['frac']:.3f} skip={d['screen']['skipped_frac']:.3f} rcases={d['screen'].get('report_cases_per_task', -1):.1f}", st)
 PY
 done
