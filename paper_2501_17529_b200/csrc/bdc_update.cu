@@ -45,6 +45,7 @@ struct UpdShared {
   double den;
   double sCa[RMAX];          // C[i][a]
   double inner[MMAX * MMAX];
+  double mA[UW][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
   double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
   double ybase[RMAX];
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
@@ -400,33 +401,53 @@ __global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w)
       w.sc_ok[(size_t)b * g.N1 + c] = ok;
       if (!ok) { set_island(w, b, g.sc_order[c]); atomicAdd(&s.nisl, 1); }
     }
-    // multi-branch cases: m x m inner system, SVD islanding test, inverse
-    for (int q = tid; q < g.NM; q += UT) {
+    // multi-branch cases: m x m inner system, SVD islanding test, inverse; a warp per case
+    // (lanes form the member W rows and the m x m entries, lane 0 factorises)
+    for (int q = tid >> 5; q < g.NM; q += UW) {
+      const int lane = tid & 31, wid = tid >> 5;
       const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-      double A[MMAX * MMAX];
-      for (int i = 0; i < m; ++i) {
+      for (int idx = lane; idx < m * rt; idx += 32) {
+        const int i = idx / rt, j = idx % rt;
         const int row = g.mb_row[st + i];
         const int fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]), tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
-        double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-        for (int j = 0; j < rt; ++j) Wq[j] = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
+        w.Wm[((size_t)b * g.NMB + st + i) * rs + j] = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
       }
-      for (int aa = 0; aa < m; ++aa) {
+      __syncwarp();
+      double* A = s.mA[wid];
+      for (int idx = lane; idx < m * m; idx += 32) {
+        const int aa = idx / m, bb = idx % m;
         const int ra = g.mb_row[st + aa];
-        const bool dead = is_dead(s.dead, nd, ra);
-        for (int bb = 0; bb < m; ++bb) {
-          double v = g.Dm64[(size_t)(st + bb) * R + ra];
-          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + bb) * rs;
-          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + ra], Wq[j], v);
-          if (dead) v = 0.0;
-          A[aa * m + bb] = (aa == bb ? 1.0 : 0.0) - v;
-        }
+        double v = g.Dm64[(size_t)(st + bb) * R + ra];
+        const double* Wq = w.Wm + ((size_t)b * g.NMB + st + bb) * rs;
+        for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + ra], Wq[j], v);
+        if (is_dead(s.dead, nd, ra)) v = 0.0;
+        A[aa * m + bb] = (aa == bb ? 1.0 : 0.0) - v;
       }
-      double smax, smin;
-      svd_minmax(A, m, smax, smin);
-      const bool ok = !(smin < ISL_TOL * fmax(1.0, smax));
-      if (ok) invert_small(A, m, w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX);
-      w.mc_ok[(size_t)b * g.NM + q] = ok;
-      if (!ok) { set_island(w, b, g.mc_order[q]); atomicAdd(&s.nisl, 1); }
+      __syncwarp();
+      if (lane == 0) {
+        double smax, smin;
+        double* inv = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
+        bool ok;
+        if (m == 2) {
+          // closed form: sigma_max from the Frobenius norm and |det|, sigma_min = |det| / sigma_max
+          const double a = A[0], bq = A[1], c = A[2], d = A[3];
+          const double S = a * a + bq * bq + c * c + d * d, det = a * d - bq * c;
+          smax = sqrt(0.5 * (S + sqrt(fmax(S * S - 4.0 * det * det, 0.0))));
+          smin = smax > 0.0 ? fabs(det) / smax : 0.0;
+          ok = !(smin < ISL_TOL * fmax(1.0, smax));
+          if (ok) {
+            const double id = 1.0 / det;
+            inv[0] = d * id; inv[1] = -bq * id; inv[2] = -c * id; inv[3] = a * id;
+          }
+        } else {
+          svd_minmax(A, m, smax, smin);
+          ok = !(smin < ISL_TOL * fmax(1.0, smax));
+          if (ok) invert_small(A, m, inv);
+        }
+        w.mc_ok[(size_t)b * g.NM + q] = ok;
+        if (!ok) { set_island(w, b, g.mc_order[q]); atomicAdd(&s.nisl, 1); }
+      }
+      __syncwarp();
     }
     // injection cases: coupler coefficients of the outaged injection's columns
     for (int q = tid; q < g.NI; q += UT) {
