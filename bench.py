@@ -232,6 +232,54 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- rooflines
+def stage_rooflines(tb, splits, discos, fe, T, evaluated, stage_ms, n_cases):
+    """Algorithmic work of each device stage over its live
+    CUDA-event time, against its bound: HBM bytes, tcgen05 TF32 flops, or FP32 lane-ops."""
+    peaks, src = _peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    tf32 = float(peaks.get("bf16_tflops", 2250.0)) * 1e12 / 2.0  # dense TF32 = BF16 / 2
+    alu = 148 * 128 * sm_mhz * 1e6
+    R, M, N1, C0 = tb.R, tb.M, tb.N1, tb.C0
+    sp = splits.view(np.uint8).reshape(splits.shape[0], tb.S, -1).astype(bool)
+    moved = sp.any(axis=2)                                   # (B, S) split substations
+    k = moved.sum(axis=1)
+    d = (discos >= 0).sum(axis=1) if discos.size else np.zeros(len(k), dtype=np.int64)
+    r = (k + d)[fe].astype(np.float64)
+    e_sum = (moved * np.asarray(tb.sub_count)[None, :]).sum(axis=1)[fe].astype(np.float64)
+    kf, df = k[fe].astype(np.float64), d[fe].astype(np.float64)
+    # update: touched FP64 rows / columns of P0 and the factors written (SURVEY 8(d) stage 1)
+    upd = float((8 * (e_sum * C0 + (e_sum + kf) * R) + 8 * df * (C0 + 2 * R) + 4 * (R + C0 + N1) * r).sum())
+    # N-0: n0/rating and s written (FP32), B''/rating (FP32 + FP64 copies), B'' and Y read
+    n0b = float((4.0 * (M + N1) * T + 12.0 * r * M + 8.0 * r * (R + T)).sum())
+    # screening scales: the rank-r product per (monitored row, case) on the tensor cores
+    scl = float((2.0 * M * N1 * r).sum())
+    # N-1 single-branch: FFMA + FMNMX per monitored row of every evaluated (case, candidate)
+    n1 = 2.0 * M * evaluated
+    out = []
+
+    def add(kernel, stage_keys, bound, work, peak, unit, what):
+        ms = sum(stage_ms.get(s, 0.0) for s in stage_keys)
+        if ms <= 0:
+            return
+        ach = work / (ms / 1e3)
+        out.append({"kernel": kernel, "bound": bound, "achieved": ach / (1e9 if unit == "GB/s" else 1e12 if unit == "TFLOP/s" else 1e9),
+                    "peak": peak / (1e9 if unit == "GB/s" else 1e12 if unit == "TFLOP/s" else 1e9), "unit": unit,
+                    "frac": ach / peak, "kernel_ms_per_step": ms, "work": what})
+
+    add("k_update (split chain, outages, case factors; FP64)", ["update"], "hbm", upd, hbm, "GB/s",
+        "8*sum_j(|E_j| C + (|E_j|+1) R) + 8 d (C + 2R) + 4 (R + C + N1)(k+d) bytes per task")
+    add("k_n0 (N-0 contraction + screening data)", ["n0"], "hbm", n0b, hbm, "GB/s",
+        "4 (M + N1) T + 12 (k+d) M + 8 (k+d)(R + T) bytes per task")
+    add("k_scale_tc (screening scales, tcgen05 TF32)", ["scale"], "tensor", scl, tf32, "TFLOP/s",
+        f"2 M N1 (k+d) flops per task; peak = dense TF32 = BF16/2 ({src} MEASURED_PEAKS.json)")
+    add("k_top + k_live + k_pairs (single-branch N-1, FFMA2/FMNMX3)", ["top", "screen"], "alu", n1, alu, "Gop/s",
+        f"2 lane-ops (FFMA + FMNMX) per monitored row per evaluated (case, candidate); "
+        f"peak = 148 SMs x 128 lanes x {sm_mhz:.0f} MHz")
+    return out
+
+
 # ---------------------------------------------------------------------------- GPU leg
 def run_ours(args):
     import torch
@@ -295,7 +343,9 @@ def run_ours(args):
     pairs_eval = 0
     report_cases = 0
     lf_total = 0
-    stage = [0.0] * 8
+    from paper_2501_17529_b200.engine import STAGES
+
+    stage = [0.0] * len(STAGES)
     launches = 0
     waves = 0
     for _ in range(args.steps):
@@ -360,7 +410,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (k_single), live from the engine's CUDA events
+    # ---- per-stage rooflines, kernel times live from the engine's CUDA events
     tb = eng.tables
     fe = out.feasible.astype(bool)
     single_orders = set(int(x) for x in tb.sc_order)
@@ -368,24 +418,23 @@ def run_ours(args):
     for b in np.flatnonzero(out.n_islanded > 0):
         isl_single[b] = sum(1 for o in out.islanded_orders(int(b)) if o in single_orders)
     pairs = float(((tb.N1 - isl_single) * fe).sum()) * T  # feasible (case, candidate) pairs per step
-    evaluated = pairs_eval / args.steps  # pairs the sweep actually evaluated (screen on)
-    ops_per_launch_set = 2.0 * tb.M * evaluated  # FFMA + FMNMX per monitored row
-    single_ms = stage[3] / args.steps
-    peaks, src = _peaks()
-    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_ops = 148 * 128 * sm_mhz * 1e6
-    achieved = ops_per_launch_set / (single_ms / 1e3)
+    evaluated = pairs_eval / args.steps  # pairs the N-1 kernels actually evaluated (screen on)
+    stage_ms = {n: v / args.steps for n, v in zip(STAGES, stage)}
+    roof = stage_rooflines(tb, splits, discos, fe, T, evaluated, stage_ms, len(grid.contingencies))
+    dom = max(roof, key=lambda r: r["kernel_ms_per_step"])  # the dominant stage with a roofline
     traffic = None
-    tp = os.path.join(REPO, "profiles", "k_single_traffic.json")
+    tp = os.path.join(REPO, "profiles", "kernel_traffic.json")
     if os.path.exists(tp):
         try:
             with open(tp) as fh:
                 tj = json.load(fh)
-            pw = tj.get("per_workload", {}).get(args.config)
-            if pw:
-                traffic = pw["dram_bytes_per_task"] * B / max(1, waves)
+            per_task = tj.get(args.config, {}).get(dom["kernel"].split()[0])
+            if per_task:
+                traffic = per_task * B / max(1, waves)  # DRAM bytes per launch (ncu --set full)
         except (OSError, ValueError):
             traffic = None
+    roofline = dict(dom)
+    roofline["traffic"] = traffic
     step_ms = elapsed_max / args.steps
     line = {
         "metric": "DC loadflows/sec (topo x inj x N-1)",
@@ -415,23 +464,9 @@ def run_ours(args):
         },
         "e2e": {"value": e2e_val, "unit": "loadflows/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "how": "session API solve_batch_output, pinned host arrays in, host arrays out, wall clock, max over ranks"},
-        "roofline": {
-            "kernel": "k_single (fused single-branch N-1 screen)",
-            "bound": "alu",
-            "achieved": achieved / 1e9,
-            "peak": peak_ops / 1e9,
-            "unit": "Gop/s",
-            "frac": achieved / peak_ops,
-            "traffic": traffic,
-            "ops_definition": "2 lane-ops (FFMA + FMNMX) per monitored row per (task, candidate, single case) "
-            "pair the sweep evaluated; kernel time = scale pass + screened sweep",
-            "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz {sm_mhz:.0f} ({src} MEASURED_PEAKS.json)",
-            "kernel_ms_per_step": single_ms,
-        },
-        "stage_ms_per_step": {
-            n: v / args.steps
-            for n, v in zip(["h2d", "update", "other_n1", "single_n1", "select", "winner", "report", "d2h"], stage)
-        },
+        "roofline": roofline,
+        "stages_roofline": roof,
+        "stage_ms_per_step": stage_ms,
         "screen": {
             "enabled": bool(eng.screen),
             "pairs_total": pairs,

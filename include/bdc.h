@@ -98,6 +98,23 @@ typedef struct {
   const int32_t* ic_order;   /* (NI)      */
 } BdcGrid;
 
+/* Device-time stages of bdc_solve (BdcBatch.stage_ms). */
+#define BDC_STAGES 12
+enum {
+  BDC_STAGE_H2D = 0,      /* input copies + per-wave resets */
+  BDC_STAGE_UPDATE = 1,   /* k_update: split chain, outages, case factors */
+  BDC_STAGE_N0 = 2,       /* k_n0: N-0 contraction, screening data */
+  BDC_STAGE_OTHER = 3,    /* k_other: multi-branch / injection cases */
+  BDC_STAGE_SCALE = 4,    /* k_scale_tc: screening scales (tcgen05) */
+  BDC_STAGE_TOPK = 5,     /* k_topk */
+  BDC_STAGE_TOP = 6,      /* k_top: the TOP tile */
+  BDC_STAGE_SCREEN = 7,   /* k_live + k_queue + k_pairs */
+  BDC_STAGE_SELECT = 8,   /* k_select */
+  BDC_STAGE_REPORT = 9,   /* k_rsel + k_rsweep + k_rmerge */
+  BDC_STAGE_D2H = 10,     /* output copies */
+  BDC_STAGE_SPARE = 11
+};
+
 /* SolveConfig (solver.py:61-91) fields the device needs. */
 typedef struct {
   int32_t topk_per_case;
@@ -150,7 +167,7 @@ typedef struct {
                                 (summed over tasks) */
   int32_t screen;            /* 0 = brute force every pair, 1 = exact dominance screen */
   /* timing (filled by the engine; milliseconds of device time per stage, summed over waves) */
-  float stage_ms[8];
+  float stage_ms[BDC_STAGES];  /* see BDC_STAGE_* */
   int32_t waves;
   int32_t kernel_launches;
 } BdcBatch;

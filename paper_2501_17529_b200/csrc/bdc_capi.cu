@@ -447,7 +447,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   const DevGrid& g = s->g;
   const int64_t B = bt->B;
   const int T = bt->T, D = bt->D, Ein = g.E > 0 ? g.E : 1;
-  for (int i = 0; i < 8; ++i) bt->stage_ms[i] = 0.f;
+  for (int i = 0; i < BDC_STAGES; ++i) bt->stage_ms[i] = 0.f;
   bt->waves = 0;
   bt->kernel_launches = 0;
   if (B < 0 || T < 1 || D < 0) return fail(BDC_EINVAL, "bad batch dimensions");
@@ -495,7 +495,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   CK(cudaMemsetAsync(w.lf, 0, 32, st));
 
   const int nwaves = (int)((B + Wb - 1) / Wb);
-  std::vector<cudaEvent_t> ev((size_t)nwaves * 9);
+  constexpr int NE = BDC_STAGES + 1;  // events per wave
+  std::vector<cudaEvent_t> ev((size_t)nwaves * NE);
   for (auto& e : ev) CK(cudaEventCreate(&e));
   const bool ondev_in = bt->inputs_on_device != 0, ondev_out = bt->outputs_on_device != 0;
   const int kg = s->cfg.kg, NCw = w.NCw;
@@ -567,7 +568,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     const int nb = (int)std::min<int64_t>(Wb, B - b0);
     Work x = w;
     x.Wb = nb;
-    cudaEvent_t* E = &ev[(size_t)wv * 9];
+    cudaEvent_t* E = &ev[(size_t)wv * NE];
     cudaEventRecord(E[0], st);
     const cudaMemcpyKind hk = ondev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const size_t sz_spl = (size_t)g.S * Ein, sz_inj = (size_t)T * g.K;
@@ -587,20 +588,21 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
-    // stage_ms: 0 h2d, 1 update (+ fused N-0, screen data), 2 multi/injection N-1,
-    // 3 single N-1 (top tile + screened sweep), 4 select, 5 (unused), 6 report, 7 d2h
+    // stage_ms (bdc.h BDC_STAGE_*): 0 h2d, 1 update, 2 N-0, 3 multi/injection N-1,
+    // 4 screening scales (tcgen05), 5 top-k, 6 TOP tile, 7 screen + live cases,
+    // 8 select, 9 winner report, 10 d2h, 11 unused
     launch_update(g, s->cfg, x, st);
-    launch_n0(g, x, st);
     cudaEventRecord(E[2], st);
-    launch_other(g, x, st);
+    launch_n0(g, x, st);
     cudaEventRecord(E[3], st);
-    launch_single(g, s->cfg, x, st);
+    launch_other(g, x, st);
     cudaEventRecord(E[4], st);
+    launch_single(g, s->cfg, x, st, &E[4]);  // records E[5], E[6], E[7]
+    cudaEventRecord(E[8], st);
     launch_select(g, s->cfg, x, st);
-    cudaEventRecord(E[5], st);
-    cudaEventRecord(E[6], st);
+    cudaEventRecord(E[9], st);
     launch_report(g, s->cfg, x, st);
-    cudaEventRecord(E[7], st);
+    cudaEventRecord(E[10], st);
     launches += kernels_per_wave(g, x);
     err = cudaGetLastError();
     if (err != cudaSuccess) break;
@@ -659,7 +661,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
       staged_nb[wv & 1] = nb;
       if (wv > 0 && e2 == cudaSuccess) chk(unpack((wv - 1) & 1));
     }
-    cudaEventRecord(E[8], st);
+    cudaEventRecord(E[11], st);
+    cudaEventRecord(E[12], st);
     err = e2;
   }
   if (!ondev_out && err == cudaSuccess) err = unpack((nwaves - 1) & 1);
@@ -669,8 +672,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (err == cudaSuccess) err = es;
   if (err == cudaSuccess) {
     for (int wv = 0; wv < nwaves; ++wv) {
-      cudaEvent_t* E = &ev[(size_t)wv * 9];
-      for (int k = 0; k < 8; ++k) {
+      cudaEvent_t* E = &ev[(size_t)wv * NE];
+      for (int k = 0; k < BDC_STAGES; ++k) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, E[k], E[k + 1]) == cudaSuccess) {
           bt->stage_ms[k] += ms;

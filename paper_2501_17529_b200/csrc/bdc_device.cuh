@@ -267,7 +267,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
-void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s, cudaEvent_t* ev = nullptr);
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);

@@ -718,7 +718,8 @@ int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
   // update, N-0, select, report select + merge (+ single: the N-1 stage's launches and
   // the report sweep) (+ other)
-  return 5 + (single ? single_launches(g, w) + 1 : 0) + (g.NM + g.NI > 0 && g.M > 0);
+  // (+ multi/injection: the correction terms and k_other)
+  return 5 + (single ? single_launches(g, w) + 1 : 0) + 2 * (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

@@ -19,6 +19,8 @@
 //   candidate injection vectors   solver.py:575-595   (y_t = C''^T p_t, so n0 = f0 + B'' y_t)
 #include "bdc_device.cuh"
 
+#include <algorithm>
+
 namespace bdc {
 
 namespace {
@@ -515,76 +517,6 @@ __global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w)
       w.rank[b] = rt;
     }
     __syncthreads();
-    if (!s.fail) {
-      const int T = w.T, M = g.M;
-      // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
-      // F = n0 + sum_j Lo[r][j] So[j][t]; columns formed once per task in FP64
-      const int NTM = w.NTERM, MT = g.MT, NQ = g.NM + g.NI;
-      if (NTM > 0) {
-        float* Lo = w.Lo + (size_t)b * M * NTM;
-        float* So = w.So + (size_t)b * NTM * T;
-        for (int idx = tid; idx < M * NQ; idx += UT) {
-          const int p = idx / NQ, q = idx % NQ;
-          const int row = g.mon_row[p];
-          const double inv = g.inv_rating[p];
-          const bool dead = is_dead(s.dead, nd, row);
-          float* out = Lo + ((size_t)p * NQ + q) * MT;
-          for (int j = 0; j < MT; ++j) out[j] = 0.f;
-          if (dead) continue;
-          if (q < g.NM) {
-            const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-            if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
-            int own = -1;
-            for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
-            if (own >= 0) {
-              out[own] = (float)(-inv);
-              continue;
-            }
-            double Dv[MMAX];
-            for (int i = 0; i < m; ++i) {
-              double v = g.Dm64[(size_t)(st + i) * R + row];
-              const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-              for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
-              Dv[i] = v;
-            }
-            const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
-            for (int j = 0; j < m; ++j) {
-              double v = 0.0;
-              for (int i = 0; i < m; ++i) v += Dv[i] * Mi[i * m + j];
-              out[j] = (float)(v * inv);
-            }
-          } else {
-            const int qi = q - g.NM, sl = g.ic_slot[qi];
-            const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
-            const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
-            const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
-            double pa = g.P0T[(size_t)ca * R + row], pb = pa;
-            for (int j = 0; j < rt; ++j) {
-              const double bv = Bm[(size_t)j * R + row];
-              pa = fma(bv, pa_[j], pa);
-              pb = fma(bv, pb_[j], pb);
-            }
-            const double sp = g.ic_sp[qi];
-            out[0] = (float)(-sp * pa * inv);
-            out[1] = (float)(-sp * (pb - pa) * inv);
-          }
-        }
-        const uint8_t* ib = w.inj + (size_t)b * T * g.K;
-        for (int idx = tid; idx < NTM * T; idx += UT) {
-          const int qj = idx / T, t = idx % T, q = qj / MT, j = qj % MT;
-          float v = 0.f;
-          if (q < g.NM) {
-            const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-            if (j < m) v = (float)n0_at(g, w, b, g.mb_row[st + j], t, rt, s.dead, nd);
-          } else if (j < 2) {
-            const int sl = g.ic_slot[q - g.NM];
-            v = j == 0 ? 1.f : ((sl >= 0 && ib[(size_t)t * g.K + sl]) ? 1.f : 0.f);
-          }
-          So[idx] = v;
-        }
-      }
-      __syncthreads();
-    }
   }
   __syncthreads();
 
@@ -605,6 +537,83 @@ done:
 #undef MB
 #undef SCF
 #undef OB
+}
+
+// ---- multi-branch and injection cases as correction terms (solver.py:614-622):
+// F = n0 + sum_j Lo[r][j] So[j][t], columns formed once per task in FP64 and rounded
+// to FP32 (scaled by 1/rating) for k_other.  Fully parallel over (row, case) and
+// (term, candidate): grid (blocks, task), grid-stride over both index ranges.
+__global__ void __launch_bounds__(NT) k_terms(DevGrid g, Work w) {
+  const int b = blockIdx.y;
+  if (w.status[b] != 0) return;
+  const int R = g.R, rs = w.rs, rt = w.rank[b], T = w.T, M = g.M;
+  const int NTM = w.NTERM, MT = g.MT, NQ = g.NM + g.NI;
+  const int nd = w.ndead[b];
+  const int* dead = w.dead + (size_t)b * RMAX;
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  float* Lo = w.Lo + (size_t)b * M * NTM;
+  float* So = w.So + (size_t)b * NTM * T;
+  const uint8_t* ib = w.inj + (size_t)b * T * g.K;
+  const int nlo = M * NQ, nso = NTM * T;
+  for (int idx = blockIdx.x * NT + threadIdx.x; idx < nlo + nso; idx += gridDim.x * NT) {
+    if (idx < nlo) {
+      const int p = idx / NQ, q = idx % NQ;
+      const int row = g.mon_row[p];
+      const double inv = g.inv_rating[p];
+      float* out = Lo + ((size_t)p * NQ + q) * MT;
+      for (int j = 0; j < MT; ++j) out[j] = 0.f;
+      if (is_dead(dead, nd, row)) continue;
+      if (q < g.NM) {
+        const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+        if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
+        int own = -1;
+        for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+        if (own >= 0) {
+          out[own] = (float)(-inv);
+          continue;
+        }
+        double Dv[MMAX];
+        for (int i = 0; i < m; ++i) {
+          double v = g.Dm64[(size_t)(st + i) * R + row];
+          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+          Dv[i] = v;
+        }
+        const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
+        for (int j = 0; j < m; ++j) {
+          double v = 0.0;
+          for (int i = 0; i < m; ++i) v += Dv[i] * Mi[i * m + j];
+          out[j] = (float)(v * inv);
+        }
+      } else {
+        const int qi = q - g.NM, sl = g.ic_slot[qi];
+        const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
+        const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
+        const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
+        double pa = g.P0T[(size_t)ca * R + row], pb = pa;
+        for (int j = 0; j < rt; ++j) {
+          const double bv = Bm[(size_t)j * R + row];
+          pa = fma(bv, pa_[j], pa);
+          pb = fma(bv, pb_[j], pb);
+        }
+        const double sp = g.ic_sp[qi];
+        out[0] = (float)(-sp * pa * inv);
+        out[1] = (float)(-sp * (pb - pa) * inv);
+      }
+    } else {
+      const int i2 = idx - nlo;
+      const int qj = i2 / T, t = i2 % T, q = qj / MT, j = qj % MT;
+      float v = 0.f;
+      if (q < g.NM) {
+        const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+        if (j < m) v = (float)n0_at(g, w, b, g.mb_row[st + j], t, rt, dead, nd);
+      } else if (j < 2) {
+        const int sl = g.ic_slot[q - g.NM];
+        v = j == 0 ? 1.f : ((sl >= 0 && ib[(size_t)t * g.K + sl]) ? 1.f : 0.f);
+      }
+      So[i2] = v;
+    }
+  }
 }
 
 // ---- N-0 contraction (solver.py:575-595): n0 = f0 + B'' y_t, emitted for
@@ -829,6 +838,11 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
     opted = update_dyn_bytes(RMAX, EMAX);
   }
   k_update<<<w.Wb, UT, dyn, st>>>(g, c, w);
+  if (w.NTERM > 0 && g.M > 0) {
+    const int work = g.M * (g.NM + g.NI) + w.NTERM * w.T;
+    const dim3 grid((unsigned)std::min(8, (work + NT - 1) / NT), w.Wb);
+    k_terms<<<grid, NT, 0, st>>>(g, w);
+  }
 }
 
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {

@@ -44,6 +44,10 @@ TASK_DETACHED = 6
 
 _P = ctypes.c_void_p
 
+# device-time stages of bdc_solve (include/bdc.h BDC_STAGE_*)
+STAGES = ("h2d", "update", "n0", "other_n1", "scale", "topk", "top", "screen", "select", "report", "d2h", "spare")
+N_STAGES = len(STAGES)
+
 
 class _Grid(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("R", "C0", "M", "S", "E", "K", "N1", "NM", "NMB", "NI", "NC", "NBR", "static_col")] + [
@@ -103,7 +107,7 @@ class _Batch(ctypes.Structure):
         ("n1_pairs", _P),
         ("report_cases", _P),
         ("screen", ctypes.c_int32),
-        ("stage_ms", ctypes.c_float * 8),
+        ("stage_ms", ctypes.c_float * N_STAGES),
         ("waves", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
     ]
@@ -452,7 +456,7 @@ class BatchOutput:
         self._lf = np.zeros(1, dtype=np.int64)
         self._bsdf = np.zeros(1, dtype=np.int64)
         self._pairs = np.zeros(1, dtype=np.int64)
-        self.stage_ms = [0.0] * 8
+        self.stage_ms = [0.0] * N_STAGES
         self.waves = 0
         self.kernel_launches = 0
 
