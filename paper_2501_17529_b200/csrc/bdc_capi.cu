@@ -488,8 +488,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   carve(g, (int)Wb, T, D, Ein, rs, ws.p, &w);
   w.screen = bt->screen ? 1 : 0;
   {
-    const char* pt = std::getenv("BDC_PTOP");
-    if (pt && std::atoi(pt) > 0) w.ptop = std::min(w.ptop, std::atoi(pt));
+    const char* rc = std::getenv("BDC_RSEL_CTA");
+    w.rsel_cta = (rc && rc[0] == '1') ? 1 : 0;
   }
   w.ranked = (w.screen && g.N1 > w.ptop) ? 1 : 0;
   CK(cudaMemsetAsync(w.lf, 0, 32, st));

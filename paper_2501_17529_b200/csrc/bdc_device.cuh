@@ -104,6 +104,7 @@ struct Work {
   float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
   int screen;     // 1 = exact dominance screen on
+  int rsel_cta;   // 1: winner report selection always CTA-per-task (test knob BDC_RSEL_CTA)
   int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
   float* s32;     // (Wb, N1, T)   n0[r_c][t] (pre-outage flow of each single case), FP32

@@ -185,6 +185,81 @@ __device__ __forceinline__ float pair_bound(const DevGrid& g, const Work& w, int
   return ub;
 }
 
+// One multi-branch or injection case q (q < NM: multi) of the winner, FP64, one warp:
+// lanes over monitored rows keep stable top-kc lists (entries >= the list floor),
+// merged into the warp list L with the case's order.  Updates the lane's running max.
+template <int KC>
+__device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q, int best, float theta, int kc,
+                                  int kg, WarpList& L, const double* n0b, const int* sdead, int nd,
+                                  double* sMinv, double& mymax) {
+  const int lane = threadIdx.x & 31;
+  const int R = g.R, M = g.M, T = w.T, rs = w.rs, rt = w.rank[b];
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  int order, kind = 1;
+  if (q < g.NM) {
+    order = g.mc_order[q];
+  } else {
+    kind = 2; q -= g.NM;
+    order = g.ic_order[q];
+  }
+  LaneTop<KC> lt;
+  lt.clear();
+  // entries below theta cannot reach the final top-kg (it holds the kg largest case
+  // maxima, all >= theta): a floor for the lane lists
+  const double thresh = fmax(warp_thresh(L, kg), (double)theta);
+  if (kind == 1) {
+    const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+    for (int i = lane; i < m * m; i += 32) sMinv[i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
+    __syncwarp();
+    double sv[MMAX];
+    for (int j = 0; j < m; ++j) sv[j] = n0b[g.mb_row[st + j]];
+    for (int p = lane; p < M; p += 32) {
+      const int row = g.mon_row[p];
+      if (is_dead(sdead, nd, row)) continue;
+      int own = -1;
+      for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+      double f = n0b[row];
+      if (own >= 0) {
+        for (int j = 0; j < m; ++j) f += (j == own ? -1.0 : 0.0) * sv[j];
+      } else {
+        double Dv[MMAX];
+        for (int i = 0; i < m; ++i) {
+          double v = g.Dm64[(size_t)(st + i) * R + row];
+          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+          Dv[i] = v;
+        }
+        for (int j = 0; j < m; ++j) {
+          double l = 0.0;
+          for (int i = 0; i < m; ++i) l += Dv[i] * sMinv[i * m + j];
+          f += l * sv[j];
+        }
+      }
+      const double rel = fabs(f) * g.inv_rating[p];
+      mymax = fmax(mymax, rel);
+      if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
+    }
+  } else {
+    const int sl = g.ic_slot[q];
+    const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
+    const bool bit = sl >= 0 && w.inj[((size_t)b * T + best) * g.K + sl];
+    const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * g.NI + q) * rs;
+    const double sp = g.ic_sp[q];
+    for (int p = lane; p < M; p += 32) {
+      const int row = g.mon_row[p];
+      if (is_dead(sdead, nd, row)) continue;
+      double pc = g.P0T[(size_t)ca * R + row];
+      for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
+      const double f = n0b[row] - pc * sp;
+      const double rel = fabs(f) * g.inv_rating[p];
+      mymax = fmax(mymax, rel);
+      if (rel >= thresh) lt.insert(rel, p, f);
+    }
+  }
+  warp_merge<KC>(lt, kc, L, kg, order);
+  __syncwarp();
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------- k_rsel
@@ -336,71 +411,9 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   }
 
   // ---- multi-branch and injection cases of the report (FP64, warp per case) --------------
-  LaneTop<KC> lt;
   for (int ci = N1 + wid; ci < ncase; ci += RW) {
     if (!feasible_case(ci) || !(cm[(size_t)ci * T] >= theta)) continue;
-    int order, kind = 1, q = ci - N1;
-    if (q < g.NM) {
-      order = g.mc_order[q];
-    } else {
-      kind = 2; q -= g.NM;
-      order = g.ic_order[q];
-    }
-    lt.clear();
-    // entries below theta cannot reach the final top-kg (it holds the kg largest case
-    // maxima, all >= theta): a floor for the lane lists
-    const double thresh = fmax(warp_thresh(wl[wid], kg), (double)theta);
-    if (kind == 1) {
-      const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-      for (int i = lane; i < m * m; i += 32) sMinv[wid][i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
-      __syncwarp();
-      double sv[MMAX];
-      for (int j = 0; j < m; ++j) sv[j] = n0b[g.mb_row[st + j]];
-      for (int p = lane; p < M; p += 32) {
-        const int row = g.mon_row[p];
-        if (is_dead(sdead, nd, row)) continue;
-        int own = -1;
-        for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
-        double f = n0b[row];
-        if (own >= 0) {
-          for (int j = 0; j < m; ++j) f += (j == own ? -1.0 : 0.0) * sv[j];
-        } else {
-          double Dv[MMAX];
-          for (int i = 0; i < m; ++i) {
-            double v = g.Dm64[(size_t)(st + i) * R + row];
-            const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-            for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
-            Dv[i] = v;
-          }
-          for (int j = 0; j < m; ++j) {
-            double l = 0.0;
-            for (int i = 0; i < m; ++i) l += Dv[i] * sMinv[wid][i * m + j];
-            f += l * sv[j];
-          }
-        }
-        const double rel = fabs(f) * g.inv_rating[p];
-        mymax = fmax(mymax, rel);
-        if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
-      }
-    } else {
-      const int sl = g.ic_slot[q];
-      const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
-      const bool bit = sl >= 0 && w.inj[((size_t)b * T + best) * g.K + sl];
-      const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * g.NI + q) * rs;
-      const double sp = g.ic_sp[q];
-      for (int p = lane; p < M; p += 32) {
-        const int row = g.mon_row[p];
-        if (is_dead(sdead, nd, row)) continue;
-        double pc = g.P0T[(size_t)ca * R + row];
-        for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
-        const double f = n0b[row] - pc * sp;
-        const double rel = fabs(f) * g.inv_rating[p];
-        mymax = fmax(mymax, rel);
-        if (rel >= thresh) lt.insert(rel, p, f);
-      }
-    }
-    warp_merge<KC>(lt, kc, wl[wid], kg, order);
-    __syncwarp();
+    other_case_report<KC>(g, w, b, ci - N1, best, theta, kc, kg, wl[wid], n0b, sdead, nd, sMinv[wid], mymax);
   }
   // each warp's list and max is one partial slot (merged by k_rmerge)
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
@@ -413,6 +426,167 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
     w.prel[o + e] = has ? wl[wid].rel[e] : -1.0;
   }
   if (lane == 0) w.pmax[(size_t)b * w.nslot + wid] = mymax;
+}
+
+// --------------------------------------------------------------------------- k_rsel_w
+// k_rsel for small grids (M, cases <= 32 NCW): a warp per task, RW tasks per CTA, no
+// block barriers.  The N-0 loadings and the case values live in registers; the N-0
+// top-kg and the kg-th case value are kg rounds of warp argmax (same order as k_rsel:
+// value desc, index asc); the warp's list is partial slot 0 (slots 1..RW-1 empty).
+template <int KC, int NCW>
+__global__ void __launch_bounds__(RT) k_rsel_w(DevGrid g, DevCfg cfg, Work w) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b = blockIdx.x * RW + wid;
+  __shared__ WarpList wl[RW];
+  __shared__ int sdead[RW][RMAX];
+  __shared__ double sMinv[RW][MMAX * MMAX];
+  __shared__ double sY[RW][RMAX];
+  if (b >= w.Wb || w.status[b] != 0) return;  // warp-uniform; no block barrier below
+  const int R = g.R, M = g.M, T = w.T, rs = w.rs, rt = w.rank[b];
+  const int best = (int)w.best[b];
+  const int kc = cfg.kc, kg = cfg.kg;
+  const int N1 = g.N1, ncase = N1 + g.NM + g.NI;
+  double* n0b = w.n0b + (size_t)b * R;
+  double* n0m = w.n0m + (size_t)b * M;
+  const double* Bm = w.Bm + (size_t)b * rs * R;
+  const int nd = w.ndead[b];
+  if (lane < nd) sdead[wid][lane] = w.dead[(size_t)b * RMAX + lane];
+  if (lane < rt) sY[wid][lane] = w.Y[((size_t)b * rs + lane) * T + best];
+  if (lane == 0) wl[wid].n = 0;
+  __syncwarp();
+  // the winner's N-0 column, FP64, from the factors
+  for (int r = lane; r < R; r += 32) {
+    double v = 0.0;
+    if (!is_dead(sdead[wid], nd, r)) {
+      v = g.f0[r];
+      for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + r], sY[wid][j], v);
+    }
+    n0b[r] = v;
+    const int p = g.row_mon_pos[r];
+    if (p >= 0) n0m[p] = v;
+  }
+  __syncwarp();
+  // N-0 loadings (dead rows excluded from the report, 0 in the metric)
+  double nv[NCW];
+  double mymax = 0.0;
+#pragma unroll
+  for (int k = 0; k < NCW; ++k) {
+    const int p = lane + 32 * k;
+    nv[k] = -1.0;
+    if (p < M) {
+      const double v = fabs(n0m[p]) * g.inv_rating[p];
+      mymax = fmax(mymax, v);
+      if (!is_dead(sdead[wid], nd, g.mon_row[p])) nv[k] = v;
+    }
+  }
+  // N-0 report: top-kg by (rel desc, position asc) (_top_rows, solver.py:287-299)
+  int cnt = 0;
+  for (int e = 0; e < kg; ++e) {
+    double bv = -1.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < NCW; ++k)
+      if (nv[k] >= 0.0 && better(nv[k], lane + 32 * k, bv, bi)) { bv = nv[k]; bi = lane + 32 * k; }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    if (bv < 0.0) break;
+    if (lane == 0) {
+      const double f = n0m[bi];
+      w.n0pos[(size_t)b * kg + e] = bi;
+      w.n0flow[(size_t)b * kg + e] = f;
+      w.n0rel[(size_t)b * kg + e] = fabs(f) * g.inv_rating[bi];
+    }
+#pragma unroll
+    for (int k = 0; k < NCW; ++k)
+      if (lane + 32 * k == bi) nv[k] = -1.0;
+    ++cnt;
+  }
+  if (lane == 0) w.n0cnt[b] = cnt;
+  // case values: exact FP32 maximum (or -1) and upper bound (exact, or the dominance bound)
+  const float* cm = w.cmax + (size_t)b * ncase * T + best;
+  float cv[NCW], cub[NCW];
+#pragma unroll
+  for (int k = 0; k < NCW; ++k) {
+    const int ci = lane + 32 * k;
+    cv[k] = -1.f;
+    cub[k] = -1.f;
+    if (ci >= ncase) continue;
+    bool feas;
+    if (ci < N1) feas = w.sc_ok[(size_t)b * N1 + ci] != 0;
+    else if (ci < N1 + g.NM) feas = w.mc_ok[(size_t)b * g.NM + (ci - N1)] != 0;
+    else feas = true;
+    if (!feas) continue;
+    if (ci >= N1 || pair_evaluated(g, w, b, ci, best)) {
+      cv[k] = cm[(size_t)ci * T];
+      cub[k] = cv[k];
+    } else {
+      cub[k] = pair_bound(g, w, b, ci, best);
+    }
+  }
+  // kg-th largest exact case value -> theta (k_rsel's exact pruning rule)
+  float kth = -1.f;
+  int nfound = 0;
+  {
+    float sel[NCW];
+#pragma unroll
+    for (int k = 0; k < NCW; ++k) sel[k] = cv[k];
+    for (int e = 0; e < kg; ++e) {
+      float bv = -1.f;
+      int bi = INT_MAX;
+#pragma unroll
+      for (int k = 0; k < NCW; ++k)
+        if (sel[k] >= 0.f && (sel[k] > bv || (sel[k] == bv && lane + 32 * k < bi))) { bv = sel[k]; bi = lane + 32 * k; }
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (bv < 0.f) break;
+#pragma unroll
+      for (int k = 0; k < NCW; ++k)
+        if (lane + 32 * k == bi) sel[k] = -1.f;
+      kth = bv;
+      ++nfound;
+    }
+  }
+  const float theta = nfound == kg ? kth - 2.f * SCREEN_EPS : -1.f;
+  if (lane == 0) w.theta[b] = theta;
+  // single cases to visit, ascending (cases lane + 32 k: k-major order is ascending)
+  int off = 0;
+#pragma unroll
+  for (int k = 0; k < NCW; ++k) {
+    const int ci = lane + 32 * k;
+    const bool take = ci < N1 && cub[k] >= theta && cub[k] >= 0.f;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (take) w.rlist[(size_t)b * N1 + off + __popc(bal & ((1u << lane) - 1u))] = ci;
+    off += __popc(bal);
+  }
+  if (lane == 0) {
+    w.rcnt[b] = off;
+    atomicAdd(w.lf + 3, (unsigned long long)off);
+  }
+  // multi-branch and injection cases (FP64)
+  for (int ci = N1; ci < ncase; ++ci) {
+    bool feas = ci < N1 + g.NM ? w.mc_ok[(size_t)b * g.NM + (ci - N1)] != 0 : true;
+    if (!feas || !(cm[(size_t)ci * T] >= theta)) continue;
+    other_case_report<KC>(g, w, b, ci - N1, best, theta, kc, kg, wl[wid], n0b, sdead[wid], nd, sMinv[wid], mymax);
+  }
+  for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  // slot 0: this warp's list and max; slots 1..RW-1 empty
+  for (int sl = 0; sl < RSEL_WARPS; ++sl) {
+    const size_t o = ((size_t)b * w.nslot + sl) * KMAX;
+    for (int e = lane; e < kg; e += 32) {
+      const bool has = sl == 0 && e < wl[wid].n;
+      w.pcase[o + e] = has ? wl[wid].cs[e] : INT_MAX;
+      w.ppos[o + e] = has ? wl[wid].pos[e] : INT_MAX;
+      w.pflow[o + e] = has ? wl[wid].flow[e] : 0.0;
+      w.prel[o + e] = has ? wl[wid].rel[e] : -1.0;
+    }
+    if (lane == 0) w.pmax[(size_t)b * w.nslot + sl] = sl == 0 ? mymax : 0.0;
+  }
 }
 
 // --------------------------------------------------------------------------- k_rsweep
@@ -684,7 +858,10 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
 namespace {
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
+  if (!w.rsel_cta && g.M <= 32 * 16 && g.N1 + g.NM + g.NI <= 32 * 16)
+    k_rsel_w<KC, 16><<<(w.Wb + RW - 1) / RW, RT, 0, s>>>(g, c, w);
+  else
+    k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
   if (g.N1 > 0 && g.M > 0) {
     const size_t dyn = (2 * (size_t)w.rs * SRC + 4 * (size_t)SRC) * sizeof(double);
     static bool init = false;

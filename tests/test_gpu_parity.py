@@ -245,3 +245,21 @@ def test_wave_split_is_invisible(name, sessions):
     assert np.array_equal(one.cand_metric, many.cand_metric)
     assert one.reports() == many.reports()
     assert one.loadflows == many.loadflows and one.n1_pairs == many.n1_pairs
+
+
+@pytest.mark.parametrize("name", ["fixture_a", "fixture_b", "case300", "g118"])
+def test_report_select_variants_agree(name, sessions, monkeypatch):
+    """The warp-per-task winner-report selection (small grids) and the CTA-per-task one
+    (large grids, forced here with BDC_RSEL_CTA=1) give bit-identical results."""
+    case = next(c for c in CASES if c["name"] == name)
+    sess = sessions(case)
+    arr, _ = load_case(name)
+    eng = sess.engine
+    args = (arr["splits"], arr["disconnections"], arr["injection_sets"])
+    warp = eng.solve(*args)
+    monkeypatch.setenv("BDC_RSEL_CTA", "1")
+    cta = eng.solve(*args)
+    monkeypatch.delenv("BDC_RSEL_CTA")
+    assert np.array_equal(warp.best, cta.best)
+    assert np.array_equal(warp.metric, cta.metric, equal_nan=True)
+    assert warp.reports() == cta.reports()
