@@ -864,9 +864,57 @@ void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
   else k_n0<1><<<grid, NT, dyn, st>>>(g, w);
 }
 
+// k_topk for small grids (N1 <= 32 KW): a warp per task, keys in registers, ptop rounds
+// of warp argmax by (key desc, index asc) -- the same set as k_topk's radix select.
+template <int KW>
+__global__ void __launch_bounds__(NT) k_topk_w(DevGrid g, Work w) {
+  const int lane = threadIdx.x & 31, b = blockIdx.x * NW + (threadIdx.x >> 5);
+  if (b >= w.Wb || w.status[b] != 0) return;
+  const int N1 = g.N1, P = min(w.ptop, N1);
+  const uint32_t* key = w.bkey + (size_t)b * N1;
+  uint32_t kv[KW];
+  bool take[KW];
+#pragma unroll
+  for (int k = 0; k < KW; ++k) {
+    const int c = lane + 32 * k;
+    kv[k] = c < N1 ? key[c] : 0u;
+    take[k] = false;
+  }
+  for (int e = 0; e < P; ++e) {
+    uint32_t bv = 0u;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+      const int c = lane + 32 * k;
+      if (c < N1 && !take[k] && (kv[k] > bv || (kv[k] == bv && c < bi))) { bv = kv[k]; bi = c; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const uint32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+#pragma unroll
+    for (int k = 0; k < KW; ++k)
+      if (lane + 32 * k == bi) take[k] = true;
+  }
+  uint8_t* done = w.done + (size_t)b * N1;
+  int* top = w.top + (size_t)b * w.ptop;
+  int off = 0;
+#pragma unroll
+  for (int k = 0; k < KW; ++k) {  // ascending case index (k-major)
+    const int c = lane + 32 * k;
+    if (c < N1) done[c] = take[k] ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, take[k]);
+    if (take[k]) top[off + __popc(bal & ((1u << lane) - 1u))] = c;
+    off += __popc(bal);
+  }
+  for (int i = off + lane; i < w.ptop; i += 32) top[i] = -1;
+}
+
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t st) {
   if (g.N1 == 0 || g.M == 0) return;
-  k_topk<<<w.Wb, NT, 0, st>>>(g, w);
+  if (g.N1 <= 32 * 16) k_topk_w<16><<<(w.Wb + NW - 1) / NW, NT, 0, st>>>(g, w);
+  else k_topk<<<w.Wb, NT, 0, st>>>(g, w);
 }
 
 }  // namespace bdc
