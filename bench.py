@@ -129,12 +129,14 @@ class ClockSampler:
         }
 
 
-def make_workload(name, rank, n_tasks=None):
+def make_workload(name, rank, n_tasks=None, n_cand=None):
     from paper_2501_17529_b200 import synth
 
     spec, tasks, T, k, d = WORKLOADS[name]
     if n_tasks is not None:
         tasks = n_tasks
+    if n_cand:
+        T = n_cand
     grid = synth.make_grid(spec, seed=0)
     splits, discos, inj = synth.random_task_arrays(grid, tasks, T, k, seed=1000 + rank, n_disconnections=d)
     return grid, splits, discos, inj
@@ -296,7 +298,9 @@ def run_ours(args):
     spec, tasks, T, k, d = WORKLOADS[args.config]
     if args.tasks:
         tasks = args.tasks
-    grid, splits, discos, inj = make_workload(args.config, rank, tasks)
+    if args.candidates:
+        T = args.candidates
+    grid, splits, discos, inj = make_workload(args.config, rank, tasks, T)
     sess = session_open(grid, device=local)
     eng = sess.engine
     eng.screen = not args.no_screen
@@ -500,6 +504,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="g118", choices=sorted(WORKLOADS))
     ap.add_argument("--tasks", type=int, default=0, help="override tasks per GPU per step")
+    ap.add_argument("--candidates", type=int, default=0, help="override injection candidates per task")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-screen", action="store_true", help="brute-force every (case, candidate) pair")
