@@ -8,6 +8,7 @@
 #include <memory>
 #include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -283,20 +284,39 @@ int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, 
   if (!s || (B > 0 && !splits && s->g.S > 0) || (D > 0 && B > 0 && !discos))
     return fail(BDC_EINVAL, "null argument");
   const int S = s->g.S, E = s->g.E > 0 ? s->g.E : 1;
-  int32_t mr = 0, md = 0, ma = 0;
-  for (int64_t b = 0; b < B; ++b) {
-    int k = 0, act = 0, d = 0;
-    const uint8_t* sp = splits + (size_t)b * S * E;
-    for (int si = 0; si < S; ++si) {
-      const uint8_t* e = sp + (size_t)si * E;
-      bool any = false;
-      for (int j = 0; j < E; ++j) any |= e[j] != 0;
-      if (any) { ++k; act += s->slots_per_sub[si]; }
+  // chunks of tasks on host threads (a few ms per 10^5 tasks on one core)
+  auto scan = [&](int64_t b0, int64_t b1, int32_t* out) {
+    int32_t mr = 0, md = 0, ma = 0;
+    for (int64_t b = b0; b < b1; ++b) {
+      int k = 0, act = 0, d = 0;
+      const uint8_t* sp = splits + (size_t)b * S * E;
+      for (int si = 0; si < S; ++si) {
+        const uint8_t* e = sp + (size_t)si * E;
+        bool any = false;
+        for (int j = 0; j < E; ++j) any |= e[j] != 0;
+        if (any) { ++k; act += s->slots_per_sub[si]; }
+      }
+      for (int i = 0; i < D; ++i) d += discos[(size_t)b * D + i] >= 0;
+      mr = std::max(mr, k + d);
+      md = std::max(md, d);
+      ma = std::max(ma, act);
     }
-    for (int i = 0; i < D; ++i) d += discos[(size_t)b * D + i] >= 0;
-    mr = std::max(mr, k + d);
-    md = std::max(md, d);
-    ma = std::max(ma, act);
+    out[0] = mr; out[1] = md; out[2] = ma;
+  };
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(hw, B / 8192));
+  std::vector<int32_t> res((size_t)nt * 3, 0);
+  std::vector<std::thread> th;
+  const int64_t per = (B + nt - 1) / nt;
+  for (int i = 1; i < nt; ++i)
+    th.emplace_back(scan, i * per, std::min<int64_t>(B, (i + 1) * per), &res[(size_t)i * 3]);
+  scan(0, std::min<int64_t>(B, per), &res[0]);
+  for (auto& t : th) t.join();
+  int32_t mr = 0, md = 0, ma = 0;
+  for (int i = 0; i < nt; ++i) {
+    mr = std::max(mr, res[(size_t)i * 3]);
+    md = std::max(md, res[(size_t)i * 3 + 1]);
+    ma = std::max(ma, res[(size_t)i * 3 + 2]);
   }
   if (max_rank) *max_rank = mr;
   if (max_disc) *max_disc = md;
@@ -334,6 +354,9 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   const int NCw = (g.NC + 31) / 32 > 0 ? (g.NC + 31) / 32 : 1;
   size_t o_spl = L.add(B * g.S * Ein), o_dis = L.add(B * (D > 0 ? D : 1) * 8), o_inj = L.add(B * T * (g.K > 0 ? g.K : 1));
   size_t o_tc = L.add(B * 4);
+  // a second input buffer: host inputs of wave w + 1 are copied while wave w computes
+  size_t o_spl2 = L.add(B * g.S * Ein), o_dis2 = L.add(B * (D > 0 ? D : 1) * 8), o_inj2 = L.add(B * T * (g.K > 0 ? g.K : 1));
+  size_t o_tc2 = L.add(B * 4);
   size_t o_st = L.add(B * 4), o_sa = L.add(B * 4), o_rk = L.add(B * 4), o_ns = L.add(B * 4), o_nd = L.add(B * 4);
   size_t o_dead = L.add(B * RMAX * 4), o_ss = L.add(B * RMAX * 4), o_ni = L.add(B * 4), o_isl = L.add(B * NCw * 4);
   size_t o_B = L.add(B * rs * g.R * 8), o_C = L.add(B * rs * Cs * 8);
@@ -361,7 +384,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4), o_th = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
-  size_t o_b32 = L.add(B * (size_t)rs * g.M * 4), o_bmx = L.add(B * (size_t)rs * 4);
+  size_t o_b32 = L.add(B * b32_task_floats(rs, g.M) * 4), o_bmx = L.add(B * (size_t)rs * 4);
   size_t o_smx = L.add(B * (size_t)g.N1 * 4);
   size_t o_lf = L.add(32), o_bs = L.add(16);
   if (!base) return L.total;
@@ -371,6 +394,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.discos = (const int64_t*)(base + o_dis);
   x.inj = (const uint8_t*)(base + o_inj);
   x.tcount = (const int*)(base + o_tc);
+  x.in2_splits = (const uint8_t*)(base + o_spl2);
+  x.in2_discos = (const int64_t*)(base + o_dis2);
+  x.in2_inj = (const uint8_t*)(base + o_inj2);
+  x.in2_tcount = (const int*)(base + o_tc2);
   x.status = (int*)(base + o_st); x.sarg = (int*)(base + o_sa); x.rank = (int*)(base + o_rk);
   x.nsplit = (int*)(base + o_ns); x.ndead = (int*)(base + o_nd); x.dead = (int*)(base + o_dead);
   x.splitsub = (int*)(base + o_ss); x.nisl = (int*)(base + o_ni); x.isl = (uint32_t*)(base + o_isl);
@@ -438,6 +465,15 @@ cudaError_t out_copy(T* dst, const T* src, size_t n, int64_t off, bool on_dev, c
   if (!dst || n == 0) return cudaSuccess;
   return cudaMemcpyAsync(dst + off, src, n * sizeof(T),
                          on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
+}
+
+// The wave workspace with its input pointers switched to input buffer `i` (0 or 1).
+Work in_buf(const Work& w, int i) {
+  Work x = w;
+  if (i) {
+    x.splits = w.in2_splits; x.discos = w.in2_discos; x.inj = w.in2_inj; x.tcount = w.in2_tcount;
+  }
+  return x;
 }
 
 }  // namespace
@@ -527,58 +563,100 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     const OutLayout& O = olay;
     const int64_t b0 = staged_b0[slot];
     const size_t nb = (size_t)staged_nb[slot];
-    auto put = [&](void* dst, size_t off, size_t bytes_per_task) {
-      if (dst) std::memcpy((char*)dst + b0 * bytes_per_task, hp + off, nb * bytes_per_task);
-    };
-    put(bt->metric, O.metric, 8);
-    put(bt->best, O.best, 8);
-    put(bt->feasible, O.feasible, 1);
-    put(bt->status, O.status, 4);
-    put(bt->status_arg, O.sarg, 4);
-    put(bt->n_islanded, O.nisl, 4);
-    put(bt->islanded_bits, O.isl, (size_t)NCw * 4);
-    put(bt->n0_count, O.n0cnt, 4);
-    put(bt->n1_count, O.n1cnt, 4);
-    put(bt->n0_pos, O.n0pos, (size_t)kg * 4);
-    put(bt->n0_flow, O.n0flow, (size_t)kg * 8);
-    put(bt->n1_case, O.n1case, (size_t)kg * 4);
-    put(bt->n1_pos, O.n1pos, (size_t)kg * 4);
-    put(bt->n1_flow, O.n1flow, (size_t)kg * 8);
-    if (bt->cand_metric) put(bt->cand_metric, O.cand, (size_t)T * 4);
     const double* inv = s->inv_rating.data();
     const int M = (int)s->inv_rating.size();
-    auto rel = [&](double* dst, size_t pos_off, size_t flow_off) {
-      if (!dst) return;
-      const int32_t* pos = (const int32_t*)(hp + pos_off);
-      const double* fl = (const double*)(hp + flow_off);
-      double* d = dst + b0 * kg;
-      for (size_t i = 0; i < nb * (size_t)kg; ++i) {
-        const int p = pos[i];
-        d[i] = (p >= 0 && p < M) ? std::fabs(fl[i]) * inv[p] : 0.0;
-      }
+    // tasks [t0, t1) of the staged wave into the caller's arrays (first-touch page faults
+    // and copies dominate for large waves: a few host threads share them)
+    auto part = [&](size_t t0, size_t t1) {
+      auto put = [&](void* dst, size_t off, size_t bpt) {
+        if (dst) std::memcpy((char*)dst + (b0 + t0) * bpt, hp + off + t0 * bpt, (t1 - t0) * bpt);
+      };
+      put(bt->metric, O.metric, 8);
+      put(bt->best, O.best, 8);
+      put(bt->feasible, O.feasible, 1);
+      put(bt->status, O.status, 4);
+      put(bt->status_arg, O.sarg, 4);
+      put(bt->n_islanded, O.nisl, 4);
+      put(bt->islanded_bits, O.isl, (size_t)NCw * 4);
+      put(bt->n0_count, O.n0cnt, 4);
+      put(bt->n1_count, O.n1cnt, 4);
+      put(bt->n0_pos, O.n0pos, (size_t)kg * 4);
+      put(bt->n0_flow, O.n0flow, (size_t)kg * 8);
+      put(bt->n1_case, O.n1case, (size_t)kg * 4);
+      put(bt->n1_pos, O.n1pos, (size_t)kg * 4);
+      put(bt->n1_flow, O.n1flow, (size_t)kg * 8);
+      if (bt->cand_metric) put(bt->cand_metric, O.cand, (size_t)T * 4);
+      auto rel = [&](double* dst, size_t pos_off, size_t flow_off) {
+        if (!dst) return;
+        const int32_t* pos = (const int32_t*)(hp + pos_off);
+        const double* fl = (const double*)(hp + flow_off);
+        double* d = dst + b0 * kg;
+        for (size_t i = t0 * kg; i < t1 * (size_t)kg; ++i) {
+          const int p = pos[i];
+          d[i] = (p >= 0 && p < M) ? std::fabs(fl[i]) * inv[p] : 0.0;
+        }
+      };
+      rel(bt->n0_rel, O.n0pos, O.n0flow);
+      rel(bt->n1_rel, O.n1pos, O.n1flow);
     };
-    rel(bt->n0_rel, O.n0pos, O.n0flow);
-    rel(bt->n1_rel, O.n1pos, O.n1flow);
+    const unsigned hw = std::max(1u, std::min(4u, std::thread::hardware_concurrency()));
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(hw, nb / 4096));
+    const size_t per = (nb + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (size_t i = 1; i < nt; ++i) th.emplace_back(part, i * per, std::min(nb, (i + 1) * per));
+    part(0, std::min(nb, per));
+    for (auto& t : th) t.join();
     return cudaSuccess;
+  };
+  // host inputs with several waves: copies on their own stream into two input buffers
+  const bool overlap_in = !ondev_in && nwaves > 1;
+  StreamGuard cs;
+  cudaEvent_t in_ready[2] = {nullptr, nullptr}, buf_free[2] = {nullptr, nullptr};
+  struct EvGuard4 {
+    cudaEvent_t* a; cudaEvent_t* b;
+    ~EvGuard4() { for (int i = 0; i < 2; ++i) { if (a[i]) cudaEventDestroy(a[i]); if (b[i]) cudaEventDestroy(b[i]); } }
+  } evg4{in_ready, buf_free};
+  if (overlap_in) {
+    CK(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+    cs.own = true;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&buf_free[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(buf_free[0], st));  // the caller's prior work on st precedes the copies
+    CK(cudaStreamWaitEvent(cs.s, buf_free[0], 0));
+  }
+  const cudaMemcpyKind hk = ondev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const size_t sz_spl = (size_t)g.S * Ein, sz_inj = (size_t)T * g.K;
+  // inputs of wave v into x's buffers on stream q (records in_ready when overlapping)
+  auto copy_inputs = [&](const Work& x, int v, cudaStream_t q) -> cudaError_t {
+    const int64_t v0 = (int64_t)v * Wb;
+    const size_t m = (size_t)std::min<int64_t>(Wb, B - v0);
+    cudaError_t e = cudaSuccess;
+    if (sz_spl) e = cudaMemcpyAsync((void*)x.splits, bt->splits + v0 * sz_spl, m * sz_spl, hk, q);
+    if (e == cudaSuccess && D > 0)
+      e = cudaMemcpyAsync((void*)x.discos, bt->discos + v0 * D, m * D * 8, hk, q);
+    if (e == cudaSuccess && sz_inj) e = cudaMemcpyAsync((void*)x.inj, bt->inj + v0 * sz_inj, m * sz_inj, hk, q);
+    if (e == cudaSuccess && bt->t_count)
+      e = cudaMemcpyAsync((void*)x.tcount, bt->t_count + v0, m * 4, hk, q);
+    if (e == cudaSuccess && overlap_in) e = cudaEventRecord(in_ready[v & 1], q);
+    return e;
   };
   int launches = 0;
   cudaError_t err = cudaSuccess;
   for (int wv = 0; wv < nwaves && err == cudaSuccess; ++wv) {
     const int64_t b0 = (int64_t)wv * Wb;
     const int nb = (int)std::min<int64_t>(Wb, B - b0);
-    Work x = w;
+    Work x = in_buf(w, wv & 1);
     x.Wb = nb;
     cudaEvent_t* E = &ev[(size_t)wv * NE];
     cudaEventRecord(E[0], st);
-    const cudaMemcpyKind hk = ondev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    const size_t sz_spl = (size_t)g.S * Ein, sz_inj = (size_t)T * g.K;
-    if (sz_spl) err = cudaMemcpyAsync((void*)x.splits, bt->splits + b0 * sz_spl, nb * sz_spl, hk, st);
-    if (err == cudaSuccess && D > 0)
-      err = cudaMemcpyAsync((void*)x.discos, bt->discos + b0 * D, (size_t)nb * D * 8, hk, st);
-    if (err == cudaSuccess && sz_inj)
-      err = cudaMemcpyAsync((void*)x.inj, bt->inj + b0 * sz_inj, nb * sz_inj, hk, st);
-    if (err == cudaSuccess && bt->t_count)
-      err = cudaMemcpyAsync((void*)x.tcount, bt->t_count + b0, (size_t)nb * 4, hk, st);
+    if (!overlap_in) {
+      err = copy_inputs(x, wv, st);
+    } else {
+      if (wv == 0) err = copy_inputs(x, 0, cs.s);
+      if (err == cudaSuccess) err = cudaStreamWaitEvent(st, in_ready[wv & 1], 0);
+    }
     if (!bt->t_count) x.tcount = nullptr;
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
@@ -586,6 +664,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.lcnt, 0, (size_t)nb * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
+    // zero padding of the tensor-core operand (rank slots past the task's rank, rows past M)
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.B32, 0, (size_t)nb * b32_task_floats(rs, g.M) * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
     // stage_ms (bdc.h BDC_STAGE_*): 0 h2d, 1 update, 2 N-0, 3 multi/injection N-1,
@@ -603,6 +683,13 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     cudaEventRecord(E[9], st);
     launch_report(g, s->cfg, x, st);
     cudaEventRecord(E[10], st);
+    if (overlap_in && wv + 1 < nwaves) {
+      // the next wave's inputs go into the other buffer once wave wv - 1 is done with it
+      cudaEventRecord(buf_free[wv & 1], st);
+      if (wv >= 1) cudaStreamWaitEvent(cs.s, buf_free[(wv + 1) & 1], 0);
+      Work nx = in_buf(w, (wv + 1) & 1);
+      if (err == cudaSuccess) err = copy_inputs(nx, wv + 1, cs.s);
+    }
     launches += kernels_per_wave(g, x);
     err = cudaGetLastError();
     if (err != cudaSuccess) break;

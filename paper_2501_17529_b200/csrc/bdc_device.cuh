@@ -30,6 +30,18 @@ constexpr int TOPC = 16;
 constexpr int SB = 4;
 // Candidates per TOP-tile CTA (bdc_single.cu launch_top).
 __host__ __device__ inline int top_tile_cands(int T) { return T >= 96 ? 128 : (T >= 48 ? 64 : 32); }
+// B32 (k_n0 writes, k_scale_tc reads): per task, 64-row chunks of the monitored rows; each
+// chunk holds KB blocks of the UMMA K-major no-swizzle core-matrix layout (64 rows x 8 TF32
+// values = 2 KB: 8-row x 16-byte core matrices, K halves at +128 B, row groups at +256 B),
+// so the tensor-core kernel stages a chunk with contiguous 16-byte copies.
+__host__ __device__ inline int b32_kb(int rs) { return rs <= 8 ? 1 : (rs <= 16 ? 2 : 4); }
+__host__ __device__ inline size_t b32_task_floats(int rs, int M) {
+  return (size_t)((M + 63) / 64) * b32_kb(rs) * 512;
+}
+__host__ __device__ inline size_t b32_off(int rs, int m, int j) {  // in floats
+  const int ch = m >> 6, r = m & 63, kb = j >> 3, jj = j & 7;
+  return ((size_t)ch * b32_kb(rs) + kb) * 512 + (size_t)((r >> 3) * 64 + (jj >> 2) * 32 + (r & 7) * 4 + (jj & 3));
+}
 // Rows per screening block: a multiple of 32 (the k_scale epilogue's row half, also a
 // multiple of the k_n0 row group), so neither straddles two blocks; block of m = m / MB.
 __host__ __device__ inline int screen_block_rows(int M) {
@@ -72,6 +84,7 @@ struct Work {
   const int64_t* discos;   // (Wb, D)
   const uint8_t* inj;      // (Wb, T, K)
   const int* tcount;       // (Wb) or null
+  const uint8_t* in2_splits; const int64_t* in2_discos; const uint8_t* in2_inj; const int* in2_tcount;  // 2nd input buffer
   // per-task scalars
   int* status; int* sarg; int* rank; int* nsplit; int* ndead; int* dead;  // dead: (Wb, RMAX)
   int* splitsub;  // (Wb, RMAX) substation of split j
@@ -100,7 +113,8 @@ struct Work {
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
   float* scale;   // (Wb, SB, N1)  FP32 upper bound of max_{r in block} |LODF(r,c)|/rating_r
-  float* B32;     // (Wb, rs, M)   FP32 B''/rating on monitored rows, 0 on dead rows (k_scale)
+  float* B32;     // (Wb, b32_task_floats) FP32 B''/rating on monitored rows, 0 on dead rows,
+                  //               in the tensor-core operand layout (b32_off)
   float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
   int screen;     // 1 = exact dominance screen on

@@ -184,12 +184,15 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
       const bool ok = c0 + i < N1 && m0 + q < g.Mp;
       cp16(&D[i * SD_LD + q], ok ? &g.DsT[(size_t)(c0 + i) * g.Mp + m0 + q] : g.DsT, ok);
     }
+    // B operands: the chunk's KB operand blocks of every task, already in the core-matrix
+    // layout in global memory (k_n0, b32_off): contiguous 16-byte copies
     unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
-    for (int idx = tid; idx < TB * KB * 8 * SM_ROWS; idx += NT) {
-      const int r = idx % SM_ROWS, jj = (idx / SM_ROWS) % 8, kb = (idx / (SM_ROWS * 8)) % KB, k = idx / (SM_ROWS * 8 * KB);
-      const int j = kb * 8 + jj, m = m0 + r;
-      const bool ok = srt[k] >= 0 && j < srt[k] && m < M;
-      cp4(Bt + (k * KB + kb) * BBYTES + core_off(r, jj), ok ? &w.B32[((size_t)(tb0 + k) * rs + j) * M + m] : w.B32, ok);
+    const size_t tf = b32_task_floats(rs, M);
+    for (int idx = tid; idx < TB * KB * (BBYTES / 16); idx += NT) {
+      const int q = idx % (BBYTES / 16), kb = (idx / (BBYTES / 16)) % KB, k = idx / ((BBYTES / 16) * KB);
+      const bool ok = srt[k] >= 0;
+      const float* src = w.B32 + (size_t)(tb0 + k) * tf + ((size_t)ch * KB + kb) * 512 + 4 * q;
+      cp16(Bt + (k * KB + kb) * BBYTES + 16 * q, ok ? src : w.B32, ok);
     }
     cp_commit();
   };

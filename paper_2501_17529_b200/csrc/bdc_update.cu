@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
       sB[j * N0_ROWS + i] = bv;
       if (li < M) {
         // FP32 B'' on monitored rows and max_r |B''(r,j)|/rating_r for the scale bound
-        w.B32[((size_t)b * rs + j) * M + li] = live ? (float)(bv * scl) : 0.f;
+        w.B32[(size_t)b * b32_task_floats(rs, M) + b32_off(rs, li, j)] = live ? (float)(bv * scl) : 0.f;
         w.Bmon[((size_t)b * rs + j) * M + li] = bv;
         if (live)
           atomicMax(reinterpret_cast<unsigned*>(&w.bmax[(size_t)b * rs + j]),

@@ -436,23 +436,25 @@ class BatchOutput:
         self.engine = eng
         self.B, self.T, self.kg = B, T, kg
         self.splits, self.discos, self.inj = splits, discos, inj
-        self.metric = np.full(B, np.nan)
-        self.best = np.full(B, -1, dtype=np.int64)
-        self.feasible = np.zeros(B, dtype=np.uint8)
-        self.status = np.zeros(B, dtype=np.int32)
-        self.status_arg = np.zeros(B, dtype=np.int32)
-        self.n_islanded = np.zeros(B, dtype=np.int32)
-        self.islanded_bits = np.zeros((B, ncw), dtype=np.uint32)
-        self.n0_count = np.zeros(B, dtype=np.int32)
-        self.n0_pos = np.zeros((B, kg), dtype=np.int32)
-        self.n0_flow = np.zeros((B, kg))
-        self.n0_rel = np.zeros((B, kg))
-        self.n1_count = np.zeros(B, dtype=np.int32)
-        self.n1_case = np.zeros((B, kg), dtype=np.int32)
-        self.n1_pos = np.zeros((B, kg), dtype=np.int32)
-        self.n1_flow = np.zeros((B, kg))
-        self.n1_rel = np.zeros((B, kg))
-        self.cand_metric = np.zeros((B, T), dtype=np.float32) if want_candidates else None
+        # every element is written by bdc_solve (report rows past their count are scratch);
+        # np.empty keeps the host allocation off the e2e path
+        self.metric = np.empty(B)
+        self.best = np.empty(B, dtype=np.int64)
+        self.feasible = np.empty(B, dtype=np.uint8)
+        self.status = np.empty(B, dtype=np.int32)
+        self.status_arg = np.empty(B, dtype=np.int32)
+        self.n_islanded = np.empty(B, dtype=np.int32)
+        self.islanded_bits = np.empty((B, ncw), dtype=np.uint32)
+        self.n0_count = np.empty(B, dtype=np.int32)
+        self.n0_pos = np.empty((B, kg), dtype=np.int32)
+        self.n0_flow = np.empty((B, kg))
+        self.n0_rel = np.empty((B, kg))
+        self.n1_count = np.empty(B, dtype=np.int32)
+        self.n1_case = np.empty((B, kg), dtype=np.int32)
+        self.n1_pos = np.empty((B, kg), dtype=np.int32)
+        self.n1_flow = np.empty((B, kg))
+        self.n1_rel = np.empty((B, kg))
+        self.cand_metric = np.empty((B, T), dtype=np.float32) if want_candidates else None
         self._lf = np.zeros(1, dtype=np.int64)
         self._bsdf = np.zeros(1, dtype=np.int64)
         self._pairs = np.zeros(1, dtype=np.int64)

@@ -1,4 +1,5 @@
-timeout 180 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
-timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+set -u
+timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 bash scripts/gpu_test_bench.sh "g118 g1k g3k" skip
-bash scripts/launches.sh tc1 g118 g1k g3k
+timeout 300 python scripts/e2e_breakdown.py g118 2>&1 | tail -3
+bash scripts/launches.sh b32 g1k g3k 2>&1 | grep -E "k_scale|launch list"
