@@ -67,29 +67,6 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
     sRowC[cc] = c >= 0 ? g.sc_row[c] : -1;
   }
   __syncthreads();
-  for (int idx = tid; idx < NC * rt; idx += NTH) {
-    const int cc = idx / rt, j = idx % rt, c = sCase[cc];
-    sW[j * NC + cc] = c >= 0 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
-  }
-
-  // s(c,t) = n0[r_c][t] (FP32, from k_n0) and the accumulators
-  float acc[CPT][TPT], sv[CPT][TPT];
-  int cnt = 0;
-#pragma unroll
-  for (int i = 0; i < CPT; ++i) {
-    const int c = sCase[tx * CPT + i];
-#pragma unroll
-    for (int jj = 0; jj < TPT; ++jj) {
-      const int t = t0 + ty * TPT + jj;
-      sv[i][jj] = (c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
-      acc[i][jj] = 0.f;
-      cnt += c >= 0 && t < T;
-    }
-  }
-  // evaluated (case, candidate) pairs, for the roofline accounting
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((tid & 31) == 0 && cnt) atomicAdd(w.pairs, (unsigned long long)cnt);
-
   // ---- stage one row chunk (async): row ids + 1/rating, B'' rows, n0/rating, D_base
   auto issue = [&](int m0, int buf) {
     for (int rr = tid; rr < RC; rr += NTH) {
@@ -134,7 +111,30 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
     cp_commit();
   };
 
-  issue(0, 0);
+  issue(0, 0);  // the first chunk is in flight while the tile's factors load
+  for (int idx = tid; idx < NC * rt; idx += NTH) {
+    const int cc = idx / rt, j = idx % rt, c = sCase[cc];
+    sW[j * NC + cc] = c >= 0 ? w.Wsc[((size_t)b * N1 + c) * rs + j] : 0.0;
+  }
+
+  // s(c,t) = n0[r_c][t] (FP32, from k_n0) and the accumulators
+  float acc[CPT][TPT], sv[CPT][TPT];
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = sCase[tx * CPT + i];
+#pragma unroll
+    for (int jj = 0; jj < TPT; ++jj) {
+      const int t = t0 + ty * TPT + jj;
+      sv[i][jj] = (c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
+      acc[i][jj] = 0.f;
+      cnt += c >= 0 && t < T;
+    }
+  }
+  // evaluated (case, candidate) pairs, for the roofline accounting
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((tid & 31) == 0 && cnt) atomicAdd(w.pairs, (unsigned long long)cnt);
+
   const int nchunks = (M + RC - 1) / RC;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int buf = ch & 1;
@@ -179,13 +179,15 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
       }
     }
     __syncthreads();
-    const int rend = min(RC, M - ch * RC);
-    if (rend == RC) {
+    // rows past M were staged as zero rows (n0' = 0, L' = 0): they add |0| to the maxima,
+    // so the last chunk runs the same paired loop over an even row count
+    const int rend = min(RC, (M - ch * RC + 1) & ~1);
+    {
       // two rows x two candidates per step: FFMA2 (packed FP32 FMA, same rounding as
       // fmaf) and one FMNMX3 (|.| on every input) per accumulator
       static_assert(TPT % 2 == 0, "candidate pairs");
 #pragma unroll 2
-      for (int rr = 0; rr < RC; rr += 2) {
+      for (int rr = 0; rr < rend; rr += 2) {
         float2 l2[2][CPT], n2[2][TPT / 2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -208,19 +210,6 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
             acc[i][2 * p] = max3abs(acc[i][2 * p], f0.x, f1.x);
             acc[i][2 * p + 1] = max3abs(acc[i][2 * p + 1], f0.y, f1.y);
           }
-      }
-    } else {
-      for (int rr = 0; rr < rend; ++rr) {
-        float l[CPT], n[TPT];
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) l[i] = sL[rr][tx * CPT + i];
-#pragma unroll
-        for (int jj = 0; jj < TPT; ++jj) n[jj] = SN(buf, rr, ty * TPT + jj);
-#pragma unroll
-        for (int i = 0; i < CPT; ++i)
-#pragma unroll
-          for (int jj = 0; jj < TPT; ++jj)
-            acc[i][jj] = fmaxf(acc[i][jj], fabsf(fmaf(l[i], sv[i][jj], n[jj])));
       }
     }
     __syncthreads();
