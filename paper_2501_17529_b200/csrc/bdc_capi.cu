@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <cstdlib>
+#include <cudaTypedefs.h>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -50,6 +51,7 @@ size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 struct BdcSession {
+  alignas(64) CUtensorMap tm_ds{};  // TMA descriptor of the screening table DsT
   int device = 0;
   DevGrid g{};
   DevCfg cfg{};
@@ -226,7 +228,26 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
       for (int p = 0; p < G->M; ++p)
         ds[(size_t)c * g.Mp + p] = (float)(G->D64[(size_t)c * G->R + G->mon_row[p]] * (1.0 / G->rating[p]));
     e = upload(ds.data(), ds.size(), &g.DsT, o);
+    if (e == cudaSuccess) {
+      // TMA descriptor: dim 0 = monitored rows (contiguous), dim 1 = cases; boxes of
+      // 32 rows x 128 cases with the 128-byte swizzle; out-of-range elements read as 0
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+      if (e == cudaSuccess && (fn == nullptr || q != cudaDriverEntryPointSuccess)) e = cudaErrorNotSupported;
+      if (e == cudaSuccess) {
+        const cuuint64_t dims[2] = {(cuuint64_t)g.Mp, (cuuint64_t)G->N1};
+        const cuuint64_t strides[1] = {(cuuint64_t)g.Mp * sizeof(float)};
+        const cuuint32_t box[2] = {32, 128}, estr[2] = {1, 1};
+        const CUresult r = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
+            &s->tm_ds, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)g.DsT, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) e = cudaErrorInvalidValue;
+      }
+    }
   }
+  g.tm_ds = &s->tm_ds;
   // D_base on monitored rows, case-major, for the winner report's coalesced sweeps
   if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
     std::vector<double> dm((size_t)G->N1 * G->M);

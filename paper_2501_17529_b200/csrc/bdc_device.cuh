@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/bdc.h"
@@ -60,6 +61,7 @@ struct DevGrid {
   const double *sc_delta, *sc_dscale, *D64, *Dm64, *ic_sp;
   const double* DM64;  // (N1, M) D_base on monitored rows, case-major (winner report)
   const float* DsT;    // (N1, Mp) D_base / rating on monitored rows, case-major, FP32 (k_scale)
+  const CUtensorMap* tm_ds;  // host pointer: TMA descriptor of DsT (box 32 rows x 128 cases, 128B swizzle)
   int Mp;              // M rounded up to a multiple of 4
   const float* D32;
   const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;

@@ -23,6 +23,8 @@
 // tasks); one elected thread issues the MMAs and commits them to an mbarrier.
 #include "bdc_device.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
 
 namespace bdc {
@@ -31,7 +33,7 @@ namespace {
 
 constexpr int SM_CASES = 128;  // UMMA M
 constexpr int SM_ROWS = 64;    // UMMA N: monitored rows per chunk
-constexpr int SD_LD = SM_ROWS + 4;  // padded row length of the staged D' tile (floats)
+constexpr int DT_BYTES = SM_CASES * 32 * 4;  // one TMA tile of D': 128 cases x 32 rows FP32
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
@@ -96,7 +98,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // 32-row half of every 64-row chunk.  The D' tile and the B operands of chunk ch + 1 are
 // in flight (cp.async, double buffer) while chunk ch is multiplied and reduced.
 template <int TB, int KB>
-__global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w) {
+__global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
+                                                               const __grid_constant__ CUtensorMap tmD) {
   constexpr int NT = 2 * SM_CASES;
   constexpr int TCOLS = TB * SM_ROWS;  // TMEM columns: one accumulator per task
   constexpr int NCOLS = TCOLS <= 32 ? 32 : (TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : 256));
@@ -107,11 +110,15 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
   const int tb0 = blockIdx.y * TB;
   const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
   const int MB = screen_block_rows(M);
-  extern __shared__ __align__(1024) unsigned char ssm[];
-  unsigned char* sA = ssm;                            // [TB][KB] A tiles
+  extern __shared__ __align__(1024) unsigned char ssm_raw[];
+  // the 128-byte swizzle repeats every 1024 bytes: the tiles start on a 1024-byte boundary
+  unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
+  // [2 buffers][2 row halves] TMA tiles of D' (128 cases x 32 rows, 128-byte swizzle)
+  float* sD = reinterpret_cast<float*>(ssm);
+  unsigned char* sA = ssm + 4 * DT_BYTES;             // [TB][KB] A tiles
   unsigned char* sBt = sA + TB * KB * ABYTES;         // [2][TB][KB] B tiles
-  float* sD = reinterpret_cast<float*>(sBt + 2 * TB * KB * BBYTES);  // [2][128 cases][SD_LD]
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar;              // MMA completion
+  __shared__ __align__(8) uint64_t full[2];           // TMA completion per buffer
   __shared__ uint32_t tmem_base;
   __shared__ int sdead[TB][RMAX];
   __shared__ int snd[TB], srt[TB];
@@ -124,6 +131,8 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&full[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&full[1])));
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
   if (tid < TB) {
@@ -174,27 +183,35 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
       ownloose |= fabs(1.0 - den) > 0.999 * fabs(den);
     }
 
-  // stage chunk ch into buffer bf: D' tile (cp16) and B operands (cp4 into the core-matrix
-  // layout; fp32 bits, which the tf32 MMA truncates: <= 2^-10 relative)
+  // stage chunk ch into buffer bf (thread 0): two TMA tensor tiles of D' (rows x cases,
+  // zero-filled out of bounds) and the tasks' B operand blocks as bulk copies (already in
+  // the core-matrix layout, b32_off), all completing on full[bf]
+  const size_t tf = b32_task_floats(rs, M);
+  int nvalid = 0;
+  for (int k = 0; k < TB; ++k) nvalid += srt[k] >= 0;
   auto issue = [&](int ch, int bf) {
     const int m0 = ch * SM_ROWS;
-    float* D = sD + bf * SM_CASES * SD_LD;
-    for (int idx = tid; idx < SM_CASES * (SM_ROWS / 4); idx += NT) {
-      const int i = idx / (SM_ROWS / 4), q = 4 * (idx % (SM_ROWS / 4));
-      const bool ok = c0 + i < N1 && m0 + q < g.Mp;
-      cp16(&D[i * SD_LD + q], ok ? &g.DsT[(size_t)(c0 + i) * g.Mp + m0 + q] : g.DsT, ok);
-    }
-    // B operands: the chunk's KB operand blocks of every task, already in the core-matrix
-    // layout in global memory (k_n0, b32_off): contiguous 16-byte copies
+    const uint32_t bar = smem_u32(&full[bf]);
+    const uint32_t bytes = 2u * DT_BYTES + (uint32_t)(nvalid * KB * BBYTES);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    for (int h = 0; h < 2; ++h)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+              smem_u32(sD + (bf * 2 + h) * (DT_BYTES / 4))),
+          "l"(&tmD), "r"(m0 + 32 * h), "r"(c0), "r"(bar)
+          : "memory");
     unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
-    const size_t tf = b32_task_floats(rs, M);
-    for (int idx = tid; idx < TB * KB * (BBYTES / 16); idx += NT) {
-      const int q = idx % (BBYTES / 16), kb = (idx / (BBYTES / 16)) % KB, k = idx / ((BBYTES / 16) * KB);
-      const bool ok = srt[k] >= 0;
-      const float* src = w.B32 + (size_t)(tb0 + k) * tf + ((size_t)ch * KB + kb) * 512 + 4 * q;
-      cp16(Bt + (k * KB + kb) * BBYTES + 16 * q, ok ? src : w.B32, ok);
+    for (int k = 0; k < TB; ++k) {
+      if (srt[k] < 0) continue;
+      for (int kb = 0; kb < KB; ++kb) {
+        const float* src = w.B32 + (size_t)(tb0 + k) * tf + ((size_t)ch * KB + kb) * 512;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_u32(Bt + (k * KB + kb) * BBYTES)),
+            "l"(src), "r"(BBYTES), "r"(bar)
+            : "memory");
+      }
     }
-    cp_commit();
   };
 
   const int nchunks = (M + SM_ROWS - 1) / SM_ROWS;
@@ -215,21 +232,16 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
       mx[k] = 0.f;
     }
   };
-  issue(0, 0);
+  if (tid == 0) issue(0, 0);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = tmem_base;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int bf = ch & 1;
-    if (ch + 1 < nchunks) {
-      issue(ch + 1, bf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncthreads();
+    // the other buffer was released at the end of the previous chunk
+    if (tid == 0 && ch + 1 < nchunks) issue(ch + 1, bf ^ 1);
+    mbar_wait(&full[bf], (ch >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     if (tid == 0) {
       const unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
@@ -253,12 +265,14 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
         flush();
         curblk = blk;
       }
-      const float* D = sD + bf * SM_CASES * SD_LD + ci * SD_LD + wg * 32;
+      // this thread's 32 rows of its case: one 128-byte row of the swizzled TMA tile
+      // (16-byte chunk q lives at chunk q ^ (case & 7))
+      const float* D = sD + (bf * 2 + wg) * (DT_BYTES / 4) + ci * 32;
       float dv[32];
 #pragma unroll
-      for (int q = 0; q < 32; q += 4) {
-        const float4 v4 = *reinterpret_cast<const float4*>(&D[q]);
-        dv[q] = v4.x; dv[q + 1] = v4.y; dv[q + 2] = v4.z; dv[q + 3] = v4.w;
+      for (int q = 0; q < 8; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(&D[4 * (q ^ (ci & 7))]);
+        dv[4 * q] = v4.x; dv[4 * q + 1] = v4.y; dv[4 * q + 2] = v4.z; dv[4 * q + 3] = v4.w;
       }
       const int ownq = ownp - r0;
       const bool ownin = ownloose && ownq >= 0 && ownq < 32;
@@ -348,8 +362,8 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w)
 namespace {
 template <int TB, int KB>
 void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
-  size_t dyn = (size_t)TB * KB * (SM_CASES + 2 * SM_ROWS) * 32 + 2 * (size_t)SM_CASES * SD_LD * 4;
-  static_assert(SB * 4 * SM_CASES <= 2 * SM_CASES * SD_LD, "block maxima fit the D' buffer");
+  size_t dyn = 1024 + 4 * (size_t)DT_BYTES + (size_t)TB * KB * (SM_CASES + 2 * SM_ROWS) * 32;
+  static_assert(SB * 4 * SM_CASES * 4 <= 4 * DT_BYTES, "block maxima fit the D' buffers");
   // at most 512 / NCOLS CTAs per SM fit their TMEM columns: size the shared memory so
   // that no more are resident (a CTA spinning in tcgen05.alloc would hold an SM slot)
   const int ncols = TB * SM_ROWS <= 64 ? 64 : (TB * SM_ROWS <= 128 ? 128 : 256);
@@ -360,7 +374,7 @@ void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
     init = true;
   }
   const dim3 grid((g.N1 + SM_CASES - 1) / SM_CASES, (w.Wb + TB - 1) / TB);
-  k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, w);
+  k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, w, *g.tm_ds);
 }
 }  // namespace
 

@@ -1,4 +1,5 @@
 set -u
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 bash scripts/gpu_test_bench.sh "g118 g1k g3k" skip
-bash scripts/launches.sh tp g118 g1k g3k 2>&1 | grep -E "k_top<|k_pairs|launch list"
+bash scripts/launches.sh tma g118 g1k g3k 2>&1 | grep -E "k_scale|launch list"
