@@ -46,6 +46,8 @@ struct UpdShared {
   double ssign[EMAX], sw[EMAX];
   double den;
   double sCa[RMAX];          // C[i][a]
+  double coefC[RMAX];        // sum_m sign_m B_i[row_m]            (coupler row of split j)
+  double coefB[RMAX];        // sum_st w_st (C_i[far_st] - C_i[a]) (numerator of split j)
   double inner[MMAX * MMAX];
   double mA[UW][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
   double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
@@ -196,15 +198,20 @@ __global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w)
     }
     __syncthreads();
     // coupler row over every current column: c[col] = sum_moved sign * P_{j-1}[row, col]
+    //   = sum_m sign_m P0[row_m, base(col)] + sum_i (sum_m sign_m B_i[row_m]) C_i[col]:
+    // the rank-i coefficients once per split, then j (not nm * j) loads of C per column
+    for (int i = tid; i < j; i += UT) {
+      double cf = 0.0;
+      for (int m = 0; m < nm; ++m) cf += s.msign[m] * MB(m, i);
+      s.coefC[i] = cf;
+    }
+    __syncthreads();
     const int ncols = C0 + j;
     for (int col = tid; col < ncols; col += UT) {
       const int bc = base_col(g, s, col);
       double c = 0.0;
-      for (int m = 0; m < nm; ++m) {
-        double v = g.P0[(size_t)s.mrow[m] * C0 + bc];
-        for (int i = 0; i < j; ++i) v = fma(MB(m, i), Cm[(size_t)i * Cs + col], v);
-        c += s.msign[m] * v;
-      }
+      for (int m = 0; m < nm; ++m) c += s.msign[m] * g.P0[(size_t)s.mrow[m] * C0 + bc];
+      for (int i = 0; i < j; ++i) c = fma(s.coefC[i], Cm[(size_t)i * Cs + col], c);
       Cm[(size_t)j * Cs + col] = c;
     }
     // the new busbar column starts as a copy of column a for every earlier term
@@ -225,19 +232,26 @@ __global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w)
     }
     __syncthreads();
     if (s.fail) goto done;
+    // numerator num[r] = sum_st w_st (P_{j-1}[r, far_st] - P_{j-1}[r, a]) (+ own rows)
+    //   = sum_st w_st (P0[r, base(far_st)] - P0[r, a]) + sum_i B_i[r] coefB_i,
+    //   coefB_i = sum_st w_st (C_i[far_st] - C_i[a]): j loads of B per row, not (nst+1) j
+    for (int i = tid; i < j; i += UT) {
+      double cf = 0.0;
+      for (int st = 0; st < nst; ++st) cf += s.sw[st] * (SCF(st, i) - s.sCa[i]);
+      s.coefB[i] = cf;
+    }
+    __syncthreads();
     {
       const double den = s.den;
       for (int r = tid; r < R; r += UT) {
-        double pa = g.P0T[(size_t)a * R + r];
-        for (int i = 0; i < j; ++i) pa = fma(Bm[(size_t)i * R + r], s.sCa[i], pa);
+        const double p0a = g.P0T[(size_t)a * R + r];
         double num = 0.0;
         for (int st = 0; st < nst; ++st) {
           const int bf = base_col(g, s, s.sfar[st]);
-          double pf = g.P0T[(size_t)bf * R + r];
-          for (int i = 0; i < j; ++i) pf = fma(Bm[(size_t)i * R + r], SCF(st, i), pf);
-          num += s.sw[st] * (pf - pa);
+          num += s.sw[st] * (g.P0T[(size_t)bf * R + r] - p0a);
           if (r == s.srow[st]) num += s.ssign[st] * s.sw[st];
         }
+        for (int i = 0; i < j; ++i) num = fma(Bm[(size_t)i * R + r], s.coefB[i], num);
         Bm[(size_t)j * R + r] = num / den;
       }
     }
@@ -541,8 +555,9 @@ done:
 
 // ---- multi-branch and injection cases as correction terms (solver.py:614-622):
 // F = n0 + sum_j Lo[r][j] So[j][t], columns formed once per task in FP64 and rounded
-// to FP32 (scaled by 1/rating) for k_other.  Fully parallel over (row, case) and
-// (term, candidate): grid (blocks, task), grid-stride over both index ranges.
+// to FP32 (scaled by 1/rating) for k_other.  grid (blocks, task): a thread per monitored
+// row forms that row's terms of every case (its B'' values loaded once), the remaining
+// threads the (term, candidate) multipliers.
 __global__ void __launch_bounds__(NT) k_terms(DevGrid g, Work w) {
   const int b = blockIdx.y;
   if (w.status[b] != 0) return;
@@ -554,51 +569,63 @@ __global__ void __launch_bounds__(NT) k_terms(DevGrid g, Work w) {
   float* Lo = w.Lo + (size_t)b * M * NTM;
   float* So = w.So + (size_t)b * NTM * T;
   const uint8_t* ib = w.inj + (size_t)b * T * g.K;
-  const int nlo = M * NQ, nso = NTM * T;
+  const double* Wm = w.Wm + (size_t)b * g.NMB * rs;
+  const double* Mi = w.minv + (size_t)b * g.NM * MMAX * MMAX;
+  const uint8_t* mok = w.mc_ok + (size_t)b * g.NM;
+  const int nlo = M, nso = NTM * T;
   for (int idx = blockIdx.x * NT + threadIdx.x; idx < nlo + nso; idx += gridDim.x * NT) {
     if (idx < nlo) {
-      const int p = idx / NQ, q = idx % NQ;
+      const int p = idx;
       const int row = g.mon_row[p];
       const double inv = g.inv_rating[p];
-      float* out = Lo + ((size_t)p * NQ + q) * MT;
-      for (int j = 0; j < MT; ++j) out[j] = 0.f;
-      if (is_dead(dead, nd, row)) continue;
-      if (q < g.NM) {
+      float* out = Lo + (size_t)p * NQ * MT;
+      if (is_dead(dead, nd, row)) {
+        for (int i = 0; i < NQ * MT; ++i) out[i] = 0.f;
+        continue;
+      }
+      double bv[RMAX];
+#pragma unroll 8
+      for (int j = 0; j < rt; ++j) bv[j] = Bm[(size_t)j * R + row];
+      for (int q = 0; q < g.NM; ++q) {
+        float* o = out + q * MT;
+        for (int j = 0; j < MT; ++j) o[j] = 0.f;
+        if (!mok[q]) continue;
         const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-        if (!w.mc_ok[(size_t)b * g.NM + q]) continue;
         int own = -1;
-        for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+        for (int a2 = 0; a2 < m; ++a2) if (g.mb_row[st + a2] == row) own = a2;
         if (own >= 0) {
-          out[own] = (float)(-inv);
+          o[own] = (float)(-inv);
           continue;
         }
         double Dv[MMAX];
         for (int i = 0; i < m; ++i) {
           double v = g.Dm64[(size_t)(st + i) * R + row];
-          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+          const double* Wq = Wm + (size_t)(st + i) * rs;
+          for (int j = 0; j < rt; ++j) v = fma(bv[j], Wq[j], v);
           Dv[i] = v;
         }
-        const double* Mi = w.minv + ((size_t)b * g.NM + q) * MMAX * MMAX;
+        const double* Mq = Mi + (size_t)q * MMAX * MMAX;
         for (int j = 0; j < m; ++j) {
           double v = 0.0;
-          for (int i = 0; i < m; ++i) v += Dv[i] * Mi[i * m + j];
-          out[j] = (float)(v * inv);
+          for (int i = 0; i < m; ++i) v += Dv[i] * Mq[i * m + j];
+          o[j] = (float)(v * inv);
         }
-      } else {
-        const int qi = q - g.NM, sl = g.ic_slot[qi];
+      }
+      for (int qi = 0; qi < g.NI; ++qi) {
+        float* o = out + (g.NM + qi) * MT;
+        const int sl = g.ic_slot[qi];
         const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
         const double* pa_ = w.cia + ((size_t)b * g.NI + qi) * rs;
         const double* pb_ = w.cib + ((size_t)b * g.NI + qi) * rs;
         double pa = g.P0T[(size_t)ca * R + row], pb = pa;
         for (int j = 0; j < rt; ++j) {
-          const double bv = Bm[(size_t)j * R + row];
-          pa = fma(bv, pa_[j], pa);
-          pb = fma(bv, pb_[j], pb);
+          pa = fma(bv[j], pa_[j], pa);
+          pb = fma(bv[j], pb_[j], pb);
         }
         const double sp = g.ic_sp[qi];
-        out[0] = (float)(-sp * pa * inv);
-        out[1] = (float)(-sp * (pb - pa) * inv);
+        o[0] = (float)(-sp * pa * inv);
+        o[1] = (float)(-sp * (pb - pa) * inv);
+        for (int j = 2; j < MT; ++j) o[j] = 0.f;
       }
     } else {
       const int i2 = idx - nlo;
@@ -839,7 +866,7 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   }
   k_update<<<w.Wb, UT, dyn, st>>>(g, c, w);
   if (w.NTERM > 0 && g.M > 0) {
-    const int work = g.M * (g.NM + g.NI) + w.NTERM * w.T;
+    const int work = g.M + w.NTERM * w.T;
     const dim3 grid((unsigned)std::min(8, (work + NT - 1) / NT), w.Wb);
     k_terms<<<grid, NT, 0, st>>>(g, w);
   }

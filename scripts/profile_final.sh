@@ -28,8 +28,8 @@ cap k_scale_tc g3k 0
 cap "k_update" g118 0
 cap "k_terms" g118 0
 cap "k_n0" g118 0
-cap "k_top<" g1k 1
-cap "k_top<" g118 0
+cap "^k_top$" g1k 1
+cap "^k_top$" g118 0
 cap "k_pairs" g118 0
 cap "k_live" g1k 0
 cap "k_other" g1k 0
