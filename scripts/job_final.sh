@@ -2,10 +2,10 @@ set -u
 mkdir -p gpurun_out/tmp
 timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 for C in g118 g1k g3k g14 g10k; do
-  if [ $C = g118 ]; then timeout 900 python bench.py --config $C 2>&1 | tail -1 > gpurun_out/bench_${C}_r1f.json
-  else timeout 900 python bench.py --config $C --no-cpu 2>&1 | tail -1 > gpurun_out/bench_${C}_r1f.json; fi
+  if [ $C = g118 ]; then timeout 900 python bench.py --config $C 2>&1 | tail -1 > gpurun_out/bench_${C}_r1g.json
+  else timeout 900 python bench.py --config $C --no-cpu 2>&1 | tail -1 > gpurun_out/bench_${C}_r1g.json; fi
   python -c "
-import json; d=json.load(open('gpurun_out/bench_${C}_r1f.json')); print('$C', '%.3e'%d['value'], 'e2e %.3e'%d['e2e']['value'], round(d['ms_per_step'],2), d['roofline']['kernel'][:20], round(d['roofline']['frac'],4), d.get('cpu_baseline',{}).get('value'))"
+import json; d=json.load(open('gpurun_out/bench_${C}_r1g.json')); print('$C', '%.3e'%d['value'], 'e2e %.3e'%d['e2e']['value'], round(d['ms_per_step'],2), d['roofline']['kernel'][:20], round(d['roofline']['frac'],4), d.get('cpu_baseline',{}).get('value'))"
 done
 declare -A TASKS=([g14]=1024 [g118]=16384 [g1k]=2048 [g3k]=512)
 cap() {
@@ -13,9 +13,9 @@ cap() {
   local R=gpurun_out/tmp/p_${CFG}
   timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$K" -s 1 -c 1 \
       -o $R -f python bench.py --config $CFG --tasks $N --steps 1 --warmup 1 --no-cpu > gpurun_out/tmp/n.log 2>&1
-  echo "#### capture $K $CFG ($N tasks)" >> gpurun_out/summary_r1f_b.md
-  python profiles/summarize.py $R.ncu-rep >> gpurun_out/summary_r1f_b.md
-  python profiles/summarize.py --source $R.ncu-rep >> gpurun_out/summary_r1f_b.md 2>&1
+  echo "#### capture $K $CFG ($N tasks)" >> gpurun_out/summary_r1g_b.md
+  python profiles/summarize.py $R.ncu-rep >> gpurun_out/summary_r1g_b.md
+  python profiles/summarize.py --source $R.ncu-rep >> gpurun_out/summary_r1g_b.md 2>&1
 }
 cap "^k_top$" g118
 cap "^k_top$" g1k
