@@ -248,6 +248,20 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
     }
   }
   g.tm_ds = &s->tm_ds;
+  {
+    std::vector<int32_t> pos(G->N1 > 0 ? G->N1 : 1, -1);
+    std::vector<float> rat(G->N1 > 0 ? G->N1 : 1, 0.f);
+    int all = 1;
+    for (int c = 0; c < G->N1; ++c) {
+      const int p = G->row_mon_pos[G->sc_row[c]];
+      pos[c] = p;
+      rat[c] = p >= 0 ? (float)G->rating[p] : 0.f;
+      all &= p >= 0;
+    }
+    g.s_mon = all;
+    if (e == cudaSuccess) e = upload((const int32_t*)pos.data(), pos.size(), &g.sc_pos, o);
+    if (e == cudaSuccess) e = upload((const float*)rat.data(), rat.size(), &g.sc_rat, o);
+  }
   // D_base on monitored rows, case-major, for the winner report's coalesced sweeps
   if (e == cudaSuccess && (size_t)G->N1 * G->M > 0) {
     std::vector<double> dm((size_t)G->N1 * G->M);
@@ -399,7 +413,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   const size_t nitems = B * (size_t)((g.N1 + TOPC - 1) / TOPC) * (size_t)((T + top_tile_cands(T) - 1) / top_tile_cands(T));
   size_t o_ll = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_lc = L.add(B * 4);
   size_t o_q = L.add((nitems > 0 ? nitems : 1) * 8);
-  size_t o_s32 = L.add(B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
+  size_t o_s32 = L.add(g.s_mon ? 16 : B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
+  size_t o_rmx = L.add(B * (size_t)(g.M > 0 ? g.M : 1) * 4);
   size_t o_top = L.add(B * (size_t)TOPC * 4), o_done = L.add(B * (size_t)g.N1);
   const int nslot = RSEL_WARPS + (g.N1 + RCW - 1) / RCW;
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4), o_th = L.add(B * 4);
@@ -443,7 +458,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.pairs = x.lf + 2;
   x.qcount = (unsigned*)(base + o_bs);  // k_pairs queue length, zeroed per wave
   x.m0 = (float*)(base + o_m0); x.scale = (float*)(base + o_sc);
-  x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk);
+  x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk); x.rmax = (float*)(base + o_rmx);
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = TOPC;
   x.m0b = (float*)(base + o_m0b);

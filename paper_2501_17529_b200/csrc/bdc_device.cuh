@@ -62,6 +62,11 @@ struct DevGrid {
   const double* DM64;  // (N1, M) D_base on monitored rows, case-major (winner report)
   const float* DsT;    // (N1, Mp) D_base / rating on monitored rows, case-major, FP32 (k_scale)
   const CUtensorMap* tm_ds;  // host pointer: TMA descriptor of DsT (box 32 rows x 128 cases, 128B swizzle)
+  // pre-outage flow of single case c: when every outaged row is monitored (s_mon), it is
+  // read from the N-0 table, s(c,t) = n0s[sc_pos[c]][t] * sc_rat[c]; otherwise from s32
+  const int* sc_pos;   // (N1) monitored position of the outaged row (-1: unmonitored)
+  const float* sc_rat; // (N1) its rating (FP32)
+  int s_mon;           // 1: every single case's outaged row is monitored
   int Mp;              // M rounded up to a multiple of 4
   const float* D32;
   const int *row_from, *row_to, *branch_row, *mon_row, *row_mon_pos, *sub_col, *sub_count;
@@ -124,6 +129,8 @@ struct Work {
   int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
   float* s32;     // (Wb, N1, T)   n0[r_c][t] (pre-outage flow of each single case), FP32
+                  //               (only when !g.s_mon; see s_at)
+  float* rmax;    // (Wb, M)       max_t |n0s[m][t]| (g.s_mon: smax_c = rmax[sc_pos[c]] * sc_rat[c])
   uint32_t* bkey; // (Wb, N1)      ranking key max_t m0(t) + scale_c max_t |s(c,t)| (float bits)
   float* smax;    // (Wb, N1)      max_t |s(c,t)|
   int* top;       // (Wb, ptop)    the ptop cases with the largest bound, ascending index
@@ -257,6 +264,17 @@ __device__ __forceinline__ float max3abs(float a, float b, float c) {
   float d;
   asm("max.abs.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
+}
+
+// s(c, t) = n0[r_c][t] of single case c (FP32) and max_t |s(c, t)|, the same values in every
+// kernel (solver.py:612-613).
+__device__ __forceinline__ float s_at(const DevGrid& g, const Work& w, int b, int c, int t) {
+  if (g.s_mon) return w.n0s[((size_t)b * g.M + g.sc_pos[c]) * w.T + t] * g.sc_rat[c];
+  return w.s32[((size_t)b * g.N1 + c) * w.T + t];
+}
+__device__ __forceinline__ float smax_at(const DevGrid& g, const Work& w, int b, int c) {
+  if (g.s_mon) return w.rmax[(size_t)b * g.M + g.sc_pos[c]] * g.sc_rat[c];
+  return w.smax[(size_t)b * g.N1 + c];
 }
 
 // cp.async helpers (global -> shared, zero-filling when !ok).

@@ -177,7 +177,7 @@ __device__ __forceinline__ bool pair_evaluated(const DevGrid& g, const Work& w, 
 
 // The dominance bound of a skipped pair: max_b (m0_b(t) + scale_bc |s(c,t)|).
 __device__ __forceinline__ float pair_bound(const DevGrid& g, const Work& w, int b, int c, int t) {
-  const float as = fabsf(w.s32[((size_t)b * g.N1 + c) * w.T + t]);
+  const float as = fabsf(s_at(g, w, b, c, t));
   float ub = 0.f;
 #pragma unroll
   for (int blk = 0; blk < SB; ++blk)

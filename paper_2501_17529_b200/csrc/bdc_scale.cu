@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
     bool owndead = false;
     for (int d = 0; d < snd[k]; ++d) owndead |= sdead[k][d] == ownp;
     float keyv = 0.f;
-    const float smx = w.smax[(size_t)b * N1 + c];
+    const float smx = smax_at(g, w, b, c);
     for (int blk = 0; blk < SB; ++blk) {
       float U = 0.f;
       if (ok) {

@@ -54,7 +54,6 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
   const int nd = w.ndead[b];
   const double* Bm = w.Bm + (size_t)b * rs * R;
   const float* n0s = w.n0s + (size_t)b * M * T;
-  const float* s32 = w.s32 + (size_t)b * N1 * T;
   float* cm = w.cmax + (size_t)b * (N1 + g.NM + g.NI) * T;
   const bool vecN = TT % 4 == 0 && (T % 4) == 0 && (t0 % 4) == 0;
 
@@ -126,7 +125,7 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
 #pragma unroll
     for (int jj = 0; jj < TPT; ++jj) {
       const int t = t0 + ty * TPT + jj;
-      sv[i][jj] = (c >= 0 && t < T) ? s32[(size_t)c * T + t] : 0.f;
+      sv[i][jj] = (c >= 0 && t < T) ? s_at(g, w, b, c, t) : 0.f;
       acc[i][jj] = 0.f;
       cnt += c >= 0 && t < T;
     }
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
     const bool top = w.ranked ? done[cl] != 0 : cl < w.ptop;
     cand = !top && w.sc_ok[(size_t)b * N1 + cl] != 0;
     if (cand && w.screen) {
-      const float smx = w.smax[(size_t)b * N1 + cl];
+      const float smx = smax_at(g, w, b, cl);
       float coarse = 0.f;
 #pragma unroll
       for (int blk = 0; blk < SB; ++blk) {
@@ -345,13 +344,15 @@ __global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
     float sk[SB];
 #pragma unroll
     for (int blk = 0; blk < SB; ++blk) sk[blk] = __shfl_sync(0xffffffffu, scl[blk], k);
-    const float* sc = w.s32 + ((size_t)b * N1 + c) * T;
+    // s(c, .): a row of s32, or the N-0 row of the outaged branch times its rating
+    const float* sc = g.s_mon ? w.n0s + ((size_t)b * g.M + g.sc_pos[c]) * T : w.s32 + ((size_t)b * N1 + c) * T;
+    const float srat = g.s_mon ? g.sc_rat[c] : 1.f;
     bool live = false;
     for (int t0 = 0; t0 < T && !live; t0 += 32) {
       const int t = t0 + lane;
       bool lt = false;
       if (t < T) {
-        const float as = fabsf(sc[t]);
+        const float as = g.s_mon ? fabsf(sc[t] * srat) : fabsf(sc[t]);
         float bound = 0.f;
 #pragma unroll
         for (int blk = 0; blk < SB; ++blk)

@@ -658,7 +658,8 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   const int b = blockIdx.y;
   if (w.status[b] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int R = g.R, T = w.T, M = g.M, N1 = g.N1, NL = M + N1, rs = w.rs, rt = w.rank[b];
+  // rows emitted: monitored positions, then (unless s is read from n0s) single cases
+  const int R = g.R, T = w.T, M = g.M, N1 = g.N1, NL = g.s_mon ? M : M + N1, rs = w.rs, rt = w.rank[b];
   const int r0 = blockIdx.x * N0_ROWS, nr = min(NL - r0, N0_ROWS);
   const double* Bm = w.Bm + (size_t)b * rs * R;
   const double* Y = w.Y + (size_t)b * rs * T;
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
           }
           rmax = fmaxf(rmax, fabsf(v));
         }
-        if (li >= M) {  // warp-uniform: the row's max over this candidate chunk
+        {  // warp-uniform: the row's max over this candidate chunk
           for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
           if (lane == 0) sSmax[i0 + i] = fmaxf(sSmax[i0 + i], rmax);
         }
@@ -786,8 +787,10 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
     }
     __syncthreads();
   }
-  for (int i = tid; i < nr; i += NT)
+  for (int i = tid; i < nr; i += NT) {
     if (r0 + i >= M) w.smax[(size_t)b * N1 + (r0 + i - M)] = sSmax[i];
+    else w.rmax[(size_t)b * M + r0 + i] = sSmax[i];
+  }
 }
 
 // The ptop single cases with the largest screening bound bkey_c (the cases the
@@ -873,7 +876,7 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
 }
 
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
-  const int NL = g.M + g.N1;
+  const int NL = g.s_mon ? g.M : g.M + g.N1;
   if (NL == 0) return;
   const dim3 grid((NL + N0_ROWS - 1) / N0_ROWS, w.Wb);
   const int tpl = w.T > 64 ? 4 : (w.T > 32 ? 2 : 1);
