@@ -162,32 +162,47 @@ __global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w)
 
   // ---- split chain (factors.py:428-585) -----------------------------------------
   for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
+    // split setup, warp 0: a lane per branch element of the substation (the element
+    // loads and end lookups in parallel), lists compacted in element order
+    if (tid < 32) {
+      const int lane = tid;
       const int si = s.sub[j], a = g.sub_col[si], cnt = g.sub_count[si];
       const unsigned bits = s.bits[j];
+      const bool in = lane < cnt, mv = in && ((bits >> lane) & 1u);
+      const double be = in ? g.sub_elem_b[si * g.E + lane] : 0.0;
+      // sum of the stay susceptances in element order (as the reference sums them)
       double stay_b = 0.0;
-      for (int e = 0; e < cnt; ++e)
-        if (!((bits >> e) & 1u)) stay_b += g.sub_elem_b[si * g.E + e];
-      if (!(stay_b > 0.0)) {
-        s.fail = BDC_TASK_DEGENERATE_SPLIT; s.farg = j;
-      } else {
-        int nm = 0, nst = 0;
-        for (int e = 0; e < cnt; ++e) {
-          int row = g.sub_elem_row[si * g.E + e];
-          int fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]), tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
-          double sign; int far, end;
-          if (fc == a) { sign = 1.0; far = tc; end = 0; }
-          else if (tc == a) { sign = -1.0; far = fc; end = 1; }
-          else { s.fail = BDC_TASK_DETACHED; s.farg = j; break; }
-          if ((bits >> e) & 1u) {
-            s.mrow[nm] = row; s.msign[nm] = sign; s.mend[nm] = end; ++nm;
-          } else {
-            s.srow[nst] = row; s.ssign[nst] = sign; s.sfar[nst] = far;
-            s.sw[nst] = g.sub_elem_b[si * g.E + e] / stay_b; ++nst;
-          }
-        }
-        s.a = a; s.nm = nm; s.nst = nst;
+      for (int e = 0; e < cnt; ++e) {
+        const double v = __shfl_sync(0xffffffffu, be, e);
+        if (!((bits >> e) & 1u)) stay_b += v;
       }
+      int row = -1, fc = -1, tc = -1;
+      if (in) {
+        row = g.sub_elem_row[si * g.E + lane];
+        fc = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]);
+        tc = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
+      }
+      const bool detached = in && fc != a && tc != a;
+      const unsigned dmask = __ballot_sync(0xffffffffu, detached);
+      const unsigned mmask = __ballot_sync(0xffffffffu, mv), smask = __ballot_sync(0xffffffffu, in && !mv);
+      const unsigned lt = (1u << lane) - 1u;
+      if (!(stay_b > 0.0)) {
+        if (lane == 0) { s.fail = BDC_TASK_DEGENERATE_SPLIT; s.farg = j; }
+      } else if (dmask) {
+        if (lane == 0) { s.fail = BDC_TASK_DETACHED; s.farg = j; }
+      } else if (in) {
+        const bool atf = fc == a;
+        const double sign = atf ? 1.0 : -1.0;
+        if (mv) {
+          const int q = __popc(mmask & lt);
+          s.mrow[q] = row; s.msign[q] = sign; s.mend[q] = atf ? 0 : 1;
+        } else {
+          const int q = __popc(smask & lt);
+          s.srow[q] = row; s.ssign[q] = sign; s.sfar[q] = atf ? tc : fc;
+          s.sw[q] = be / stay_b;
+        }
+      }
+      if (lane == 0) { s.a = a; s.nm = __popc(mmask); s.nst = __popc(smask); }
     }
     __syncthreads();
     if (s.fail) goto done;
