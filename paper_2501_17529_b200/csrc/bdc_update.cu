@@ -27,14 +27,13 @@ namespace {
 
 constexpr int NT = 256;  // k_n0, k_topk
 constexpr int NW = NT / 32;
-constexpr int UT = 128;  // k_update: one task per CTA, small so that many tasks are in flight
-constexpr int UW = UT / 32;
+constexpr int UWMAX = 16;  // k_update: one task per CTA of 128..512 threads (by grid size)
 
 struct UpdShared {
   int sub[RMAX];
   unsigned bits[RMAX];
   int k, d, nd, fail, farg, nrh, nact;
-  int wcnt[UW];
+  int wcnt[UWMAX];
   int dead[RMAX];
   int orow[RMAX];      // outage rows in task order
   int ofc[RMAX], otc[RMAX];  // current endpoint columns of the outaged rows
@@ -49,7 +48,7 @@ struct UpdShared {
   double coefC[RMAX];        // sum_m sign_m B_i[row_m]            (coupler row of split j)
   double coefB[RMAX];        // sum_st w_st (C_i[far_st] - C_i[a]) (numerator of split j)
   double inner[MMAX * MMAX];
-  double mA[UW][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
+  double mA[UWMAX][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
   double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
   double ybase[RMAX];
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
@@ -100,7 +99,11 @@ __device__ void set_island(const Work& w, int b, int order) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(UT, 6) k_update(DevGrid g, DevCfg cfg, Work w) {
+// UT threads per task: 128 for small grids (many tasks in flight), more for large grids,
+// whose row and column loops need the memory parallelism (few tasks per SM).
+template <int UT, int MINB>
+__global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work w) {
+  constexpr int UW = UT / 32;
   __shared__ UpdShared s;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int R = g.R, C0 = g.C0, rs = w.rs, Cs = w.Cs;
@@ -879,10 +882,15 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   const size_t dyn = update_dyn_bytes(w.rs, g.E > 0 ? g.E : 1);
   static size_t opted = 0;
   if (dyn > opted) {
-    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_dyn_bytes(RMAX, EMAX));
+    const int mx = (int)update_dyn_bytes(RMAX, EMAX);
+    cudaFuncSetAttribute(k_update<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_update<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_update<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     opted = update_dyn_bytes(RMAX, EMAX);
   }
-  k_update<<<w.Wb, UT, dyn, st>>>(g, c, w);
+  if (g.R > 2048) k_update<512, 1><<<w.Wb, 512, dyn, st>>>(g, c, w);
+  else if (g.R > 512) k_update<256, 3><<<w.Wb, 256, dyn, st>>>(g, c, w);
+  else k_update<128, 6><<<w.Wb, 128, dyn, st>>>(g, c, w);
   if (w.NTERM > 0 && g.M > 0) {
     const int work = g.M + w.NTERM * w.T;
     const dim3 grid((unsigned)std::min(8, (work + NT - 1) / NT), w.Wb);
