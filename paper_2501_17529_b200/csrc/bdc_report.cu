@@ -13,6 +13,7 @@
 #include "bdc_device.cuh"
 
 #include <climits>
+#include <cstdlib>
 
 namespace bdc {
 
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(RT) k_rsel_w(DevGrid g, DevCfg cfg, Work w) {
 namespace {
 constexpr int SRC = 128;  // monitored rows per chunk (4 per lane)
 }
-template <int KC>
+template <int KC, int CQ>  // CQ: cases per warp evaluated together
 __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
@@ -609,17 +610,44 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   if (tile * RCW >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kc = cfg.kc, kg = cfg.kg;
+  const int base = tile * RCW, ncs = min(n, base + RCW) - base;
   extern __shared__ __align__(16) double rsm[];
   double* sB = rsm;                  // [2][rt][SRC] B'' on the chunk's monitored rows
   double* sN = sB + 2 * rs * SRC;    // [2][SRC] N-0 column
   double* sI = sN + 2 * SRC;         // [2][SRC] 1 / rating
+  double* sWc = sI + 2 * SRC;        // [RCW][rs] the cases' W rows
+  double* cRel = sWc + RCW * rs;     // [RCW][KC] each case's running top-kc
+  double* cFlow = cRel + RCW * KC;
+  double* sIdn = cFlow + RCW * KC;   // [RCW] 1 / den
+  double* sSc = sIdn + RCW;          // [RCW] N-0 flow of the outaged row
+  int* cPos = (int*)(sSc + RCW);     // [RCW][KC]
+  int* sC = cPos + RCW * KC;         // [RCW] case index
+  int* sOwn = sC + RCW;              // [RCW] monitored position of the outaged row
+  int* cN = sOwn + RCW;              // [RCW] entries in the case's list
   __shared__ WarpList wl[RW];
-  __shared__ double sWc[RW][RMAX];
   __shared__ double wmax[RW];
   __shared__ int sdeadp[RMAX];  // monitored positions of the disconnected rows (-1: unmonitored)
   const int nd = w.ndead[b];
   if (tid < nd) sdeadp[tid] = g.row_mon_pos[w.dead[(size_t)b * RMAX + tid]];
   if (lane == 0) wl[wid].n = 0;
+  for (int i = tid; i < RCW; i += RT) {
+    const int c = i < ncs ? w.rlist[(size_t)b * N1 + base + i] : -1;
+    sC[i] = c;
+    cN[i] = 0;
+    if (c >= 0) {
+      const int rowc = g.sc_row[c];
+      sOwn[i] = g.row_mon_pos[rowc];
+      sIdn[i] = 1.0 / w.den[(size_t)b * N1 + c];
+      sSc[i] = w.n0b[(size_t)b * g.R + rowc];
+    } else {
+      sOwn[i] = -1; sIdn[i] = 0.0; sSc[i] = 0.0;
+    }
+  }
+  for (int idx = tid; idx < ncs * rt; idx += RT) {
+    const int i = idx / rt, j = idx - i * rt;
+    const int c = w.rlist[(size_t)b * N1 + base + i];
+    sWc[i * rs + j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+  }
   const double* n0m = w.n0m + (size_t)b * M;
   const double* Bmon = w.Bmon + (size_t)b * rs * M;
   const double floor_rel = (double)w.theta[b];  // entries below theta are never reported
@@ -637,63 +665,107 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
     }
     cp_commit();
   };
+  // chunk-outer, case-inner: the staged B'' chunk serves all RCW cases of the tile; each
+  // warp evaluates CQ of its cases at once (the B'' loads shared by the CQ columns) and
+  // folds each case's chunk top-kc into the case's running list
   const int nchunks = (M + SRC - 1) / SRC;
-  const int end = min(n, (tile + 1) * RCW);
-  for (int g0 = tile * RCW; g0 < end; g0 += RW) {
-    const int li = g0 + wid;
-    const int c = li < end ? w.rlist[(size_t)b * N1 + li] : -1;
-    int ownp = -1, order = INT_MAX;
-    double idn = 0.0, sc = 0.0;
-    if (c >= 0) {
-      const int rowc = g.sc_row[c];
-      ownp = g.row_mon_pos[rowc];
-      order = g.sc_order[c];
-      idn = 1.0 / w.den[(size_t)b * N1 + c];
-      sc = w.n0b[(size_t)b * g.R + rowc];
-      for (int j = lane; j < rt; j += 32) sWc[wid][j] = w.Wsc[((size_t)b * N1 + c) * rs + j];
+  issue(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int bf = ch & 1, m0 = ch * SRC;
+    if (ch + 1 < nchunks) {
+      issue(m0 + SRC, bf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
-    const double* Dc = g.DM64 + (size_t)(c >= 0 ? c : 0) * M;
-    lt.clear();
-    __syncthreads();  // sWc written; the previous group's chunk buffers are free
-    const double thresh = fmax(warp_thresh(wl[wid], kg), floor_rel);
-    issue(0, 0);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int bf = ch & 1, m0 = ch * SRC;
-      if (ch + 1 < nchunks) {
-        issue(m0 + SRC, bf ^ 1);
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
-      }
-      __syncthreads();
-      if (c >= 0) {
-        double dv[SRC / 32];
+    __syncthreads();
+    unsigned skip = 0;  // rows past M or disconnected (flow exactly 0)
+#pragma unroll
+    for (int u = 0; u < SRC / 32; ++u) {
+      const int p = m0 + lane + 32 * u;
+      if (p >= M || is_dead(sdeadp, nd, p)) skip |= 1u << u;
+    }
+    const double* cB = sB + bf * rs * SRC + lane;
+    for (int i0 = wid * CQ; i0 < ncs; i0 += RW * CQ) {
+      double dv[CQ][SRC / 32];
+#pragma unroll
+      for (int q = 0; q < CQ; ++q) {
+        const int c = sC[i0 + q];
+        const double* Dc = g.DM64 + (size_t)(c >= 0 ? c : 0) * M;
 #pragma unroll
         for (int u = 0; u < SRC / 32; ++u) {
           const int p = m0 + lane + 32 * u;
-          dv[u] = p < M ? __ldg(&Dc[p]) : 0.0;
+          dv[q][u] = p < M ? __ldg(&Dc[p]) : 0.0;
         }
-        for (int j = 0; j < rt; ++j) {
-          const double wj = sWc[wid][j];
+      }
+      const double* W0 = sWc + i0 * rs;
+      for (int j = 0; j < rt; ++j) {
+        double bv[SRC / 32];
 #pragma unroll
-          for (int u = 0; u < SRC / 32; ++u) dv[u] = fma(sB[(bf * rs + j) * SRC + lane + 32 * u], wj, dv[u]);
+        for (int u = 0; u < SRC / 32; ++u) bv[u] = cB[j * SRC + 32 * u];
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+          const double wj = W0[q * rs + j];
+#pragma unroll
+          for (int u = 0; u < SRC / 32; ++u) dv[q][u] = fma(bv[u], wj, dv[q][u]);
         }
+      }
+#pragma unroll
+      for (int q = 0; q < CQ; ++q) {
+        const int i = i0 + q;
+        if (sC[i] < 0) continue;
+        const int ownp = sOwn[i];
+        const double idn = sIdn[i], sc = sSc[i];
+        const double thresh = fmax(floor_rel, cN[i] == kc ? cRel[i * KC + kc - 1] : -1.0);
+        lt.clear();
 #pragma unroll
         for (int u = 0; u < SRC / 32; ++u) {
+          if (skip & (1u << u)) continue;
           const int r = lane + 32 * u, p = m0 + r;
-          if (p >= M || is_dead(sdeadp, nd, p)) continue;  // disconnected: flow exactly 0
           const double nv = sN[bf * SRC + r];
-          const double f = (p == ownp) ? nv + (-1.0) * sc : nv + (dv[u] * idn) * sc;
+          const double f = (p == ownp) ? nv + (-1.0) * sc : nv + (dv[q][u] * idn) * sc;
           const double rel = fabs(f) * sI[bf * SRC + r];
           mymax = fmax(mymax, rel);
           if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
         }
+        if (!__any_sync(0xffffffffu, lt.rel[0] >= 0.0)) continue;
+        // fold: the case's list joins lane 0's, then kc rounds of warp argmax rewrite it
+        if (lane == 0)
+          for (int e = 0; e < cN[i]; ++e) lt.insert(cRel[i * KC + e], cPos[i * KC + e], cFlow[i * KC + e]);
+        __syncwarp();
+        int cnt = 0;
+        for (; cnt < kc; ++cnt) {
+          double r = lt.rel[0];
+          int p = lt.pos[0], src = lane;
+          for (int o = 16; o; o >>= 1) {
+            const double orr = __shfl_xor_sync(0xffffffffu, r, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            const int os = __shfl_xor_sync(0xffffffffu, src, o);
+            if (better(orr, op, r, p)) { r = orr; p = op; src = os; }
+          }
+          if (r < 0.0) break;
+          const double f = __shfl_sync(0xffffffffu, lt.flow[0], src);
+          if (lane == src) lt.pop();
+          if (lane == 0) { cRel[i * KC + cnt] = r; cPos[i * KC + cnt] = p; cFlow[i * KC + cnt] = f; }
+        }
+        if (lane == 0) cN[i] = cnt;
+        __syncwarp();
       }
-      __syncthreads();
     }
-    if (c >= 0) warp_merge<KC>(lt, kc, wl[wid], kg, order);
-    __syncwarp();
+    __syncthreads();
   }
+  // each warp merges its cases' lists into its top-kg by (rel desc, case order, position)
+  for (int i0 = wid * CQ; i0 < ncs; i0 += RW * CQ) {
+    for (int q = 0; q < CQ; ++q) {
+      const int i = i0 + q, c = sC[i];
+      if (c < 0 || cN[i] == 0) continue;
+      lt.clear();
+      if (lane == 0)
+        for (int e = 0; e < cN[i]; ++e) lt.insert(cRel[i * KC + e], cPos[i * KC + e], cFlow[i * KC + e]);
+      warp_merge<KC>(lt, kc, wl[wid], kg, g.sc_order[c]);
+    }
+  }
+  __syncwarp();
   for (int o = 16; o; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if (lane == 0) wmax[wid] = mymax;
   __syncthreads();
@@ -856,6 +928,10 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
 }
 
 namespace {
+size_t rsweep_dyn_bytes(int rs, int kc) {
+  return (2 * (size_t)rs * SRC + 4 * (size_t)SRC + (size_t)RCW * rs + 2 * (size_t)RCW * kc + 2 * RCW) *
+             sizeof(double) + ((size_t)RCW * kc + 3 * RCW) * sizeof(int);
+}
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   if (!w.rsel_cta && g.M <= 32 * 16 && g.N1 + g.NM + g.NI <= 32 * 16)
@@ -863,14 +939,22 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
   else
     k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
   if (g.N1 > 0 && g.M > 0) {
-    const size_t dyn = (2 * (size_t)w.rs * SRC + 4 * (size_t)SRC) * sizeof(double);
+    const size_t dyn = rsweep_dyn_bytes(w.rs, KC);
     static bool init = false;
     if (!init) {
-      cudaFuncSetAttribute(k_rsweep<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((2 * (size_t)RMAX * SRC + 4 * (size_t)SRC) * sizeof(double)));
+      cudaFuncSetAttribute(k_rsweep<KC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)rsweep_dyn_bytes(RMAX, KC));
+      cudaFuncSetAttribute(k_rsweep<KC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)rsweep_dyn_bytes(RMAX, KC));
       init = true;
     }
-    k_rsweep<KC><<<dim3(w.nslot - RSEL_WARPS, w.Wb), RT, dyn, s>>>(g, c, w);
+    // one case per warp at a time; on large grids four (their B'' loads shared) -- the
+    // test hook BDC_RSWEEP_CQ forces either
+    const char* cq_env = getenv("BDC_RSWEEP_CQ");
+    const int cq = cq_env ? atoi(cq_env) : (g.M <= 16 * SRC ? 1 : 4);
+    const dim3 grid(w.nslot - RSEL_WARPS, w.Wb);
+    if (cq == 1) k_rsweep<KC, 1><<<grid, RT, dyn, s>>>(g, c, w);
+    else k_rsweep<KC, 4><<<grid, RT, dyn, s>>>(g, c, w);
   }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);

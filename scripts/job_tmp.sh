@@ -2,4 +2,3 @@ set -u
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
 bash scripts/gpu_test_bench.sh "g118 g1k g3k" skip
-bash scripts/launches.sh ku g118 g1k g3k 2>&1 | grep -E "k_update|launch list"

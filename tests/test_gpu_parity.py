@@ -250,7 +250,8 @@ def test_wave_split_is_invisible(name, sessions):
 @pytest.mark.parametrize("name", ["fixture_a", "fixture_b", "case300", "g118"])
 def test_report_select_variants_agree(name, sessions, monkeypatch):
     """The warp-per-task winner-report selection (small grids) and the CTA-per-task one
-    (large grids, forced here with BDC_RSEL_CTA=1) give bit-identical results."""
+    (large grids, forced here with BDC_RSEL_CTA=1) give bit-identical results, and so do
+    the report sweep's one-case and four-case warp variants (BDC_RSWEEP_CQ)."""
     case = next(c for c in CASES if c["name"] == name)
     sess = sessions(case)
     arr, _ = load_case(name)
@@ -263,6 +264,12 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     assert np.array_equal(warp.best, cta.best)
     assert np.array_equal(warp.metric, cta.metric, equal_nan=True)
     assert warp.reports() == cta.reports()
+    for cq in ("1", "4"):
+        monkeypatch.setenv("BDC_RSWEEP_CQ", cq)
+        alt = eng.solve(*args)
+        monkeypatch.delenv("BDC_RSWEEP_CQ")
+        assert np.array_equal(warp.metric, alt.metric, equal_nan=True)
+        assert warp.reports() == alt.reports()
 
 
 @pytest.mark.parametrize("name,T,k,d", [("g1k", 32, 3, 1), ("g3k", 16, 6, 0)])
