@@ -934,7 +934,10 @@ size_t rsweep_dyn_bytes(int rs, int kc) {
 }
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  if (!w.rsel_cta && g.M <= 32 * 16 && g.N1 + g.NM + g.NI <= 32 * 16)
+  const int nc = g.N1 + g.NM + g.NI;
+  if (!w.rsel_cta && g.M <= 32 * 8 && nc <= 32 * 8)
+    k_rsel_w<KC, 8><<<(w.Wb + RW - 1) / RW, RT, 0, s>>>(g, c, w);
+  else if (!w.rsel_cta && g.M <= 32 * 16 && nc <= 32 * 16)
     k_rsel_w<KC, 16><<<(w.Wb + RW - 1) / RW, RT, 0, s>>>(g, c, w);
   else
     k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);

@@ -31,10 +31,12 @@ namespace bdc {
 // RC (cp.async double buffer of D_base columns, B'' rows and n0/rating).
 // One tile: task b, cases list[0..nlist) (entries < 0 are empty; list == nullptr means
 // cases 0..nlist-1), candidates t0..t0+TT.  Ends with the block synchronised.
-template <int CPT, int TPT, int TX, int TY, int RC>
+template <int CPT, int TPT, int TX, int TY, int RC, int RGS>
 __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b, const int* list, int nlist, int t0) {
-  constexpr int NTH = TX * TY, NC = CPT * TX, TT = TPT * TY;
-  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  constexpr int TG = TX * TY, NTH = TG * RGS, NC = CPT * TX, TT = TPT * TY;
+  static_assert(TG % 32 == 0, "row groups are whole warps");
+  // RGS row groups of TG threads split each chunk's rows (maxima combined at the end)
+  const int tid = threadIdx.x, gi = tid / TG, tl = tid % TG, tx = tl % TX, ty = tl / TX;
   const int rs = w.rs, rt = w.rank[b], T = w.T, M = g.M, N1 = g.N1, R = g.R;
   // dynamic: [sW rs*NC f64][sBb 2*rs*RC f64][sN 2*RC*TT f32][sD 2*RC*NC f32]
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -51,6 +53,7 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
   __shared__ int sRow[2][RC];
   __shared__ __align__(16) float sL[RC][NC];
   __shared__ int sdead[RMAX];
+  __shared__ unsigned sAcc[RGS > 1 ? NC : 1][RGS > 1 ? TT : 1];  // row groups' maxima
   const int nd = w.ndead[b];
   const double* Bm = w.Bm + (size_t)b * rs * R;
   const float* n0s = w.n0s + (size_t)b * M * T;
@@ -65,6 +68,8 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
     sInvDen[cc] = ok ? 1.0 / w.den[(size_t)b * N1 + c] : 0.0;
     sRowC[cc] = c >= 0 ? g.sc_row[c] : -1;
   }
+  if constexpr (RGS > 1)
+    for (int i = tid; i < NC * TT; i += NTH) (&sAcc[0][0])[i] = 0u;
   __syncthreads();
   // ---- stage one row chunk (async): row ids + 1/rating, B'' rows, n0/rating, D_base
   auto issue = [&](int m0, int buf) {
@@ -127,7 +132,7 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
       const int t = t0 + ty * TPT + jj;
       sv[i][jj] = (c >= 0 && t < T) ? s_at(g, w, b, c, t) : 0.f;
       acc[i][jj] = 0.f;
-      cnt += c >= 0 && t < T;
+      cnt += gi == 0 && c >= 0 && t < T;
     }
   }
   // evaluated (case, candidate) pairs, for the roofline accounting
@@ -186,18 +191,36 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
       // fmaf) and one FMNMX3 (|.| on every input) per accumulator
       static_assert(TPT % 2 == 0, "candidate pairs");
 #pragma unroll 2
-      for (int rr = 0; rr < rend; rr += 2) {
+      for (int rr = 2 * gi; rr < rend; rr += 2 * RGS) {
         float2 l2[2][CPT], n2[2][TPT / 2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+          if constexpr (CPT % 2 == 0) {
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            const float lv = sL[rr + h][tx * CPT + i];
-            l2[h][i] = make_float2(lv, lv);
+            for (int i = 0; i < CPT; i += 2) {
+              const float2 lv = *reinterpret_cast<const float2*>(&sL[rr + h][tx * CPT + i]);
+              l2[h][i] = make_float2(lv.x, lv.x);
+              l2[h][i + 1] = make_float2(lv.y, lv.y);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) {
+              const float lv = sL[rr + h][tx * CPT + i];
+              l2[h][i] = make_float2(lv, lv);
+            }
           }
+          if constexpr (TPT % 4 == 0) {
 #pragma unroll
-          for (int p = 0; p < TPT / 2; ++p)
-            n2[h][p] = *reinterpret_cast<const float2*>(&SN(buf, rr + h, ty * TPT + 2 * p));
+            for (int p = 0; p < TPT / 2; p += 2) {
+              const float4 q4 = *reinterpret_cast<const float4*>(&SN(buf, rr + h, ty * TPT + 2 * p));
+              n2[h][p] = make_float2(q4.x, q4.y);
+              n2[h][p + 1] = make_float2(q4.z, q4.w);
+            }
+          } else {
+#pragma unroll
+            for (int p = 0; p < TPT / 2; ++p)
+              n2[h][p] = *reinterpret_cast<const float2*>(&SN(buf, rr + h, ty * TPT + 2 * p));
+          }
         }
 #pragma unroll
         for (int i = 0; i < CPT; ++i)
@@ -216,6 +239,19 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
 
   // exact per-(case, candidate) maxima for the winner report; the per-candidate max
   // over the tile's cases goes into the running metric
+  if constexpr (RGS > 1) {  // combine the row groups' maxima (all >= 0: ordered as uint)
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TPT; ++jj)
+        if (gi > 0) atomicMax(&sAcc[tx * CPT + i][ty * TPT + jj], __float_as_uint(acc[i][jj]));
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TPT; ++jj) acc[i][jj] = fmaxf(acc[i][jj], __uint_as_float(sAcc[tx * CPT + i][ty * TPT + jj]));
+  }
+  if (gi == 0) {
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = sCase[tx * CPT + i];
@@ -237,29 +273,30 @@ __device__ __forceinline__ void top_tile(const DevGrid& g, const Work& w, int b,
     const int t = t0 + ty * TPT + jj;
     if ((tx % GW) == 0 && t < T) atomic_max_pos(&w.m32[(size_t)b * T + t], v);
   }
+  }
   __syncthreads();  // the caller may reuse the shared buffers for the next tile
 #undef SN
 #undef SD
 }
 
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
-__global__ void __launch_bounds__(TX* TY, MINB) k_top(DevGrid g, DevCfg cfg, Work w) {
+template <int CPT, int TPT, int TX, int TY, int RC, int RGS, int MINB>
+__global__ void __launch_bounds__(TX* TY* RGS, MINB) k_top(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.z;
   if (w.status[b] != 0) return;
   const int* list = w.ranked ? w.top + (size_t)b * w.ptop : nullptr;
   const int nlist = w.ranked ? w.ptop : min(w.ptop, g.N1);
-  top_tile<CPT, TPT, TX, TY, RC>(g, w, b, list, nlist, blockIdx.y * (TPT * TY));
+  top_tile<CPT, TPT, TX, TY, RC, RGS>(g, w, b, list, nlist, blockIdx.y * (TPT * TY));
 }
 
 // Live cases, TOPC per item, every candidate tile: persistent over the queue.
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
-__global__ void __launch_bounds__(TX* TY, MINB) k_pairs(DevGrid g, DevCfg cfg, Work w) {
+template <int CPT, int TPT, int TX, int TY, int RC, int RGS, int MINB>
+__global__ void __launch_bounds__(TX* TY* RGS, MINB) k_pairs(DevGrid g, DevCfg cfg, Work w) {
   const unsigned nq = *w.qcount;
   for (unsigned it = blockIdx.x; it < nq; it += gridDim.x) {
     const int2 q = w.queue[it];
     const int b = q.x, grp = q.y >> 16, tt = q.y & 0xffff;
     const int n = min(TOPC, w.lcnt[b] - grp * TOPC);
-    top_tile<CPT, TPT, TX, TY, RC>(g, w, b, w.llist + (size_t)b * g.N1 + grp * TOPC, n, tt * (TPT * TY));
+    top_tile<CPT, TPT, TX, TY, RC, RGS>(g, w, b, w.llist + (size_t)b * g.N1 + grp * TOPC, n, tt * (TPT * TY));
   }
 }
 
@@ -389,7 +426,7 @@ __global__ void k_queue(DevGrid g, Work w) {
 }
 
 namespace {
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+template <int CPT, int TPT, int TX, int TY, int RC, int RGS, int MINB>
 void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   constexpr int NC = CPT * TX, TT = TPT * TY;
   static_assert(NC == TOPC, "TOP tile = TOPC cases");
@@ -402,15 +439,15 @@ void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_top<CPT, TPT, TX, TY, RC, MINB>);
+    cudaFuncGetAttributes(&fa, k_top<CPT, TPT, TX, TY, RC, RGS, MINB>);
     max_dyn = optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_top<CPT, TPT, TX, TY, RC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaFuncSetAttribute(k_top<CPT, TPT, TX, TY, RC, RGS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
   dim3 grid(1, (w.T + TT - 1) / TT, w.Wb);
-  k_top<CPT, TPT, TX, TY, RC, MINB><<<grid, TX * TY, dyn, s>>>(g, c, w);
+  k_top<CPT, TPT, TX, TY, RC, RGS, MINB><<<grid, TX * TY * RGS, dyn, s>>>(g, c, w);
 }
 
-template <int CPT, int TPT, int TX, int TY, int RC, int MINB>
+template <int CPT, int TPT, int TX, int TY, int RC, int RGS, int MINB>
 void launch_pairs_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   constexpr int NC = CPT * TX, TT = TPT * TY;
   const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
@@ -422,25 +459,26 @@ void launch_pairs_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_pairs<CPT, TPT, TX, TY, RC, MINB>);
+    cudaFuncGetAttributes(&fa, k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>);
     max_dyn = optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_pairs<CPT, TPT, TX, TY, RC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaFuncSetAttribute(k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
   // persistent: as many CTAs as fit at once for this rank stride's shared memory
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pairs<CPT, TPT, TX, TY, RC, MINB>, TX * TY, dyn);
-  k_pairs<CPT, TPT, TX, TY, RC, MINB><<<nsm * (per_sm > 0 ? per_sm : 1), TX * TY, dyn, s>>>(g, c, w);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>, TX * TY * RGS, dyn);
+  k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB><<<nsm * (per_sm > 0 ? per_sm : 1), TX * TY * RGS, dyn, s>>>(g, c, w);
 }
 
 // tile shapes: 16 cases x top_tile_cands(T) candidates (bdc_device.cuh)
 void launch_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  if (w.T >= 96) launch_top_t<1, 8, 16, 16, 64, 2>(g, c, w, s);       // 16 cases x 128 candidates
-  else if (w.T >= 48) launch_top_t<1, 4, 16, 16, 64, 2>(g, c, w, s);  // 16 x 64
-  else launch_top_t<1, 2, 16, 16, 64, 2>(g, c, w, s);                 // 16 x 32
+  // thread tile 2 cases x 8 or 4 candidates; 2 or 4 row groups split each chunk's rows
+  if (w.T >= 96) launch_top_t<2, 8, 8, 16, 64, 2, 2>(g, c, w, s);       // 16 cases x 128 candidates
+  else if (w.T >= 48) launch_top_t<2, 4, 8, 16, 64, 2, 2>(g, c, w, s);  // 16 x 64
+  else launch_top_t<2, 4, 8, 8, 64, 4, 2>(g, c, w, s);                 // 16 x 32
 }
 void launch_pairs(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  if (w.T >= 96) launch_pairs_t<1, 8, 16, 16, 64, 2>(g, c, w, s);
-  else if (w.T >= 48) launch_pairs_t<1, 4, 16, 16, 64, 2>(g, c, w, s);
-  else launch_pairs_t<1, 2, 16, 16, 64, 2>(g, c, w, s);
+  if (w.T >= 96) launch_pairs_t<2, 8, 8, 16, 64, 2, 2>(g, c, w, s);
+  else if (w.T >= 48) launch_pairs_t<2, 4, 8, 16, 64, 2, 2>(g, c, w, s);
+  else launch_pairs_t<2, 4, 8, 8, 64, 4, 2>(g, c, w, s);
 }
 }  // namespace
 

@@ -1,4 +1,4 @@
 set -u
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-bash scripts/gpu_test_bench.sh "g118 g1k g3k" skip
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+bash scripts/gpu_test_bench.sh "g118 g1k g3k g10k" skip
