@@ -599,11 +599,9 @@ __global__ void __launch_bounds__(RT) k_rsel_w(DevGrid g, DevCfg cfg, Work w) {
 // top-kc (rel desc, position asc; solver.py:287-299), merged per case into the warp's
 // top-kg by (rel desc, case order, position) (_merge_entries, solver.py:302-318); the
 // CTA merges its warps' lists into one partial slot.
-namespace {
-constexpr int SRC = 128;  // monitored rows per chunk (4 per lane)
-}
-template <int KC, int CQ>  // CQ: cases per warp evaluated together
+template <int KC, int CQ, int RPL>  // CQ: cases per warp evaluated together; RPL: rows per lane
 __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+  constexpr int SRC = 32 * RPL;  // monitored rows per chunk
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
   const int n = w.rcnt[b];
@@ -669,6 +667,9 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   // warp evaluates CQ of its cases at once (the B'' loads shared by the CQ columns) and
   // folds each case's chunk top-kc into the case's running list
   const int nchunks = (M + SRC - 1) / SRC;
+  // one chunk (small grids): every case completes in one pass, so its lanes' lists merge
+  // straight into the warp's top-kg (and the warp's kg-th entry prunes the next cases)
+  const bool one = nchunks == 1;
   issue(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
     const int bf = ch & 1, m0 = ch * SRC;
@@ -681,33 +682,33 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
     __syncthreads();
     unsigned skip = 0;  // rows past M or disconnected (flow exactly 0)
 #pragma unroll
-    for (int u = 0; u < SRC / 32; ++u) {
+    for (int u = 0; u < RPL; ++u) {
       const int p = m0 + lane + 32 * u;
       if (p >= M || is_dead(sdeadp, nd, p)) skip |= 1u << u;
     }
     const double* cB = sB + bf * rs * SRC + lane;
     for (int i0 = wid * CQ; i0 < ncs; i0 += RW * CQ) {
-      double dv[CQ][SRC / 32];
+      double dv[CQ][RPL];
 #pragma unroll
       for (int q = 0; q < CQ; ++q) {
         const int c = sC[i0 + q];
         const double* Dc = g.DM64 + (size_t)(c >= 0 ? c : 0) * M;
 #pragma unroll
-        for (int u = 0; u < SRC / 32; ++u) {
+        for (int u = 0; u < RPL; ++u) {
           const int p = m0 + lane + 32 * u;
           dv[q][u] = p < M ? __ldg(&Dc[p]) : 0.0;
         }
       }
       const double* W0 = sWc + i0 * rs;
       for (int j = 0; j < rt; ++j) {
-        double bv[SRC / 32];
+        double bv[RPL];
 #pragma unroll
-        for (int u = 0; u < SRC / 32; ++u) bv[u] = cB[j * SRC + 32 * u];
+        for (int u = 0; u < RPL; ++u) bv[u] = cB[j * SRC + 32 * u];
 #pragma unroll
         for (int q = 0; q < CQ; ++q) {
           const double wj = W0[q * rs + j];
 #pragma unroll
-          for (int u = 0; u < SRC / 32; ++u) dv[q][u] = fma(bv[u], wj, dv[q][u]);
+          for (int u = 0; u < RPL; ++u) dv[q][u] = fma(bv[u], wj, dv[q][u]);
         }
       }
 #pragma unroll
@@ -716,10 +717,11 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
         if (sC[i] < 0) continue;
         const int ownp = sOwn[i];
         const double idn = sIdn[i], sc = sSc[i];
-        const double thresh = fmax(floor_rel, cN[i] == kc ? cRel[i * KC + kc - 1] : -1.0);
+        const double thresh = one ? fmax(floor_rel, warp_thresh(wl[wid], kg))
+                                  : fmax(floor_rel, cN[i] == kc ? cRel[i * KC + kc - 1] : -1.0);
         lt.clear();
 #pragma unroll
-        for (int u = 0; u < SRC / 32; ++u) {
+        for (int u = 0; u < RPL; ++u) {
           if (skip & (1u << u)) continue;
           const int r = lane + 32 * u, p = m0 + r;
           const double nv = sN[bf * SRC + r];
@@ -729,6 +731,11 @@ __global__ void __launch_bounds__(RT) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
           if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
         }
         if (!__any_sync(0xffffffffu, lt.rel[0] >= 0.0)) continue;
+        if (one) {
+          warp_merge<KC>(lt, kc, wl[wid], kg, g.sc_order[sC[i]]);
+          __syncwarp();
+          continue;
+        }
         // fold: the case's list joins lane 0's, then kc rounds of warp argmax rewrite it
         if (lane == 0)
           for (int e = 0; e < cN[i]; ++e) lt.insert(cRel[i * KC + e], cPos[i * KC + e], cFlow[i * KC + e]);
@@ -928,8 +935,8 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
 }
 
 namespace {
-size_t rsweep_dyn_bytes(int rs, int kc) {
-  return (2 * (size_t)rs * SRC + 4 * (size_t)SRC + (size_t)RCW * rs + 2 * (size_t)RCW * kc + 2 * RCW) *
+size_t rsweep_dyn_bytes(int rs, int kc, int src) {
+  return (2 * (size_t)rs * src + 4 * (size_t)src + (size_t)RCW * rs + 2 * (size_t)RCW * kc + 2 * RCW) *
              sizeof(double) + ((size_t)RCW * kc + 3 * RCW) * sizeof(int);
 }
 template <int KC>
@@ -942,22 +949,26 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
   else
     k_rsel<KC><<<w.Wb, RT, 0, s>>>(g, c, w);
   if (g.N1 > 0 && g.M > 0) {
-    const size_t dyn = rsweep_dyn_bytes(w.rs, KC);
+    // one case per warp at a time, a single row chunk where M <= 192; on large grids four
+    // cases per warp (their B'' loads shared) -- the test hook BDC_RSWEEP_CQ forces either
+    const char* cq_env = getenv("BDC_RSWEEP_CQ");
+    const int cq = cq_env ? atoi(cq_env) : (g.M <= 2048 ? 1 : 4);
+    const int rpl = cq == 1 && g.M <= 64 ? 2 : cq == 1 && g.M > 128 && g.M <= 192 ? 6 : 4;
+    const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl);
     static bool init = false;
     if (!init) {
-      cudaFuncSetAttribute(k_rsweep<KC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)rsweep_dyn_bytes(RMAX, KC));
-      cudaFuncSetAttribute(k_rsweep<KC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)rsweep_dyn_bytes(RMAX, KC));
+      const int mx = (int)rsweep_dyn_bytes(RMAX, KC, 192);
+      cudaFuncSetAttribute(k_rsweep<KC, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_rsweep<KC, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_rsweep<KC, 1, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_rsweep<KC, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
       init = true;
     }
-    // one case per warp at a time; on large grids four (their B'' loads shared) -- the
-    // test hook BDC_RSWEEP_CQ forces either
-    const char* cq_env = getenv("BDC_RSWEEP_CQ");
-    const int cq = cq_env ? atoi(cq_env) : (g.M <= 16 * SRC ? 1 : 4);
     const dim3 grid(w.nslot - RSEL_WARPS, w.Wb);
-    if (cq == 1) k_rsweep<KC, 1><<<grid, RT, dyn, s>>>(g, c, w);
-    else k_rsweep<KC, 4><<<grid, RT, dyn, s>>>(g, c, w);
+    if (cq != 1) k_rsweep<KC, 4, 4><<<grid, RT, dyn, s>>>(g, c, w);
+    else if (rpl == 2) k_rsweep<KC, 1, 2><<<grid, RT, dyn, s>>>(g, c, w);
+    else if (rpl == 6) k_rsweep<KC, 1, 6><<<grid, RT, dyn, s>>>(g, c, w);
+    else k_rsweep<KC, 1, 4><<<grid, RT, dyn, s>>>(g, c, w);
   }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
