@@ -20,24 +20,163 @@ namespace bdc {
 // (MODF columns with the pre-outage flows of the outaged rows, or the injection
 // column with 1 and the candidate's slot bit), so this is a pure stream over
 // monitored-row chunks.  CTA = (task, tile of 32*TPT candidates); lane = TPT
-// consecutive candidates, warp = up to QW cases (warp-uniform, so the Lo reads are
-// shared-memory broadcasts); the multipliers So stay in registers.
+// consecutive candidates for a batch of QC cases (the multipliers So in registers, the
+// n0 loads shared by the batch's cases); the 8 warps split each chunk's row pairs and
+// their maxima are combined in shared memory at the end of the batch.
 namespace {
 constexpr int OT = 256;        // threads
-constexpr int OW = OT / 32;    // warps
-constexpr int ORC = 32;        // monitored rows per chunk
+constexpr int OW = OT / 32;    // warps (row groups)
+constexpr int ORC = 64;        // monitored rows per chunk
+}  // namespace
+
+template <int MT, int QC, int TPT>
+__global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
+  constexpr int TT = 32 * TPT, LQ = QC * MT;  // candidates per CTA, Lo floats per row
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int t0 = blockIdx.x * TT;
+  if (w.status[b] != 0) return;
+  const int T = w.T, M = g.M, NQ = g.NM + g.NI;
+  extern __shared__ __align__(16) float osm[];
+  float* sN = osm;                   // [2][ORC][TT]  n0 / rating
+  float* sL = sN + 2 * ORC * TT;     // [2][ORC][LQ]  correction columns of the batch
+  __shared__ unsigned sAcc[QC][TT];  // the row groups' maxima (>= 0: ordered as uint)
+  __shared__ float sMax[TT];
+  const float* Lo = w.Lo + (size_t)b * M * NQ * MT;
+  const float* n0s = w.n0s + (size_t)b * M * T;
+  const float* So = w.So + (size_t)b * NQ * MT * T;
+  float* cm = w.cmax + (size_t)b * (g.N1 + NQ) * T;
+  const bool vecN = (T % 4) == 0;
+  for (int i = tid; i < TT; i += OT) sMax[i] = 0.f;
+
+  for (int qb = 0; qb < NQ; qb += QC) {
+    const int nqb = min(QC, NQ - qb), LW = nqb * MT;  // cases / Lo floats of this batch
+    float sv[QC][MT][TPT], acc[QC][TPT];
+#pragma unroll
+    for (int k = 0; k < QC; ++k) {
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int i = 0; i < TPT; ++i) {
+          const int t = t0 + lane * TPT + i;
+          sv[k][j][i] = (k < nqb && t < T) ? So[((size_t)(qb + k) * MT + j) * T + t] : 0.f;
+        }
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) acc[k][i] = 0.f;
+    }
+    for (int i = tid; i < QC * TT; i += OT) (&sAcc[0][0])[i] = 0u;
+    auto issue = [&](int m0, int buf) {
+      if (vecN) {
+        for (int idx = tid; idx < ORC * (TT / 4); idx += OT) {
+          const int rr = idx / (TT / 4), u = 4 * (idx % (TT / 4)), m = m0 + rr;
+          const bool ok = m < M && t0 + u < T;
+          cp16(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+        }
+      } else {
+        for (int idx = tid; idx < ORC * TT; idx += OT) {
+          const int rr = idx / TT, u = idx % TT, m = m0 + rr;
+          const bool ok = m < M && t0 + u < T;
+          cp4(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+        }
+      }
+      // LW = nqb * MT is a multiple of 2; rows of Lo are NQ*MT floats (8-byte aligned)
+      for (int idx = tid; idx < ORC * (LW / 2); idx += OT) {
+        const int rr = idx / (LW / 2), u = 2 * (idx % (LW / 2)), m = m0 + rr;
+        const bool ok = m < M;
+        cp8(&sL[(buf * ORC + rr) * LQ + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
+      }
+      cp_commit();
+    };
+    issue(0, 0);
+    const int nchunks = (M + ORC - 1) / ORC;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nchunks) {
+        issue((ch + 1) * ORC, buf ^ 1);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      // rows past M were staged as zeros (n0 = 0, Lo = 0): |F| = 0 there, so the paired
+      // loop runs over whole chunks; two rows per step: FFMA2 over the row pair (same
+      // rounding as fmaf), one FMNMX3 per accumulator
+      const int rend = min(ORC, (M - ch * ORC + 1) & ~1);
+      for (int rr = 2 * wid; rr < rend; rr += 2 * OW) {
+        const float* n0r = &sN[(buf * ORC + rr) * TT + lane * TPT];
+        float2 n[TPT];
+        if constexpr (TPT == 2) {
+          const float2 a = *reinterpret_cast<const float2*>(n0r);
+          const float2 c = *reinterpret_cast<const float2*>(n0r + TT);
+          n[0] = make_float2(a.x, c.x);
+          n[1] = make_float2(a.y, c.y);
+        } else {
+#pragma unroll
+          for (int i = 0; i < TPT; ++i) n[i] = make_float2(n0r[i], n0r[TT + i]);
+        }
+        const float* lrow0 = &sL[(buf * ORC + rr) * LQ];
+#pragma unroll
+        for (int k = 0; k < QC; ++k) {
+          if (k >= nqb) break;  // uniform
+          float2 l[MT];
+#pragma unroll
+          for (int j = 0; j < MT; j += 2) {
+            const float2 a = *reinterpret_cast<const float2*>(&lrow0[k * MT + j]);
+            const float2 c = *reinterpret_cast<const float2*>(&lrow0[LQ + k * MT + j]);
+            l[j] = make_float2(a.x, c.x);
+            l[j + 1] = make_float2(a.y, c.y);
+          }
+#pragma unroll
+          for (int i = 0; i < TPT; ++i) {
+            float2 f = n[i];
+#pragma unroll
+            for (int j = 0; j < MT; ++j) f = __ffma2_rn(l[j], make_float2(sv[k][j][i], sv[k][j][i]), f);
+            acc[k][i] = max3abs(acc[k][i], f.x, f.y);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // combine the row groups, then per-(case, candidate) maxima (islanded multi cases
+    // contribute 0) and the candidate max
+#pragma unroll
+    for (int k = 0; k < QC; ++k) {
+      if (k >= nqb) break;
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) atomicMax(&sAcc[k][lane * TPT + i], __float_as_uint(acc[k][i]));
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nqb * TT; idx += OT) {
+      const int k = idx / TT, u = idx % TT, q = qb + k, t = t0 + u;
+      const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
+      const float v = ok ? __uint_as_float(sAcc[k][u]) : 0.f;
+      if (t < T) {
+        cm[(size_t)(g.N1 + q) * T + t] = v;
+        atomicMax(reinterpret_cast<unsigned*>(&sMax[u]), __float_as_uint(v));
+      }
+    }
+    __syncthreads();  // sAcc is cleared by the next batch
+  }
+  for (int u = tid; u < TT; u += OT)
+    if (t0 + u < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + u], sMax[u]);
+}
+
+// k_other_w: the same stream for many cases (NQ > 8 with more than 64 candidates): a
+// warp per case (up to QW per warp, the Lo reads shared-memory broadcasts), lanes over
+// TPT candidates each, one pass over the task's n0 for up to 32 cases.
+namespace {
+constexpr int ORC_W = 32;      // monitored rows per chunk (k_other_w)
 }  // namespace
 
 template <int MT, int QW, int TPT>
-__global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
+__global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
   constexpr int TT = 32 * TPT, QB = OW * QW;  // candidates per CTA, cases per batch
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int t0 = blockIdx.x * TT;
   if (w.status[b] != 0) return;
   const int T = w.T, M = g.M, NQ = g.NM + g.NI;
   extern __shared__ __align__(16) float osm[];
-  float* sN = osm;                   // [2][ORC][TT]   n0 / rating
-  float* sL = sN + 2 * ORC * TT;     // [2][ORC][QB*MT] correction columns of the batch
+  float* sN = osm;                   // [2][ORC_W][TT]   n0 / rating
+  float* sL = sN + 2 * ORC_W * TT;     // [2][ORC_W][QB*MT] correction columns of the batch
   __shared__ float sMax[TT];
   const float* Lo = w.Lo + (size_t)b * M * NQ * MT;
   const float* n0s = w.n0s + (size_t)b * M * T;
@@ -64,50 +203,50 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
     }
     auto issue = [&](int m0, int buf) {
       if (vecN) {
-        for (int idx = tid; idx < ORC * (TT / 4); idx += OT) {
+        for (int idx = tid; idx < ORC_W * (TT / 4); idx += OT) {
           const int rr = idx / (TT / 4), u = 4 * (idx % (TT / 4)), m = m0 + rr;
           const bool ok = m < M && t0 + u < T;
-          cp16(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+          cp16(&sN[(buf * ORC_W + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
         }
       } else {
-        for (int idx = tid; idx < ORC * TT; idx += OT) {
+        for (int idx = tid; idx < ORC_W * TT; idx += OT) {
           const int rr = idx / TT, u = idx % TT, m = m0 + rr;
           const bool ok = m < M && t0 + u < T;
-          cp4(&sN[(buf * ORC + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
+          cp4(&sN[(buf * ORC_W + rr) * TT + u], ok ? &n0s[(size_t)m * T + t0 + u] : n0s, ok);
         }
       }
       // LW = nqb * MT is a multiple of 2; rows of Lo are NQ*MT floats (8-byte aligned)
-      for (int idx = tid; idx < ORC * (LW / 2); idx += OT) {
+      for (int idx = tid; idx < ORC_W * (LW / 2); idx += OT) {
         const int rr = idx / (LW / 2), u = 2 * (idx % (LW / 2)), m = m0 + rr;
         const bool ok = m < M;
-        cp8(&sL[(buf * ORC + rr) * QB * MT + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
+        cp8(&sL[(buf * ORC_W + rr) * QB * MT + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
       }
       cp_commit();
     };
     issue(0, 0);
-    const int nchunks = (M + ORC - 1) / ORC;
+    const int nchunks = (M + ORC_W - 1) / ORC_W;
     for (int ch = 0; ch < nchunks; ++ch) {
       const int buf = ch & 1;
       if (ch + 1 < nchunks) {
-        issue((ch + 1) * ORC, buf ^ 1);
+        issue((ch + 1) * ORC_W, buf ^ 1);
         cp_wait<1>();
       } else {
         cp_wait<0>();
       }
       __syncthreads();
-      const int rend = min(ORC, M - ch * ORC);  // zero-filled rows past M are harmless
+      const int rend = min(ORC_W, M - ch * ORC_W);  // zero-filled rows past M are harmless
       (void)rend;
       // two rows per step: FFMA2 over the row pair (same rounding as fmaf), one FMNMX3
 #pragma unroll 2
-      for (int rr = 0; rr < ORC; rr += 2) {
+      for (int rr = 0; rr < ORC_W; rr += 2) {
         float2 n[TPT];
 #pragma unroll
         for (int i = 0; i < TPT; ++i)
-          n[i] = make_float2(sN[(buf * ORC + rr) * TT + lane * TPT + i], sN[(buf * ORC + rr + 1) * TT + lane * TPT + i]);
+          n[i] = make_float2(sN[(buf * ORC_W + rr) * TT + lane * TPT + i], sN[(buf * ORC_W + rr + 1) * TT + lane * TPT + i]);
 #pragma unroll
         for (int k = 0; k < QW; ++k) {
           if (wid + OW * k >= nqb) break;  // warp-uniform
-          const float* lrow0 = &sL[(buf * ORC + rr) * QB * MT + (wid + OW * k) * MT];
+          const float* lrow0 = &sL[(buf * ORC_W + rr) * QB * MT + (wid + OW * k) * MT];
           const float* lrow1 = lrow0 + QB * MT;
           float2 l[MT];
 #pragma unroll
@@ -180,32 +319,57 @@ __global__ void k_select(DevGrid g, DevCfg cfg, Work w) {
 
 // ---------------------------------------------------------------------------- launches
 namespace {
-template <int MT, int QW, int TPT>
+template <int MT, int QC, int TPT>
 void launch_other_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int TT = 32 * TPT;
-  const size_t dyn = (2 * (size_t)ORC * TT + 2 * (size_t)ORC * OW * QW * MT) * sizeof(float);
+  const size_t dyn = (2 * (size_t)ORC * TT + 2 * (size_t)ORC * QC * MT) * sizeof(float);
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_other<MT, QW, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(k_other<MT, QC, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     init = true;
   }
   dim3 grid((w.T + TT - 1) / TT, w.Wb);
-  k_other<MT, QW, TPT><<<grid, OT, dyn, s>>>(g, w);
+  k_other<MT, QC, TPT><<<grid, OT, dyn, s>>>(g, w);
+}
+template <int MT, int QC>
+void launch_other_m(const DevGrid& g, const Work& w, cudaStream_t s) {
+  if (w.T > 32) launch_other_t<MT, QC, 2>(g, w, s);
+  else launch_other_t<MT, QC, 1>(g, w, s);
+}
+template <int MT, int QW, int TPT>
+void launch_other_w(const DevGrid& g, const Work& w, cudaStream_t s) {
+  constexpr int TT = 32 * TPT;
+  const size_t dyn = (2 * (size_t)ORC_W * TT + 2 * (size_t)ORC_W * OW * QW * MT) * sizeof(float);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_other_w<MT, QW, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    init = true;
+  }
+  dim3 grid((w.T + TT - 1) / TT, w.Wb);
+  k_other_w<MT, QW, TPT><<<grid, OT, dyn, s>>>(g, w);
 }
 template <int MT, int QW>
-void launch_other_m(const DevGrid& g, const Work& w, cudaStream_t s) {
-  if (w.T > 64) launch_other_t<MT, QW, 4>(g, w, s);
-  else if (w.T > 32) launch_other_t<MT, QW, 2>(g, w, s);
-  else launch_other_t<MT, QW, 1>(g, w, s);
+void launch_other_wm(const DevGrid& g, const Work& w, cudaStream_t s) {
+  launch_other_w<MT, QW, 4>(g, w, s);
 }
 }  // namespace
 
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s) {
   const int nq = g.NM + g.NI;
   if (nq == 0 || g.M == 0) return;
-  if (g.MT <= 2) launch_other_m<2, 4>(g, w, s);
-  else if (g.MT <= 4) launch_other_m<4, 2>(g, w, s);
-  else launch_other_m<8, 1>(g, w, s);
+  // every lane carries a batch of cases and the warps split the rows; many cases over
+  // more than 64 candidates: a warp per case, one pass over n0 (measured faster there)
+  if (nq > 8 && w.T > 64) {
+    if (g.MT <= 2) launch_other_wm<2, 4>(g, w, s);
+    else if (g.MT <= 4) launch_other_wm<4, 2>(g, w, s);
+    else launch_other_wm<8, 1>(g, w, s);
+  } else if (g.MT <= 2) {
+    launch_other_m<2, 8>(g, w, s);
+  } else if (g.MT <= 4) {
+    launch_other_m<4, 4>(g, w, s);
+  } else {
+    launch_other_m<8, 2>(g, w, s);
+  }
 }
 
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {

@@ -272,7 +272,7 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
         assert warp.reports() == alt.reports()
 
 
-@pytest.mark.parametrize("name,T,k,d", [("g1k", 32, 3, 1), ("g3k", 16, 6, 0)])
+@pytest.mark.parametrize("name,T,k,d", [("g1k", 72, 3, 1), ("g3k", 16, 6, 0)])
 def test_large_grid_matches_oracle(name, T, k, d):
     """Paper-scale synthetic grids exercise the large-grid kernel variants (CTA top-k and
     report selection, multi-chunk report sweep, many tensor-core case tiles) against the
