@@ -142,6 +142,39 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
     srt[tid] = on ? w.rank[b] : -1;  // -1: slot idle
   }
   __syncthreads();
+  // stage chunk ch into buffer bf (thread 0): two TMA tensor tiles of D' (rows x cases,
+  // zero-filled out of bounds) and the tasks' B operand blocks as bulk copies (already in
+  // the core-matrix layout, b32_off), all completing on full[bf]
+  const size_t tf = b32_task_floats(rs, M);
+  int nvalid = 0;
+  for (int k = 0; k < TB; ++k) nvalid += srt[k] >= 0;
+  auto issue = [&](int ch, int bf) {
+    const int m0 = ch * SM_ROWS;
+    const uint32_t bar = smem_u32(&full[bf]);
+    const uint32_t bytes = 2u * DT_BYTES + (uint32_t)(nvalid * KB * BBYTES);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    for (int h = 0; h < 2; ++h)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+              smem_u32(sD + (bf * 2 + h) * (DT_BYTES / 4))),
+          "l"(&tmD), "r"(m0 + 32 * h), "r"(c0), "r"(bar)
+          : "memory");
+    unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
+    for (int k = 0; k < TB; ++k) {
+      if (srt[k] < 0) continue;
+      for (int kb = 0; kb < KB; ++kb) {
+        const float* src = w.B32 + (size_t)(tb0 + k) * tf + ((size_t)ch * KB + kb) * 512;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_u32(Bt + (k * KB + kb) * BBYTES)),
+            "l"(src), "r"(BBYTES), "r"(bar)
+            : "memory");
+      }
+    }
+  };
+
+  // chunk 0 is in flight while the tile's operands and bounds are prepared
+  if (tid == 0) issue(0, 0);
   for (int i = tid; i < TB * RMAX; i += NT) {
     const int k = i / RMAX, d = i % RMAX;
     if (d < snd[k]) sdead[k][d] = g.row_mon_pos[w.dead[(size_t)(tb0 + k) * RMAX + d]];  // -1: unmonitored
@@ -183,37 +216,6 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
       ownloose |= fabs(1.0 - den) > 0.999 * fabs(den);
     }
 
-  // stage chunk ch into buffer bf (thread 0): two TMA tensor tiles of D' (rows x cases,
-  // zero-filled out of bounds) and the tasks' B operand blocks as bulk copies (already in
-  // the core-matrix layout, b32_off), all completing on full[bf]
-  const size_t tf = b32_task_floats(rs, M);
-  int nvalid = 0;
-  for (int k = 0; k < TB; ++k) nvalid += srt[k] >= 0;
-  auto issue = [&](int ch, int bf) {
-    const int m0 = ch * SM_ROWS;
-    const uint32_t bar = smem_u32(&full[bf]);
-    const uint32_t bytes = 2u * DT_BYTES + (uint32_t)(nvalid * KB * BBYTES);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-    for (int h = 0; h < 2; ++h)
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-              smem_u32(sD + (bf * 2 + h) * (DT_BYTES / 4))),
-          "l"(&tmD), "r"(m0 + 32 * h), "r"(c0), "r"(bar)
-          : "memory");
-    unsigned char* Bt = sBt + bf * TB * KB * BBYTES;
-    for (int k = 0; k < TB; ++k) {
-      if (srt[k] < 0) continue;
-      for (int kb = 0; kb < KB; ++kb) {
-        const float* src = w.B32 + (size_t)(tb0 + k) * tf + ((size_t)ch * KB + kb) * 512;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                smem_u32(Bt + (k * KB + kb) * BBYTES)),
-            "l"(src), "r"(BBYTES), "r"(bar)
-            : "memory");
-      }
-    }
-  };
-
   const int nchunks = (M + SM_ROWS - 1) / SM_ROWS;
   float mx[TB], mxb[TB][SB];  // running max of the current block; finished blocks
 #pragma unroll
@@ -232,7 +234,6 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
       mx[k] = 0.f;
     }
   };
-  if (tid == 0) issue(0, 0);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
