@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
 // top-kg and the kg-th case value are kg rounds of warp argmax (same order as k_rsel:
 // value desc, index asc); the warp's list is partial slot 0 (slots 1..RW-1 empty).
 template <int KC, int NCW>
-__global__ void __launch_bounds__(RT) k_rsel_w(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int b = blockIdx.x * RW + wid;
   __shared__ WarpList wl[RW];
