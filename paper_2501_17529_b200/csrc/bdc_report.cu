@@ -274,7 +274,7 @@ __device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q,
 // bound (exact FP32 max, or the dominance bound m0 + scale_c |s(c,t)| of a pair the
 // sweep skipped) is >= kth - 2 eps is visited; the metric's binding case is one of them.
 template <int KC>
-__global__ void __launch_bounds__(RT) k_rsel(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT, 3) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   const int b = blockIdx.x;
   if (w.status[b] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
