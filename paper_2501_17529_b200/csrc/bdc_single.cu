@@ -471,9 +471,9 @@ void launch_pairs_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream
 // tile shapes: 16 cases x top_tile_cands(T) candidates (bdc_device.cuh)
 void launch_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   // thread tile 2 cases x 8 or 4 candidates; 2 or 4 row groups split each chunk's rows
-  if (w.T >= 96) launch_top_t<2, 8, 8, 16, 64, 2, 2>(g, c, w, s);       // 16 cases x 128 candidates
-  else if (w.T >= 48) launch_top_t<2, 4, 8, 16, 64, 2, 2>(g, c, w, s);  // 16 x 64
-  else launch_top_t<2, 4, 8, 8, 64, 4, 2>(g, c, w, s);                 // 16 x 32
+  if (w.T >= 96) launch_top_t<2, 8, 8, 16, 64, 2, 3>(g, c, w, s);       // 16 cases x 128 candidates
+  else if (w.T >= 48) launch_top_t<2, 4, 8, 16, 64, 2, 3>(g, c, w, s);  // 16 x 64
+  else launch_top_t<2, 4, 8, 8, 64, 4, 3>(g, c, w, s);                 // 16 x 32
 }
 void launch_pairs(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   if (w.T >= 96) launch_pairs_t<2, 8, 8, 16, 64, 2, 2>(g, c, w, s);
