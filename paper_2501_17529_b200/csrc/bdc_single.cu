@@ -476,9 +476,9 @@ void launch_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s
   else launch_top_t<2, 4, 8, 8, 64, 4, 3>(g, c, w, s);                 // 16 x 32
 }
 void launch_pairs(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  if (w.T >= 96) launch_pairs_t<2, 8, 8, 16, 64, 2, 2>(g, c, w, s);
-  else if (w.T >= 48) launch_pairs_t<2, 4, 8, 16, 64, 2, 2>(g, c, w, s);
-  else launch_pairs_t<2, 4, 8, 8, 64, 4, 2>(g, c, w, s);
+  if (w.T >= 96) launch_pairs_t<2, 8, 8, 16, 64, 2, 3>(g, c, w, s);
+  else if (w.T >= 48) launch_pairs_t<2, 4, 8, 16, 64, 2, 3>(g, c, w, s);
+  else launch_pairs_t<2, 4, 8, 8, 64, 4, 3>(g, c, w, s);
 }
 }  // namespace
 
