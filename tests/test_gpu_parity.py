@@ -275,7 +275,8 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
 @pytest.mark.parametrize("name,T,k,d", [("g1k", 72, 3, 1), ("g3k", 16, 6, 0)])
 def test_large_grid_matches_oracle(name, T, k, d):
     """Paper-scale synthetic grids exercise the large-grid kernel variants (CTA top-k and
-    report selection, multi-chunk report sweep, many tensor-core case tiles) against the
+    report selection, multi-chunk report sweep, many tensor-core case tiles, the
+    warp-per-case multi/injection stream at G1k's 11 cases x 72 candidates) against the
     CPU oracle: feasibility and reasons exact, metric within TAU, winner metric-minimal."""
     from paper_2501_17529_b200 import synth
     from paper_2501_17529_b200.session import session_open, solve_batch_output
