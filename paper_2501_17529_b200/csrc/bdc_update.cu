@@ -884,12 +884,12 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   if (dyn > opted) {
     const int mx = (int)update_dyn_bytes(RMAX, EMAX);
     cudaFuncSetAttribute(k_update<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_update<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_update<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_update<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     opted = update_dyn_bytes(RMAX, EMAX);
   }
   if (g.R > 2048) k_update<512, 1><<<w.Wb, 512, dyn, st>>>(g, c, w);
-  else if (g.R > 512) k_update<256, 3><<<w.Wb, 256, dyn, st>>>(g, c, w);
+  else if (g.R > 512) k_update<256, 4><<<w.Wb, 256, dyn, st>>>(g, c, w);
   else k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
   if (w.NTERM > 0 && g.M > 0) {
     const int work = g.M + w.NTERM * w.T;
