@@ -885,10 +885,10 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
     const int mx = (int)update_dyn_bytes(RMAX, EMAX);
     cudaFuncSetAttribute(k_update<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_update<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_update<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_update<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     opted = update_dyn_bytes(RMAX, EMAX);
   }
-  if (g.R > 2048) k_update<512, 1><<<w.Wb, 512, dyn, st>>>(g, c, w);
+  if (g.R > 2048) k_update<512, 2><<<w.Wb, 512, dyn, st>>>(g, c, w);
   else if (g.R > 512) k_update<256, 4><<<w.Wb, 256, dyn, st>>>(g, c, w);
   else k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
   if (w.NTERM > 0 && g.M > 0) {
