@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w)
 // top-kg by (rel desc, case order, position) (_merge_entries, solver.py:302-318); the
 // CTA merges its warps' lists into one partial slot.
 template <int KC, int CQ, int RPL>  // CQ: cases per warp evaluated together; RPL: rows per lane
-__global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 2) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+__global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
   constexpr int SRC = 32 * RPL;  // monitored rows per chunk
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
