@@ -170,6 +170,9 @@ typedef struct {
   float stage_ms[BDC_STAGES];  /* see BDC_STAGE_* */
   int32_t waves;
   int32_t kernel_launches;
+  int64_t* rescore_stats;    /* (3) optional: [0] candidates re-scored in FP64 (the winner's
+                                near-tie band, solver.py:804-823), [1] tasks whose FP32 argmin
+                                the FP64 re-score replaced, [2] tasks with a band of > 1 */
 } BdcBatch;
 
 int bdc_device_count(int* count);
@@ -186,7 +189,9 @@ int bdc_solve(BdcSession* session, BdcBatch* batch);
 
 /* Flows of one task for every candidate (candidate_case_flows):
  * n0 (R, T) and n1 (NC, R, T) in contingency order, FP64, NaN rows for
- * islanded cases; case_ok (NC).  Host pointers. */
+ * islanded cases; case_ok (NC).  Host pointers.  The flows are written when
+ * *status is BDC_TASK_OK or BDC_TASK_ISLAND_ERROR (then case_ok names the
+ * islanded cases); other statuses leave them untouched. */
 int bdc_probe_flows(BdcSession* session, const uint8_t* splits, const int64_t* discos,
                     int32_t D, const uint8_t* inj, int32_t T, double* n0, double* n1,
                     uint8_t* case_ok, int32_t* status, int32_t* status_arg);

@@ -28,20 +28,10 @@ from .grid import (
     build_grid,
     static_injection_fold,
 )
-from .io import (
-    grid_from_dict,
-    grid_to_dict,
-    load_grid,
-    read_tasks,
-    result_to_dict,
-    save_grid,
-    task_from_dict,
-    task_to_dict,
-    write_results,
-    write_tasks,
-)
+from .io import grid_from_dict, grid_to_dict, load_grid, result_to_dict
 from .ptdf import PtdfMatrix, compute_ptdf, prepare_base_ptdf, reduce_static
 from .solver import (
+    CaseFlows,
     Instrumentation,
     SolveConfig,
     SolveResult,
@@ -49,6 +39,7 @@ from .solver import (
     SplitAction,
     TaskDiagnostics,
     TopologyTask,
+    candidate_case_flows,
     canonicalize_task,
     solve_batch,
 )

@@ -16,12 +16,12 @@ FLAGS = [
     "-lineinfo",
     "-gencode",
     "arch=compute_100a,code=sm_100a",
-    "-shared",
     "-Xcompiler",
     "-fPIC",
     "-Xcompiler",
     "-O3",
 ]
+OBJDIR = os.path.join(HERE, "build")
 
 
 def nvcc() -> str:
@@ -43,9 +43,22 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return TARGET
-    srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES]
+    # one nvcc per translation unit, in parallel, then one link
+    os.makedirs(OBJDIR, exist_ok=True)
+    procs = []
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        cmd = [nvcc()] + FLAGS + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((src, subprocess.Popen(cmd)))
+        objs.append(obj)
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
     tmp = TARGET + ".tmp"
-    cmd = [nvcc()] + FLAGS + ["-o", tmp] + srcs
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <cstdlib>
 #include <cudaTypedefs.h>
@@ -59,7 +60,7 @@ struct BdcSession {
   int64_t wave_cap = 0;
   size_t total_mem = 0;
   std::vector<int32_t> sub_count, slots_per_sub;  // host copies for bdc_scan_tasks
-  std::vector<double> inv_rating;                 // host copy: report loadings = |flow| / rating
+  std::vector<double> rating;                     // host copy: report loadings = |flow| / rating
   // pinned host staging for outputs bound for pageable host memory, reused across calls
   std::vector<std::pair<char*, size_t>> pin_free;
   // cached wave workspaces (one per concurrent call), reused across calls
@@ -131,6 +132,36 @@ struct PinLease {
   }
 };
 }  // namespace
+
+namespace bdc {
+namespace {
+std::mutex g_optin_mu;
+std::map<std::pair<int, const void*>, int> g_optin;  // (device, kernel) -> opted-in bytes
+}  // namespace
+
+cudaError_t smem_opt_in(const void* fn, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_optin_mu);
+  int& have = g_optin[{dev, fn}];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+int smem_opt_in_max(const void* fn) {
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  const int mx = optin - (int)fa.sharedSizeBytes;
+  smem_opt_in(fn, mx);
+  return mx;
+}
+}  // namespace bdc
 
 extern "C" {
 
@@ -275,7 +306,7 @@ int bdc_session_create(const BdcGrid* G, const BdcConfig* C, int device, BdcSess
   UP(ic_order, G->NI);
 #undef UP
   if (e == cudaSuccess) e = upload((const double*)inv.data(), inv.size(), &g.inv_rating, o);
-  s->inv_rating = inv;
+  s->rating.assign(G->rating, G->rating + G->M);
   if (e != cudaSuccess) {
     for (void* p : o) cudaFree(p);
     delete s;
@@ -422,7 +453,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
   size_t o_b32 = L.add(B * b32_task_floats(rs, g.M) * 4), o_bmx = L.add(B * (size_t)rs * 4);
   size_t o_smx = L.add(B * (size_t)g.N1 * 4);
-  size_t o_lf = L.add(32), o_bs = L.add(16);
+  size_t o_lf = L.add(64), o_bs = L.add(16), o_rsq = L.add(B * 4);
   if (!base) return L.total;
   Work& x = *w;
   x.Wb = Wb; x.T = T; x.D = D; x.Ein = Ein; x.rs = rs; x.Cs = Cs; x.NCw = NCw;
@@ -456,6 +487,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.lf = (unsigned long long*)(base + o_lf);
   x.bsdf = x.lf + 1;
   x.pairs = x.lf + 2;
+  x.rsq = (int*)(base + o_rsq);
+  x.rsq_n = (unsigned*)(base + o_bs) + 1;  // FP64 re-score queue length, zeroed per wave
   x.qcount = (unsigned*)(base + o_bs);  // k_pairs queue length, zeroed per wave
   x.m0 = (float*)(base + o_m0); x.scale = (float*)(base + o_sc);
   x.s32 = (float*)(base + o_s32); x.bkey = (uint32_t*)(base + o_bk); x.rmax = (float*)(base + o_rmx);
@@ -564,7 +597,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     w.rsel_cta = (rc && rc[0] == '1') ? 1 : 0;
   }
   w.ranked = (w.screen && g.N1 > w.ptop) ? 1 : 0;
-  CK(cudaMemsetAsync(w.lf, 0, 32, st));
+  CK(cudaMemsetAsync(w.lf, 0, 64, st));
 
   const int nwaves = (int)((B + Wb - 1) / Wb);
   constexpr int NE = BDC_STAGES + 1;  // events per wave
@@ -574,7 +607,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   const int kg = s->cfg.kg, NCw = w.NCw;
   // pinned staging for host outputs: two wave-sized buffers, unpacked by the host while
   // the next wave runs; report loadings are recomputed on the host as |flow| / rating
-  // (bit-identical to the device's fabs(flow) * inv_rating), so they are not copied
+  // (true division, as the reference's np.abs(flows) / ratings, solver.py:293), so they are not copied
   OutLayout olay{};
   std::unique_ptr<PinLease> pin[2];
   cudaEvent_t wdone[2] = {nullptr, nullptr};
@@ -599,8 +632,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     const OutLayout& O = olay;
     const int64_t b0 = staged_b0[slot];
     const size_t nb = (size_t)staged_nb[slot];
-    const double* inv = s->inv_rating.data();
-    const int M = (int)s->inv_rating.size();
+    const double* rat = s->rating.data();
+    const int M = (int)s->rating.size();
     // tasks [t0, t1) of the staged wave into the caller's arrays (first-touch page faults
     // and copies dominate for large waves: a few host threads share them)
     auto part = [&](size_t t0, size_t t1) {
@@ -629,7 +662,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
         double* d = dst + b0 * kg;
         for (size_t i = t0 * kg; i < t1 * (size_t)kg; ++i) {
           const int p = pos[i];
-          d[i] = (p >= 0 && p < M) ? std::fabs(fl[i]) * inv[p] : 0.0;
+          d[i] = (p >= 0 && p < M) ? std::fabs(fl[i]) / rat[p] : 0.0;
         }
       };
       rel(bt->n0_rel, O.n0pos, O.n0flow);
@@ -697,7 +730,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0b, 0, (size_t)nb * SB * T * 4, st);
-    if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 8, st);  // k_pairs queue, re-score queue
     if (err == cudaSuccess) err = cudaMemsetAsync(x.lcnt, 0, (size_t)nb * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
     // zero padding of the tensor-core operand (rank slots past the task's rank, rows past M)
@@ -789,10 +822,16 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     err = e2;
   }
   if (!ondev_out && err == cudaSuccess) err = unpack((nwaves - 1) & 1);
-  unsigned long long counters[4] = {0, 0, 0, 0};
-  if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 32, cudaMemcpyDeviceToHost, st);
+  unsigned long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(counters, w.lf, 64, cudaMemcpyDeviceToHost, st);
   cudaError_t es = cudaStreamSynchronize(st);
   if (err == cudaSuccess) err = es;
+  // a copy of the next wave's inputs may still be in flight on the copy stream (error
+  // break): it must land before the workspace goes back to the session cache
+  if (overlap_in) {
+    es = cudaStreamSynchronize(cs.s);
+    if (err == cudaSuccess) err = es;
+  }
   if (err == cudaSuccess) {
     for (int wv = 0; wv < nwaves; ++wv) {
       cudaEvent_t* E = &ev[(size_t)wv * NE];
@@ -810,6 +849,11 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (bt->bsdf_applications) *bt->bsdf_applications = (int64_t)counters[1];
   if (bt->n1_pairs) *bt->n1_pairs = (int64_t)counters[2];
   if (bt->report_cases) *bt->report_cases = (int64_t)counters[3];
+  if (bt->rescore_stats) {
+    bt->rescore_stats[0] = (int64_t)counters[4];
+    bt->rescore_stats[1] = (int64_t)counters[5];
+    bt->rescore_stats[2] = (int64_t)counters[6];
+  }
   bt->waves = nwaves;
   bt->kernel_launches = launches;
   return BDC_OK;
@@ -839,7 +883,7 @@ extern "C" int bdc_probe_flows(BdcSession* s, const uint8_t* splits, const int64
   cudaError_t e = cudaMalloc(&dn0, (size_t)g.R * T * 8);
   if (e == cudaSuccess) e = cudaMalloc(&dn1, n1n * 8 + 8);
   if (e == cudaSuccess) e = cudaMalloc(&dok, g.NC + 1);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w.lf, 0, 32, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.lf, 0, 64, st);
   if (e == cudaSuccess && g.S) e = cudaMemcpyAsync((void*)w.splits, splits, (size_t)g.S * Ein, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && D) e = cudaMemcpyAsync((void*)w.discos, discos, (size_t)D * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && g.K) e = cudaMemcpyAsync((void*)w.inj, inj, (size_t)T * g.K, cudaMemcpyHostToDevice, st);
@@ -852,7 +896,9 @@ extern "C" int bdc_probe_flows(BdcSession* s, const uint8_t* splits, const int64
     if (e == cudaSuccess) e = cudaMemcpyAsync(hs + 1, w.sarg, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
-  if (e == cudaSuccess && hs[0] == 0) {
+  // islanding_policy = "error" still evaluates every case (its case_ok flags name the
+  // islanded cases the reference reports, solver.py:501-511)
+  if (e == cudaSuccess && (hs[0] == BDC_TASK_OK || hs[0] == BDC_TASK_ISLAND_ERROR)) {
     launch_probe(g, w, dn0, dn1, dok, st);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(n0, dn0, (size_t)g.R * T * 8, cudaMemcpyDeviceToHost, st);

@@ -22,6 +22,14 @@ constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors
 // path's observed error is ~1e-6 (tests: <= 1e-5 enforced), so 1e-3 is a
 // >= 100x safety factor; a wider margin only costs report time.
 constexpr float SCREEN_EPS = 1e-3f;
+// Half-width of the winner's near-tie band, relative to max(1, metric): a bound on
+// |m32(t) - m64(t)| between a candidate's FP32 screening metric and its FP64 metric.  The
+// FP32 flows are FP64 values rounded once and combined by one FFMA (observed error
+// ~1.3e-6, tests enforce <= 1e-5); 2^-14 = 6.1e-5 keeps a > 40x margin.  Every candidate
+// with m32 within 2 RESCORE_EPS of the FP32 minimum is re-scored in FP64 (k_rescore), so
+// best_injection is the first argmin of the FP64 metrics, as the reference's
+// (solver.py:804-823).
+constexpr float RESCORE_EPS = 6.103515625e-05f;
 // Single-branch N-1 stage with the exact dominance screen (bdc_single.cu):
 //   TOPC  cases evaluated first for every candidate (the top of the screening ranking);
 //   SB    row blocks of the screening bound |F(r,c,t)| <= max_b (m0_b(t) + scale_bc |s(c,t)|):
@@ -124,6 +132,8 @@ struct Work {
                   //               in the tensor-core operand layout (b32_off)
   float* bmax;    // (Wb, rs)      max_r |B''(r,j)|/rating_r (float bits, atomicMax)
   unsigned long long* pairs;  // evaluated (single case, candidate) pairs, all tasks
+  int* rsq;       // (Wb)          tasks whose winner band holds more than one candidate
+  unsigned* rsq_n;  // their number (device counter, reset per wave)
   int screen;     // 1 = exact dominance screen on
   int rsel_cta;   // 1: winner report selection always CTA-per-task (test knob BDC_RSEL_CTA)
   int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
@@ -158,7 +168,9 @@ struct Work {
   double* metric; int64_t* best; uint8_t* feasible;
   int* n0cnt; int* n0pos; double* n0flow; double* n0rel;
   int* n1cnt; int* n1case; int* n1pos; double* n1flow; double* n1rel;
-  unsigned long long* lf;     // loadflow counter
+  unsigned long long* lf;     // counters: [0] loadflows [1] bsdf [2] evaluated pairs
+                              // [3] report cases [4] re-scored candidates [5] winners
+                              // replaced by the re-score [6] tasks with a band > 1
   unsigned long long* bsdf;   // split applications counter
 };
 
@@ -299,6 +311,15 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 
+// Dynamic shared-memory opt-in, per (device, kernel): cudaFuncSetAttribute applies to the
+// current device only, so a process-wide "done" flag would leave a second device (or a
+// second session on another device) without it.  Thread-safe; the lookup is a mutex and a
+// small map, cheap next to a launch.
+//   smem_opt_in(fn, bytes)  ensures the kernel may launch with `bytes` of dynamic smem;
+//   smem_opt_in_max(fn)     opts in to everything the static part leaves free, returns it.
+cudaError_t smem_opt_in(const void* fn, int bytes);
+int smem_opt_in_max(const void* fn);
+
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
@@ -308,6 +329,7 @@ void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_rescore(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s);
 int kernels_per_wave(const DevGrid& g, const Work& w);

@@ -309,11 +309,25 @@ __global__ void k_select(DevGrid g, DevCfg cfg, Work w) {
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
   }
+  // near-tie band: candidates whose FP32 metric lies within 2 E of the minimum may be the
+  // FP64 argmin (|m32 - m64| <= E); more than one -> queue the task for k_rescore
+  const float hi = bv + 2.f * RESCORE_EPS * fmaxf(1.f, bv);
+  int nband = 0;
+  for (int t = lane; t < tn; t += 32) {
+    float v = __uint_as_float(w.m32[(size_t)b * T + t]);
+    if (pen) v = fmaxf(v, penalty);
+    nband += v <= hi;
+  }
+  for (int o = 16; o; o >>= 1) nband += __shfl_xor_sync(0xffffffffu, nband, o);
   if (lane == 0) {
     w.best[b] = bi;
     w.feasible[b] = 1;
     const int nf = g.NC - w.nisl[b];
     atomicAdd(w.lf, (unsigned long long)tn * (unsigned long long)(1 + nf));
+    if (nband > 1) {
+      w.rsq[atomicAdd(w.rsq_n, 1u)] = b;
+      atomicAdd(w.lf + 6, 1ull);
+    }
   }
 }
 
@@ -323,11 +337,7 @@ template <int MT, int QC, int TPT>
 void launch_other_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int TT = 32 * TPT;
   const size_t dyn = (2 * (size_t)ORC * TT + 2 * (size_t)ORC * QC * MT) * sizeof(float);
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_other<MT, QC, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    init = true;
-  }
+  smem_opt_in((const void*)k_other<MT, QC, TPT>, (int)dyn);
   dim3 grid((w.T + TT - 1) / TT, w.Wb);
   k_other<MT, QC, TPT><<<grid, OT, dyn, s>>>(g, w);
 }
@@ -340,11 +350,7 @@ template <int MT, int QW, int TPT>
 void launch_other_w(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int TT = 32 * TPT;
   const size_t dyn = (2 * (size_t)ORC_W * TT + 2 * (size_t)ORC_W * OW * QW * MT) * sizeof(float);
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_other_w<MT, QW, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    init = true;
-  }
+  smem_opt_in((const void*)k_other_w<MT, QW, TPT>, (int)dyn);
   dim3 grid((w.T + TT - 1) / TT, w.Wb);
   k_other_w<MT, QW, TPT><<<grid, OT, dyn, s>>>(g, w);
 }
@@ -376,6 +382,7 @@ void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   const int threads = 256;
   const long long total = (long long)w.Wb * 32;
   k_select<<<(unsigned)((total + threads - 1) / threads), threads, 0, s>>>(g, c, w);
+  launch_rescore(g, c, w, s);
 }
 
 }  // namespace bdc

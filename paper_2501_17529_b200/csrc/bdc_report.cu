@@ -12,6 +12,7 @@
 // reference's bound-stop implements, solver.py:686-695).
 #include "bdc_device.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -186,6 +187,50 @@ __device__ __forceinline__ float pair_bound(const DevGrid& g, const Work& w, int
   return ub;
 }
 
+// FP64 post-contingency flows, one expression each, shared by the winner report and the
+// FP64 re-score (k_rescore) so that both see the same bits.
+// Single-branch case: F = n0 + (D''(r, c) / den_c) n0(r_c), and exactly n0 - n0(r_c) = 0 on
+// the outaged row itself (the LODF self factor -1, solver.py:498-503, 612-613).
+__device__ __forceinline__ double single_flow(double nv, double dv, double idn, double sc, bool own) {
+  return own ? fma(-1.0, sc, nv) : fma(dv * idn, sc, nv);
+}
+// Multi-branch case (st, m): F = n0 + sum_j MODF(row, j) n0(r_j) with MODF = D''[:, O] inner^-1
+// (compute_modf / apply_modf_to_ptdf, factors.py:373-425; _case_flows, solver.py:614-618);
+// the outaged rows get the -e_j row (flow exactly 0).  own = which outaged branch `row` is.
+__device__ __forceinline__ double multi_flow(const DevGrid& g, const Work& w, int b, int st, int m, int row,
+                                             double n0r, const double* sv, const double* minv,
+                                             const double* Bm, int rt, int& own) {
+  const int R = g.R, rs = w.rs;
+  own = -1;
+  for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
+  double f = n0r;
+  if (own >= 0) {
+    for (int j = 0; j < m; ++j) f = fma(j == own ? -1.0 : 0.0, sv[j], f);
+  } else {
+    double Dv[MMAX];
+    for (int i = 0; i < m; ++i) {
+      double v = g.Dm64[(size_t)(st + i) * R + row];
+      const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
+      for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
+      Dv[i] = v;
+    }
+    for (int j = 0; j < m; ++j) {
+      double l = 0.0;
+      for (int i = 0; i < m; ++i) l = fma(Dv[i], minv[i * m + j], l);
+      f = fma(l, sv[j], f);
+    }
+  }
+  return f;
+}
+// Injection case: F = n0 - setpoint * P''[:, col_t] (solver.py:619-622), the column of the
+// candidate's slot bit in rank-coefficient form.
+__device__ __forceinline__ double inj_flow(const DevGrid& g, int ca, const double* coef, double sp, int row,
+                                           double n0r, const double* Bm, int rt) {
+  double pc = g.P0T[(size_t)ca * g.R + row];
+  for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * g.R + row], coef[j], pc);
+  return fma(-pc, sp, n0r);
+}
+
 // One multi-branch or injection case q (q < NM: multi) of the winner, FP64, one warp:
 // lanes over monitored rows keep stable top-kc lists (entries >= the list floor),
 // merged into the warp list L with the case's order.  Updates the lane's running max.
@@ -217,25 +262,8 @@ __device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q,
     for (int p = lane; p < M; p += 32) {
       const int row = g.mon_row[p];
       if (is_dead(sdead, nd, row)) continue;
-      int own = -1;
-      for (int a = 0; a < m; ++a) if (g.mb_row[st + a] == row) own = a;
-      double f = n0b[row];
-      if (own >= 0) {
-        for (int j = 0; j < m; ++j) f += (j == own ? -1.0 : 0.0) * sv[j];
-      } else {
-        double Dv[MMAX];
-        for (int i = 0; i < m; ++i) {
-          double v = g.Dm64[(size_t)(st + i) * R + row];
-          const double* Wq = w.Wm + ((size_t)b * g.NMB + st + i) * rs;
-          for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * R + row], Wq[j], v);
-          Dv[i] = v;
-        }
-        for (int j = 0; j < m; ++j) {
-          double l = 0.0;
-          for (int i = 0; i < m; ++i) l += Dv[i] * sMinv[i * m + j];
-          f += l * sv[j];
-        }
-      }
+      int own;
+      const double f = multi_flow(g, w, b, st, m, row, n0b[row], sv, sMinv, Bm, rt, own);
       const double rel = fabs(f) * g.inv_rating[p];
       mymax = fmax(mymax, rel);
       if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
@@ -249,9 +277,7 @@ __device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q,
     for (int p = lane; p < M; p += 32) {
       const int row = g.mon_row[p];
       if (is_dead(sdead, nd, row)) continue;
-      double pc = g.P0T[(size_t)ca * R + row];
-      for (int j = 0; j < rt; ++j) pc = fma(Bm[(size_t)j * R + row], coef[j], pc);
-      const double f = n0b[row] - pc * sp;
+      const double f = inj_flow(g, ca, coef, sp, row, n0b[row], Bm, rt);
       const double rel = fabs(f) * g.inv_rating[p];
       mymax = fmax(mymax, rel);
       if (rel >= thresh) lt.insert(rel, p, f);
@@ -354,7 +380,7 @@ __global__ void __launch_bounds__(RT, 3) k_rsel(DevGrid g, DevCfg cfg, Work w) {
       const double f = n0b[g.mon_row[p]];
       w.n0pos[(size_t)b * kg + i] = p;
       w.n0flow[(size_t)b * kg + i] = f;
-      w.n0rel[(size_t)b * kg + i] = fabs(f) * g.inv_rating[p];
+      w.n0rel[(size_t)b * kg + i] = fabs(f) / g.rating[p];  // np.abs(flows) / ratings
     }
     if (lane == 0) w.n0cnt[b] = n;
   } else if (wid == 1) {
@@ -498,7 +524,7 @@ __global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w)
       const double f = n0m[bi];
       w.n0pos[(size_t)b * kg + e] = bi;
       w.n0flow[(size_t)b * kg + e] = f;
-      w.n0rel[(size_t)b * kg + e] = fabs(f) * g.inv_rating[bi];
+      w.n0rel[(size_t)b * kg + e] = fabs(f) / g.rating[bi];
     }
 #pragma unroll
     for (int k = 0; k < NCW; ++k)
@@ -725,7 +751,7 @@ __global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCf
           if (skip & (1u << u)) continue;
           const int r = lane + 32 * u, p = m0 + r;
           const double nv = sN[bf * SRC + r];
-          const double f = (p == ownp) ? nv + (-1.0) * sc : nv + (dv[q][u] * idn) * sc;
+          const double f = single_flow(nv, dv[q][u], idn, sc, p == ownp);
           const double rel = fabs(f) * sI[bf * SRC + r];
           mymax = fmax(mymax, rel);
           if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
@@ -851,7 +877,7 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
       w.n1case[(size_t)b * kg + e] = bc;
       w.n1pos[(size_t)b * kg + e] = bp;
       w.n1flow[(size_t)b * kg + e] = w.pflow[base + bi];
-      w.n1rel[(size_t)b * kg + e] = br;
+      w.n1rel[(size_t)b * kg + e] = fabs(w.pflow[base + bi]) / g.rating[bp];  // true division, as agg_i
     }
     pr = br; pc = bc; pp = bp;
     ++cnt;
@@ -860,6 +886,230 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
     if (w.nisl[b] > 0) mx = fmax(mx, cfg.penalty);
     w.metric[b] = mx;
     w.n1cnt[b] = cnt;
+  }
+}
+
+// -------------------------------------------------------------------------- k_rescore
+// FP64 re-score of the winner's near-tie band (solver.py:804-823: best = the first argmin
+// of the FP64 metrics).  k_select took the first FP32 argmin (value vmin) and queued the
+// tasks with more than one candidate within 2E of it, E = RESCORE_EPS max(1, vmin) bounding
+// |m32 - m64|: the FP64 argmin is one of them.  A CTA per queued task walks the band in
+// ascending candidate order with the running FP64 minimum best64:
+//   * a candidate with v(t) - E >= best64 cannot beat it (m64 >= v - E);
+//   * with islanded cases, one with m32 + E < penalty has m64 = penalty exactly;
+//   * one with the same y_t and injection-case slot bits as an earlier re-scored candidate
+//     has bit-identical flows, so the earlier index wins the tie;
+//   * any other is re-evaluated in FP64: the N-0 column and every case whose FP32 upper
+//     bound (exact FP32 maximum, or the dominance bound of a skipped pair) reaches
+//     v(t) - 2E, through the winner report's flow expressions, so the metric reported for
+//     the chosen candidate is the very value it was chosen by.
+// Once best64 equals the islanding penalty nothing can be smaller and the walk stops.
+namespace {
+constexpr int RREP = 64;  // re-scored candidates remembered for the duplicate test
+
+// FP64 max |F|/rating of one multi-branch or injection case q for candidate t (one warp);
+// the arithmetic of other_case_report.
+__device__ double other_case_max(const DevGrid& g, const Work& w, int b, int q, int t, const double* n0b,
+                                 const int* sdead, int nd, double* sMinv) {
+  const int lane = threadIdx.x & 31;
+  const int M = g.M, rt = w.rank[b];
+  const double* Bm = w.Bm + (size_t)b * w.rs * g.R;
+  double mx = 0.0;
+  if (q < g.NM) {
+    const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+    for (int i = lane; i < m * m; i += 32) sMinv[i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
+    __syncwarp();
+    double sv[MMAX];
+    for (int j = 0; j < m; ++j) sv[j] = n0b[g.mb_row[st + j]];
+    for (int p = lane; p < M; p += 32) {
+      const int row = g.mon_row[p];
+      if (is_dead(sdead, nd, row)) continue;
+      int own;
+      const double f = multi_flow(g, w, b, st, m, row, n0b[row], sv, sMinv, Bm, rt, own);
+      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+    }
+    __syncwarp();
+  } else {
+    const int qi = q - g.NM, sl = g.ic_slot[qi];
+    const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
+    const bool bit = sl >= 0 && w.inj[((size_t)b * w.T + t) * g.K + sl];
+    const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * g.NI + qi) * w.rs;
+    const double sp = g.ic_sp[qi];
+    for (int p = lane; p < M; p += 32) {
+      const int row = g.mon_row[p];
+      if (is_dead(sdead, nd, row)) continue;
+      const double f = inj_flow(g, ca, coef, sp, row, n0b[row], Bm, rt);
+      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+    }
+  }
+  return mx;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ int sdead[RMAX], sdeadp[RMAX];
+  __shared__ double sY[RMAX];
+  __shared__ double sMinv[RW][MMAX * MMAX];
+  __shared__ int sList[RT];
+  __shared__ int sCnt[RW];
+  __shared__ int sRep[RREP];
+  __shared__ double sRed[RW];
+  __shared__ int sDup;
+  const int R = g.R, M = g.M, N1 = g.N1, NQ = g.NM + g.NI, T = w.T, rs = w.rs;
+  const unsigned nq = *w.rsq_n;
+  for (unsigned qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+    const int b = w.rsq[qi];
+    const int rt = w.rank[b], nd = w.ndead[b];
+    const int tn = w.tcount ? w.tcount[b] : T;
+    const bool pen = w.nisl[b] > 0;
+    const float penf = (float)cfg.penalty;
+    const float* m32 = reinterpret_cast<const float*>(w.m32) + (size_t)b * T;
+    const int t32 = (int)w.best[b];
+    auto vof = [&](int t) -> float {
+      const float v = m32[t];
+      return pen ? fmaxf(v, penf) : v;
+    };
+    const float vmin = vof(t32);
+    const float E = RESCORE_EPS * fmaxf(1.f, vmin);
+    const float hi = vmin + 2.f * E;
+    const double* Bm = w.Bm + (size_t)b * rs * R;
+    const double* Bmon = w.Bmon + (size_t)b * rs * M;
+    const double* Y = w.Y + (size_t)b * rs * T;
+    const uint8_t* inj = w.inj + (size_t)b * T * g.K;
+    double* n0b = w.n0b + (size_t)b * R;
+    double* n0m = w.n0m + (size_t)b * M;
+    const float* cm = w.cmax + (size_t)b * (N1 + NQ) * T;
+    __syncthreads();  // the previous task's shared state is consumed
+    if (tid < nd) {
+      const int row = w.dead[(size_t)b * RMAX + tid];
+      sdead[tid] = row;
+      sdeadp[tid] = g.row_mon_pos[row];
+    }
+    double best64 = __longlong_as_double(0x7ff0000000000000ll);
+    int bestt = t32, nrep = 0;
+    unsigned long long nres = 0;
+    bool stop = false;
+    // FP64 metric of candidate t (whole CTA; v = its FP32 metric)
+    auto rescore = [&](int t, float v) -> double {
+      if (tid < rt) sY[tid] = Y[(size_t)tid * T + t];
+      __syncthreads();
+      double mx = 0.0;
+      for (int r = tid; r < R; r += RT) {
+        double val = 0.0;
+        if (!is_dead(sdead, nd, r)) {
+          val = g.f0[r];
+          for (int j = 0; j < rt; ++j) val = fma(Bm[(size_t)j * R + r], sY[j], val);
+        }
+        n0b[r] = val;
+        const int p = g.row_mon_pos[r];
+        if (p >= 0) {
+          n0m[p] = val;
+          mx = fmax(mx, fabs(val) * g.inv_rating[p]);
+        }
+      }
+      __syncthreads();
+      const float th = v - 2.f * E;
+      // single cases: lanes test 32 cases, the warp sweeps the rows of each relevant one
+      for (int c0 = wid * 32; c0 < N1; c0 += RT) {
+        const int c = c0 + lane;
+        bool take = false;
+        if (c < N1 && w.sc_ok[(size_t)b * N1 + c]) {
+          const float ub = pair_evaluated(g, w, b, c, t) ? cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
+          take = ub >= th;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, take);
+        while (todo) {
+          const int cc = c0 + __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int rowc = g.sc_row[cc], ownp = g.row_mon_pos[rowc];
+          const double idn = 1.0 / w.den[(size_t)b * N1 + cc], sc = n0b[rowc];
+          const double* Wc = w.Wsc + ((size_t)b * N1 + cc) * rs;
+          const double* Dc = g.DM64 + (size_t)cc * M;
+          for (int p = lane; p < M; p += 32) {
+            if (is_dead(sdeadp, nd, p)) continue;
+            double dv = Dc[p];
+            for (int j = 0; j < rt; ++j) dv = fma(Bmon[(size_t)j * M + p], Wc[j], dv);
+            const double f = single_flow(n0m[p], dv, idn, sc, p == ownp);
+            mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+          }
+        }
+      }
+      // multi-branch and injection cases: a warp per relevant case
+      for (int q = wid; q < NQ; q += RW) {
+        const bool feas = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
+        if (!feas || !(cm[(size_t)(N1 + q) * T + t] >= th)) continue;
+        mx = fmax(mx, other_case_max(g, w, b, q, t, n0b, sdead, nd, sMinv[wid]));
+      }
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) sRed[wid] = mx;
+      __syncthreads();
+      mx = sRed[0];
+      for (int i = 1; i < RW; ++i) mx = fmax(mx, sRed[i]);
+      return pen ? fmax(mx, cfg.penalty) : mx;
+    };
+    for (int t0 = 0; t0 < tn && !stop; t0 += RT) {
+      // the chunk's band members, ascending
+      const int tt = t0 + tid;
+      const bool inb = tt < tn && vof(tt) <= hi;
+      const unsigned bal = __ballot_sync(0xffffffffu, inb);
+      if (lane == 0) sCnt[wid] = __popc(bal);
+      __syncthreads();
+      int off = 0, cnt = 0;
+      for (int i = 0; i < RW; ++i) {
+        off += i < wid ? sCnt[i] : 0;
+        cnt += sCnt[i];
+      }
+      if (inb) sList[off + __popc(bal & ((1u << lane) - 1u))] = tt;
+      __syncthreads();
+      for (int i = 0; i < cnt; ++i) {
+        const int t = sList[i];
+        const float v = vof(t);
+        if ((double)v - (double)E >= best64) continue;
+        double m64;
+        if (pen && (double)m32[t] + (double)E < cfg.penalty) {
+          m64 = cfg.penalty;
+        } else {
+          if (tid == 0) sDup = 0;
+          __syncthreads();
+          for (int k = tid; k < nrep; k += RT) {
+            const int u = sRep[k];
+            bool same = true;
+            for (int j = 0; j < rt && same; ++j)
+              same = __double_as_longlong(Y[(size_t)j * T + t]) == __double_as_longlong(Y[(size_t)j * T + u]);
+            for (int qq = 0; qq < g.NI && same; ++qq) {
+              const int sl = g.ic_slot[qq];
+              if (sl >= 0) same = inj[(size_t)t * g.K + sl] == inj[(size_t)u * g.K + sl];
+            }
+            if (same) sDup = 1;
+          }
+          __syncthreads();
+          const int dup = sDup;
+          __syncthreads();  // every thread has read sDup before thread 0 clears it again
+          if (dup) continue;
+          m64 = rescore(t, v);
+          ++nres;
+          if (nrep < RREP) {
+            if (tid == 0) sRep[nrep] = t;
+            ++nrep;
+          }
+        }
+        if (m64 < best64) {
+          best64 = m64;
+          bestt = t;
+        }
+        if (pen && best64 == cfg.penalty) {
+          stop = true;
+          break;
+        }
+      }
+      __syncthreads();  // sList and sCnt are rewritten by the next chunk
+    }
+    if (tid == 0) {
+      w.best[b] = bestt;
+      atomicAdd(w.lf + 4, nres);
+      if (bestt != t32) atomicAdd(w.lf + 5, 1ull);
+    }
   }
 }
 
@@ -955,20 +1205,15 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
     const int cq = cq_env ? atoi(cq_env) : (g.M <= 2048 ? 1 : 4);
     const int rpl = cq == 1 && g.M <= 64 ? 2 : cq == 1 && g.M > 128 && g.M <= 192 ? 6 : 4;
     const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl);
-    static bool init = false;
-    if (!init) {
-      const int mx = (int)rsweep_dyn_bytes(RMAX, KC, 192);
-      cudaFuncSetAttribute(k_rsweep<KC, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(k_rsweep<KC, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(k_rsweep<KC, 1, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(k_rsweep<KC, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      init = true;
-    }
     const dim3 grid(w.nslot - RSEL_WARPS, w.Wb);
-    if (cq != 1) k_rsweep<KC, 4, 4><<<grid, RT, dyn, s>>>(g, c, w);
-    else if (rpl == 2) k_rsweep<KC, 1, 2><<<grid, RT, dyn, s>>>(g, c, w);
-    else if (rpl == 6) k_rsweep<KC, 1, 6><<<grid, RT, dyn, s>>>(g, c, w);
-    else k_rsweep<KC, 1, 4><<<grid, RT, dyn, s>>>(g, c, w);
+    auto go = [&](auto kern) {
+      smem_opt_in((const void*)kern, (int)dyn);
+      kern<<<grid, RT, dyn, s>>>(g, c, w);
+    };
+    if (cq != 1) go(k_rsweep<KC, 4, 4>);
+    else if (rpl == 2) go(k_rsweep<KC, 1, 2>);
+    else if (rpl == 6) go(k_rsweep<KC, 1, 6>);
+    else go(k_rsweep<KC, 1, 4>);
   }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);
@@ -982,6 +1227,15 @@ void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   else launch_report_t<32>(g, c, w, s);
 }
 
+void launch_rescore(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  // persistent CTAs over the device-side queue k_select filled
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::max(1, std::min(w.Wb, 4 * nsm));
+  k_rescore<<<grid, RT, 0, s>>>(g, c, w);
+}
+
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s) {
   const int ncase = g.N1 + g.NM + g.NI;
@@ -991,10 +1245,9 @@ void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8
 
 int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
-  // update, N-0, select, report select + merge (+ single: the N-1 stage's launches and
-  // the report sweep) (+ other)
-  // (+ multi/injection: the correction terms and k_other)
-  return 5 + (single ? single_launches(g, w) + 1 : 0) + 2 * (g.NM + g.NI > 0 && g.M > 0);
+  // update, N-0, select + FP64 re-score, report select + merge (+ single: the N-1 stage's
+  // launches and the report sweep) (+ multi/injection: the correction terms and k_other)
+  return 6 + (single ? single_launches(g, w) + 1 : 0) + 2 * (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

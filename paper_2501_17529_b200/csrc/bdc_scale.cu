@@ -369,11 +369,7 @@ void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   // that no more are resident (a CTA spinning in tcgen05.alloc would hold an SM slot)
   const int ncols = TB * SM_ROWS <= 64 ? 64 : (TB * SM_ROWS <= 128 ? 128 : 256);
   dyn = std::max(dyn, (size_t)(220 * 1024) / (size_t)(512 / ncols));
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_scale_tc<TB, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    init = true;
-  }
+  smem_opt_in((const void*)k_scale_tc<TB, KB>, (int)dyn);
   const dim3 grid((g.N1 + SM_CASES - 1) / SM_CASES, (w.Wb + TB - 1) / TB);
   k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, w, *g.tm_ds);
 }

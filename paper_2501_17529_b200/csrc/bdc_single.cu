@@ -432,17 +432,7 @@ void launch_top_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t
   static_assert(NC == TOPC, "TOP tile = TOPC cases");
   const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
                      (2 * (size_t)RC * TT + 2 * (size_t)RC * NC) * sizeof(float);
-  static int max_dyn = -1;
-  if (max_dyn < 0) {
-    // opt in to every byte of shared memory the kernel's static part leaves free
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_top<CPT, TPT, TX, TY, RC, RGS, MINB>);
-    max_dyn = optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_top<CPT, TPT, TX, TY, RC, RGS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  }
+  smem_opt_in((const void*)k_top<CPT, TPT, TX, TY, RC, RGS, MINB>, (int)dyn);
   dim3 grid(1, (w.T + TT - 1) / TT, w.Wb);
   k_top<CPT, TPT, TX, TY, RC, RGS, MINB><<<grid, TX * TY * RGS, dyn, s>>>(g, c, w);
 }
@@ -452,17 +442,10 @@ void launch_pairs_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream
   constexpr int NC = CPT * TX, TT = TPT * TY;
   const size_t dyn = ((size_t)NC * w.rs + 2 * (size_t)w.rs * RC) * sizeof(double) +
                      (2 * (size_t)RC * TT + 2 * (size_t)RC * NC) * sizeof(float);
-  static int max_dyn = -1, per_sm = 1, nsm = 148;
-  if (max_dyn < 0) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>);
-    max_dyn = optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  }
+  int per_sm = 1, nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  smem_opt_in((const void*)k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>, (int)dyn);
   // persistent: as many CTAs as fit at once for this rank stride's shared memory
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB>, TX * TY * RGS, dyn);
   k_pairs<CPT, TPT, TX, TY, RC, RGS, MINB><<<nsm * (per_sm > 0 ? per_sm : 1), TX * TY * RGS, dyn, s>>>(g, c, w);

@@ -880,17 +880,16 @@ __global__ void __launch_bounds__(NT) k_topk(DevGrid g, Work w) {
 
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t st) {
   const size_t dyn = update_dyn_bytes(w.rs, g.E > 0 ? g.E : 1);
-  static size_t opted = 0;
-  if (dyn > opted) {
-    const int mx = (int)update_dyn_bytes(RMAX, EMAX);
-    cudaFuncSetAttribute(k_update<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_update<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_update<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    opted = update_dyn_bytes(RMAX, EMAX);
+  if (g.R > 2048) {
+    smem_opt_in((const void*)k_update<512, 2>, (int)dyn);
+    k_update<512, 2><<<w.Wb, 512, dyn, st>>>(g, c, w);
+  } else if (g.R > 512) {
+    smem_opt_in((const void*)k_update<256, 4>, (int)dyn);
+    k_update<256, 4><<<w.Wb, 256, dyn, st>>>(g, c, w);
+  } else {
+    smem_opt_in((const void*)k_update<128, 8>, (int)dyn);
+    k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
   }
-  if (g.R > 2048) k_update<512, 2><<<w.Wb, 512, dyn, st>>>(g, c, w);
-  else if (g.R > 512) k_update<256, 4><<<w.Wb, 256, dyn, st>>>(g, c, w);
-  else k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
   if (w.NTERM > 0 && g.M > 0) {
     const int work = g.M + w.NTERM * w.T;
     const dim3 grid((unsigned)std::min(8, (work + NT - 1) / NT), w.Wb);
@@ -904,17 +903,13 @@ void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
   const dim3 grid((NL + N0_ROWS - 1) / N0_ROWS, w.Wb);
   const int tpl = w.T > 64 ? 4 : (w.T > 32 ? 2 : 1);
   const size_t dyn = (size_t)w.rs * (N0_ROWS + 32 * tpl) * sizeof(double);
-  static bool init = false;
-  if (!init) {
-    const int mx = RMAX * (N0_ROWS + 128) * sizeof(double);
-    cudaFuncSetAttribute(k_n0<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_n0<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_n0<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    init = true;
-  }
-  if (tpl == 4) k_n0<4><<<grid, NT, dyn, st>>>(g, w);
-  else if (tpl == 2) k_n0<2><<<grid, NT, dyn, st>>>(g, w);
-  else k_n0<1><<<grid, NT, dyn, st>>>(g, w);
+  auto go = [&](auto kern) {
+    smem_opt_in((const void*)kern, (int)dyn);
+    kern<<<grid, NT, dyn, st>>>(g, w);
+  };
+  if (tpl == 4) go(k_n0<4>);
+  else if (tpl == 2) go(k_n0<2>);
+  else go(k_n0<1>);
 }
 
 // k_topk for small grids (N1 <= 32 KW): a warp per task, keys in registers, ptop rounds

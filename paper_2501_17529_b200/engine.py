@@ -110,6 +110,7 @@ class _Batch(ctypes.Structure):
         ("stage_ms", ctypes.c_float * N_STAGES),
         ("waves", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
+        ("rescore_stats", _P),
     ]
 
 
@@ -189,9 +190,11 @@ class Engine:
         self.base = base
         self.config = config
         self.device = device
-        # exact dominance screen of the reference's metric_first mode
-        # (solver.py:798-822); False brute-forces every (case, candidate) pair
-        self.screen = True
+        # SolveConfig.mode (solver.py:777-842): metric_first runs the exact dominance
+        # screen (solver.py:798-822); symmetric and output_first evaluate every
+        # (case, candidate) pair, as those modes do.  All three give bit-identical
+        # results (tests/test_gpu_large.py::test_modes_are_bit_identical).
+        self.screen = config.mode == "metric_first"
         self.tables = tb = build_tables(grid, base)
         if tb.E > MAX_ELEMENTS:
             raise ValidationError(f"substations with more than {MAX_ELEMENTS} branch elements")
@@ -396,12 +399,15 @@ class Engine:
         bt.loadflows = _ptr(lf)
         bt.n1_pairs = _ptr(pairs)
         bt.report_cases = _ptr(rcases)
+        rstats = np.zeros(3, dtype=np.int64)
+        bt.rescore_stats = _ptr(rstats)
         bt.screen = int(self.screen)
         rc = self.lib.bdc_solve(self.handle, ctypes.byref(bt))
         if rc != 0:
             raise EngineUnavailable(f"bdc_solve failed ({rc}): {_err(self.lib)}")
         self.last_pairs = int(pairs[0])
         self.last_report_cases = int(rcases[0])
+        self.last_rescore = [int(x) for x in rstats]
         return [float(x) for x in bt.stage_ms], int(bt.waves), int(bt.kernel_launches), int(lf[0])
 
     def probe_flows(self, splits_row: np.ndarray, discos_row: np.ndarray, inj_rows: np.ndarray):
@@ -427,6 +433,34 @@ class Engine:
         if rc != 0:
             raise EngineUnavailable(f"bdc_probe_flows failed ({rc}): {_err(self.lib)}")
         return int(st.value), int(sa.value), n0, n1[:nc], ok[:nc].astype(bool)
+
+
+def task_reason(eng: Engine, st: int, arg: int, splits_row: np.ndarray, discos_row: np.ndarray,
+                islanded_orders: Sequence[int]) -> Optional[str]:
+    """The reference's infeasibility message for an engine status code: the str() of the
+    first failing split's exception (factors.py:493-495, 516-518), the MODF / sequential
+    islanding message (solver.py:401-406) or the error-policy message (solver.py:501-511)."""
+    grid = eng.grid
+    if st == TASK_OK:
+        return None
+    if st in (TASK_DEGENERATE_SPLIT, TASK_SINGULAR_SPLIT):
+        si = [int(s) for s in np.flatnonzero(np.asarray(splits_row).any(axis=1))][arg]
+        node = grid.substations[si].node
+        if st == TASK_DEGENERATE_SPLIT:
+            return f"split of node {node} leaves busbar A without any branch"
+        n = len(grid.substations[si].branch_elements)
+        bits = [bool(x) for x in splits_row[si, :n]]
+        return f"split of node {node} with assignment {bits} disconnects the grid"
+    if st == TASK_DISCONNECT_ISLAND:
+        row = np.asarray(discos_row).reshape(-1)
+        ks = [int(k) for k in row[row >= 0]]
+        if arg >= 0:
+            return f"disconnections island the grid: outage of branch {ks[arg]} islands the grid"
+        return f"disconnections island the grid: simultaneous outage of branches {ks} islands the grid"
+    if st == TASK_ISLAND_ERROR:
+        ids = [eng.case_ids[o] for o in islanded_orders]
+        return f"islanding under contingencies {ids}"
+    return f"engine status {st}"
 
 
 class BatchOutput:
@@ -458,6 +492,9 @@ class BatchOutput:
         self._lf = np.zeros(1, dtype=np.int64)
         self._bsdf = np.zeros(1, dtype=np.int64)
         self._pairs = np.zeros(1, dtype=np.int64)
+        # [0] candidates re-scored in FP64, [1] winners the re-score replaced,
+        # [2] tasks with more than one candidate in the near-tie band
+        self.rescore_stats = np.zeros(3, dtype=np.int64)
         self.stage_ms = [0.0] * N_STAGES
         self.waves = 0
         self.kernel_launches = 0
@@ -473,6 +510,7 @@ class BatchOutput:
         bt.loadflows = _ptr(self._lf)
         bt.bsdf_applications = _ptr(self._bsdf)
         bt.n1_pairs = _ptr(self._pairs)
+        bt.rescore_stats = _ptr(self.rescore_stats)
         bt.screen = int(self.engine.screen)
 
     def finish(self, bt: _Batch) -> None:
@@ -513,33 +551,11 @@ class BatchOutput:
         bits = np.unpackbits(self.islanded_bits[b].view(np.uint8), bitorder="little")
         return [int(i) for i in np.flatnonzero(bits[: len(self.engine.case_ids)])]
 
-    def _split_subs(self, b: int) -> list[int]:
-        return [int(si) for si in np.flatnonzero(self.splits[b].any(axis=1))]
-
     def reason(self, b: int) -> Optional[str]:
-        st = int(self.status[b])
-        grid = self.engine.grid
-        if st == TASK_OK:
-            return None
-        if st in (TASK_DEGENERATE_SPLIT, TASK_SINGULAR_SPLIT):
-            si = self._split_subs(b)[int(self.status_arg[b])]
-            node = grid.substations[si].node
-            if st == TASK_DEGENERATE_SPLIT:
-                return f"split of node {node} leaves busbar A without any branch"
-            n = len(grid.substations[si].branch_elements)
-            bits = [bool(x) for x in self.splits[b, si, :n]]
-            return f"split of node {node} with assignment {bits} disconnects the grid"
-        if st == TASK_DISCONNECT_ISLAND:
-            row = self.discos[b]
-            ks = [int(k) for k in row[row >= 0]]
-            arg = int(self.status_arg[b])
-            if arg >= 0:
-                return f"disconnections island the grid: outage of branch {ks[arg]} islands the grid"
-            return f"disconnections island the grid: simultaneous outage of branches {ks} islands the grid"
-        if st == TASK_ISLAND_ERROR:
-            ids = [self.engine.case_ids[o] for o in self.islanded_orders(b)]
-            return f"islanding under contingencies {ids}"
-        return f"engine status {st}"
+        return task_reason(
+            self.engine, int(self.status[b]), int(self.status_arg[b]), self.splits[b], self.discos[b],
+            self.islanded_orders(b),
+        )
 
     def result(self, b: int):
         from .solver import SolveResult, SparseReport, TaskDiagnostics

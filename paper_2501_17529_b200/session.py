@@ -9,8 +9,8 @@ as the reference binding (`pkg/bindings/src/batchdc_session/session.py:53-225`):
 
 Differences that are deliberate: opening a session also uploads the grid's
 base tables to the GPU, and ``solve_batch`` runs the whole batch there; the
-per-task report documents are built lazily on access (``out["reports"]`` is
-a sequence that compares equal to the reference's list of dicts).
+``out["reports"]`` is the reference's list of dicts; ``solve_batch_output`` returns the
+array-first results with the documents built lazily on access instead.
 """
 
 from __future__ import annotations
@@ -169,7 +169,9 @@ def solve_batch(
         "metrics": out.metric,
         "best_injection": out.best,
         "feasible": out.feasible,
-        "reports": out.reports(),
+        # a real list of dicts, as the reference returns (session.py:182-195); the lazy
+        # per-task view is BatchOutput.reports() through solve_batch_output
+        "reports": list(out.reports()),
     }
 
 

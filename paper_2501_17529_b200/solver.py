@@ -47,8 +47,10 @@ class SolveConfig:
     """Solver knobs with the reference's defaults (`solver.py:61-91`).
 
     ``mode`` selects the reference's evaluation order; all three modes are
-    bit-identical there and produce identical results here (the GPU engine
-    always brute-forces every (candidate, case) pair and reports the winner).
+    bit-identical there and produce identical results here: ``metric_first`` runs
+    the engine's exact dominance screen (pairs that provably cannot move a metric
+    are skipped), ``symmetric`` and ``output_first`` evaluate every (case,
+    candidate) pair; the winner's report is built once, in FP64, either way.
     ``workers`` / ``max_batch`` are accepted for drop-in compatibility: the
     device engine processes tasks in waves sized by device memory.
     """
@@ -193,6 +195,52 @@ def tasks_to_arrays(grid: Grid, tasks: Sequence[TopologyTask]):
         inj[b, len(rows):] = rows[0]
         tcount[b] = len(rows)
     return splits, discos, inj, tcount
+
+
+@dataclass
+class CaseFlows:
+    """Raw engine flows of one task (`solver.py:903-916`): ``n0`` is (R, T); ``n1`` has
+    one (R, T) array per contingency case in contingency order, None where the case
+    islands the topology.  Rows follow ``row_branches``."""
+
+    feasible: bool
+    reason: Optional[str] = None
+    row_branches: Optional[np.ndarray] = None
+    n0: Optional[np.ndarray] = None
+    n1: Optional[list] = None
+    islanded_cases: tuple[str, ...] = ()
+
+
+def candidate_case_flows(grid: Grid, base, task: TopologyTask, config: Optional[SolveConfig] = None) -> CaseFlows:
+    """Every flow vector the solver scores for one task (`solver.py:919-958`), computed on
+    the GPU by the production kernels' factors (``bdc_probe_flows`` -> ``k_probe``, FP64):
+    splits, disconnections, case factors and candidate columns exactly as ``solve_batch``
+    forms them, returned instead of aggregated."""
+    from .engine import TASK_ISLAND_ERROR, TASK_OK, Engine, task_reason
+    from .ptdf import check_base_ptdf
+
+    config = config or SolveConfig()
+    config.validate()
+    check_base_ptdf(grid, base)
+    canon = canonicalize_task(grid, task)
+    engine = Engine.for_grid(grid, base, config)
+    splits, discos, inj, _ = tasks_to_arrays(grid, [canon])
+    st, sa, n0, n1, ok = engine.probe_flows(splits[0], discos[0], inj[0])
+    islanded = [i for i in range(len(ok)) if not ok[i]]
+    if st not in (TASK_OK, TASK_ISLAND_ERROR):
+        return CaseFlows(feasible=False, reason=task_reason(engine, st, sa, splits[0], discos[0], []))
+    ids = tuple(grid.contingencies[i].id for i in islanded)
+    if st == TASK_ISLAND_ERROR:
+        # the error policy reports the islanded cases in case order (solver.py:501-511)
+        return CaseFlows(feasible=False, reason=task_reason(engine, st, sa, splits[0], discos[0], islanded),
+                         islanded_cases=ids)
+    return CaseFlows(
+        feasible=True,
+        row_branches=np.array(base.row_branches, copy=True),
+        n0=n0,
+        n1=[None if not ok[i] else n1[i] for i in range(len(ok))],
+        islanded_cases=ids,
+    )
 
 
 def solve_batch(

@@ -162,5 +162,62 @@ def main():
         json.dump({"reference": "/root/reference/pkg (batchdc 0.1.0)", "cases": cases}, fh, indent=1)
 
 
+def grid_sha(doc) -> str:
+    import hashlib
+
+    return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()
+
+
+def main_large():
+    """Round-2 cases (manifest_large.json): the other two evaluation modes on the
+    reference fixtures, and reference-run documents at BASELINE.json's larger grid sizes,
+    chosen so that every kernel variant the benchmarked configs launch is covered:
+      g1k_t128    configs[2] shape: G1k, T=128 (the 16x128 TOP tile / k_pairs variant)
+      g3k_r12     configs[3] multi-split: k=8 splits + 4 disconnections (rank 12: the
+                  two-K-block tensor-core screening kernel, k_scale_tc<2,2>)
+      g10k_t*     configs[4] sweep end points T = 1, 64, 1024
+    The synthetic grids are not stored: the test regenerates them from
+    paper_2501_17529_b200.synth (seeded) and checks the document's sha256."""
+    import tempfile
+
+    def rt(n, ti, k, seed, d=0):
+        return lambda g, b: random_tasks(g, b, n, ti_size=ti, n_splits=k, seed=seed, n_disconnections=d)
+
+    def combo(*fns):
+        return lambda g, b: [t for fn in fns for t in fn(g, b)]
+
+    cases = []
+    cases.append(run_case("fixture_b_sym", "fixture_b.json", SolveConfig(mode="symmetric"),
+                          combo(rt(24, 8, 2, 921), rt(8, 8, 2, 922, 1))))
+    cases.append(run_case("case300_of", "case300.json", SolveConfig(mode="output_first"),
+                          combo(rt(8, 16, 3, 33), rt(4, 16, 2, 34, 1))))
+    tmp = tempfile.mkdtemp()
+    for name, spec_name, fn in (
+        ("g1k_t128", "g1k", combo(rt(32, 128, 3, 1001), rt(8, 128, 3, 1002, 1))),
+        ("g3k_r12", "g3k", rt(6, 32, 8, 3001, 4)),
+        ("g10k_t1", "g10k", rt(3, 1, 3, 10001)),
+        ("g10k_t64", "g10k", rt(3, 64, 3, 10002)),
+        ("g10k_t1024", "g10k", rt(2, 1024, 3, 10003)),
+    ):
+        doc = synth.make_grid_doc(spec_name, seed=0)
+        path = os.path.join(tmp, f"{spec_name}.json")
+        with open(path, "w") as fh:
+            json.dump(doc, fh)
+        import time
+
+        t0 = time.time()
+        c = run_case(name, path, SolveConfig(), fn)
+        c["grid"] = None
+        c["synth"] = spec_name
+        c["grid_sha256"] = grid_sha(doc)
+        c["reference_seconds"] = round(time.time() - t0, 1)
+        cases.append(c)
+    with open(os.path.join(HERE, "manifest_large.json"), "w") as fh:
+        json.dump({"reference": "/root/reference/pkg (batchdc 0.1.0)", "cases": cases}, fh, indent=1)
+
+
 if __name__ == "__main__":
-    main()
+    if "--large" in sys.argv:
+        main_large()
+    else:
+        main()

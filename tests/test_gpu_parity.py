@@ -3,11 +3,12 @@ documents and the CPU oracle, on the same seeded inputs.
 
 Tolerance contract:
   * feasibility, infeasibility reasons and islanded case sets: exact;
-  * metric: within 1e-9 of the reference when the winner is the same candidate
-    (the engine re-scores the winner in FP64), else within TAU;
+  * metric: within 1e-9 of the reference (FP64: every candidate in the FP32
+    near-tie band of the minimum is re-scored in FP64, k_rescore);
   * best_injection: identical whenever the reference's best-vs-runner-up gap
-    exceeds TAU = 1e-5 (relative loading); otherwise the engine's pick must be
-    metric-minimal within TAU (the reference's own rule, test_solver.py:244-246);
+    exceeds GAP64 = 1e-12 x max(1, metric), i.e. the FP64 noise between two
+    implementations; otherwise the engine's pick must be metric-minimal within
+    that noise (the reference's own rule, test_solver.py:244-246, at FP64);
   * report: identical (case, branch) entries and order, flows/loadings within
     1e-9, except permutations among entries whose loadings differ by < 1e-9;
   * per-candidate FP32 screening metrics within TAU of the FP64 oracle.
@@ -24,6 +25,7 @@ from oracle import port
 pytestmark = pytest.mark.gpu
 
 TAU = 1e-5
+GAP64 = 1e-12  # FP64 noise between the engine's low-rank flows and the reference's
 CASES = load_manifest()
 
 
@@ -80,18 +82,21 @@ def test_engine_matches_reference_documents(case, sessions):
         assert mine.get("diagnostics") == doc.get("diagnostics"), b
         ev = port.evaluate(sess.grid, sess.base, canons[b], sess.config)
         metrics = ev[0]
+        # the FP64 re-score of the near-tie band makes the winner the first FP64 argmin:
+        # identical to the reference's whenever the reference's best-vs-runner-up gap is
+        # above FP64 noise (distinct-flow candidates), metric-minimal at that noise otherwise
+        scale = max(1.0, abs(doc["metric"]))
         order = np.sort(metrics)
         gap = order[1] - order[0] if len(order) > 1 else np.inf
-        if gap > TAU:
+        if gap > GAP64 * scale:
             assert mine["best_injection"] == doc["best_injection"], (b, gap)
-        assert metrics[mine["best_injection"]] <= metrics.min() + TAU, b
+        assert metrics[mine["best_injection"]] <= metrics.min() + GAP64 * scale, b
+        assert abs(mine["metric"] - doc["metric"]) <= 1e-9 * scale, b
         if mine["best_injection"] == doc["best_injection"]:
             n_exact += 1
-            assert abs(mine["metric"] - doc["metric"]) <= 1e-9 * max(1.0, abs(doc["metric"])), b
             _same_entries(mine["n0_worst"], doc["n0_worst"], ("n0", b))
             _same_entries(mine["n1_worst"], doc["n1_worst"], ("n1", b))
         else:
-            assert abs(mine["metric"] - doc["metric"]) <= TAU, b
             _, _, n0e, n1e, _ = port.evaluate(sess.grid, sess.base, canons[b], sess.config, mine["best_injection"])
             _same_entries(mine["n0_worst"], [{"branch": x[0], "flow_mw": x[1], "rel_load": x[2]} for x in n0e], ("n0*", b))
             _same_entries(

@@ -42,14 +42,37 @@ def test_library_exports_every_header_symbol():
     assert b"sm_100a" in lib.bdc_version()
 
 
-def test_struct_layouts_match_header():
-    """ctypes mirrors of BdcGrid/BdcConfig/BdcBatch have the C sizes (compiled probe)."""
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of BdcGrid/BdcConfig/BdcBatch have the C layout: a probe compiled
+    with gcc against include/bdc.h prints sizeof and every field's offsetof."""
+    import shutil
+    import subprocess
+
     from paper_2501_17529_b200 import engine
 
     # 13 int32 + 31 pointers, padded to 8
     assert ctypes.sizeof(engine._Grid) == 13 * 4 + 4 + 31 * 8
     assert ctypes.sizeof(engine._Config) == 32
     assert engine._Batch.stage_ms.offset % 4 == 0
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"BdcGrid": engine._Grid, "BdcConfig": engine._Config, "BdcBatch": engine._Batch}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "bdc.h"', "int main(void){"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f in cls._fields_:
+            lines.append(f'printf("{cname}.{f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("return 0;}")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run([cc, "-I", os.path.join(REPO, "include"), "-o", str(exe), str(src)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for f in cls._fields_:
+            assert int(got[f"{cname}.{f[0]}"]) == getattr(cls, f[0]).offset, (cname, f[0])
 
 
 def _fake_session(path):
