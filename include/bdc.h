@@ -170,9 +170,10 @@ typedef struct {
   float stage_ms[BDC_STAGES];  /* see BDC_STAGE_* */
   int32_t waves;
   int32_t kernel_launches;
-  int64_t* rescore_stats;    /* (3) optional: [0] candidates re-scored in FP64 (the winner's
-                                near-tie band, solver.py:804-823), [1] tasks whose FP32 argmin
-                                the FP64 re-score replaced, [2] tasks with a band of > 1 */
+  int64_t* rescore_stats;    /* (3) optional: [0] candidate classes (bitwise-equal rank
+                                coefficients y_t) re-scored in FP64 (the winner's near-tie band,
+                                solver.py:804-823), [1] tasks whose FP32 argmin the FP64
+                                re-score replaced, [2] tasks with a band of > 1 */
 } BdcBatch;
 
 int bdc_device_count(int* count);

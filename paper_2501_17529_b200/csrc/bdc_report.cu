@@ -894,69 +894,62 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
 // of the FP64 metrics).  k_select took the first FP32 argmin (value vmin) and queued the
 // tasks with more than one candidate within 2E of it, E = RESCORE_EPS max(1, vmin) bounding
 // |m32 - m64|: the FP64 argmin is one of them.  A CTA per queued task walks the band in
-// ascending candidate order with the running FP64 minimum best64:
+// ascending candidate order, up to RCH members per pass, with the running FP64 minimum
+// best64 of the earlier passes:
 //   * a candidate with v(t) - E >= best64 cannot beat it (m64 >= v - E);
-//   * with islanded cases, one with m32 + E < penalty has m64 = penalty exactly;
-//   * one with the same y_t and injection-case slot bits as an earlier re-scored candidate
-//     has bit-identical flows, so the earlier index wins the tie;
-//   * any other is re-evaluated in FP64: the N-0 column and every case whose FP32 upper
-//     bound (exact FP32 maximum, or the dominance bound of a skipped pair) reaches
-//     v(t) - 2E, through the winner report's flow expressions, so the metric reported for
-//     the chosen candidate is the very value it was chosen by.
-// Once best64 equals the islanding penalty nothing can be smaller and the walk stops.
+//   * with islanded cases, one with m32 + E < penalty has m64 = penalty exactly, the
+//     smallest possible metric, so no later candidate can win and the walk ends with it;
+//   * every other member is re-evaluated in FP64 through the winner report's flow
+//     expressions (the same bits as k_rsel / k_rsweep), so the metric reported for the
+//     chosen candidate is the very value it was chosen by.  The flows of N-0, single- and
+//     multi-branch cases depend on the candidate only through its rank coefficients y_t
+//     (n0 = f0 + B'' y_t, solver.py:575-595), an injection case's additionally through its
+//     own slot bit (solver.py:619-622, 642-649).  Members are grouped by bitwise-equal y_t;
+//     each class is evaluated once, by one warp (N-0 and every single/multi case whose FP32
+//     upper bound reaches th = vmin - 2E), and each injection case once per slot-bit value
+//     present in the class.  Single cases are pre-filtered per task by their screening key
+//     (bkey_c >= every pair bound of case c).
 namespace {
-constexpr int RREP = 64;  // re-scored candidates remembered for the duplicate test
+constexpr int RCH = 2 * RT;   // band members per pass
+constexpr int RREL = 512;     // single cases listed per task (more: every case is tested)
 
-// FP64 max |F|/rating of one multi-branch or injection case q for candidate t (one warp);
-// the arithmetic of other_case_report.
-__device__ double other_case_max(const DevGrid& g, const Work& w, int b, int q, int t, const double* n0b,
-                                 const int* sdead, int nd, double* sMinv) {
-  const int lane = threadIdx.x & 31;
-  const int M = g.M, rt = w.rank[b];
-  const double* Bm = w.Bm + (size_t)b * w.rs * g.R;
-  double mx = 0.0;
-  if (q < g.NM) {
-    const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-    for (int i = lane; i < m * m; i += 32) sMinv[i] = w.minv[((size_t)b * g.NM + q) * MMAX * MMAX + i];
-    __syncwarp();
-    double sv[MMAX];
-    for (int j = 0; j < m; ++j) sv[j] = n0b[g.mb_row[st + j]];
-    for (int p = lane; p < M; p += 32) {
-      const int row = g.mon_row[p];
-      if (is_dead(sdead, nd, row)) continue;
-      int own;
-      const double f = multi_flow(g, w, b, st, m, row, n0b[row], sv, sMinv, Bm, rt, own);
-      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
-    }
-    __syncwarp();
-  } else {
-    const int qi = q - g.NM, sl = g.ic_slot[qi];
-    const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[qi];
-    const bool bit = sl >= 0 && w.inj[((size_t)b * w.T + t) * g.K + sl];
-    const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * g.NI + qi) * w.rs;
-    const double sp = g.ic_sp[qi];
-    for (int p = lane; p < M; p += 32) {
-      const int row = g.mon_row[p];
-      if (is_dead(sdead, nd, row)) continue;
-      const double f = inj_flow(g, ca, coef, sp, row, n0b[row], Bm, rt);
-      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
-    }
-  }
-  return mx;
+// N-0 flow of `row` for rank coefficients y (the k_rsel expression; 0 on disconnected rows)
+__device__ __forceinline__ double n0_at(const DevGrid& g, const double* Bm, const double* y, int rt,
+                                        const int* sdead, int nd, int row) {
+  if (is_dead(sdead, nd, row)) return 0.0;
+  double v = g.f0[row];
+  for (int j = 0; j < rt; ++j) v = fma(Bm[(size_t)j * g.R + row], y[j], v);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long h, unsigned long long v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  return h * 0xff51afd7ed558ccdull;
 }
 }  // namespace
 
 __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __shared__ int sdead[RMAX], sdeadp[RMAX];
-  __shared__ double sY[RMAX];
+  __shared__ double sY[RW][RMAX];             // the warp's class coefficients y_t
   __shared__ double sMinv[RW][MMAX * MMAX];
-  __shared__ int sList[RT];
+  __shared__ int sRel[RREL];                  // single cases with bkey >= th
+  __shared__ int sMem[RCH];                   // this pass's members (candidates, ascending)
+  __shared__ int sCls[RCH];                   // index of the member's class representative
+  __shared__ unsigned char sKnown[RCH];       // m64 known without evaluation (= penalty)
+  __shared__ unsigned long long sHash[RCH];   // hash of the member's y_t bits
+  __shared__ unsigned long long sM64[RCH];    // FP64 metric bits (non-negative: ordered as integers)
   __shared__ int sCnt[RW];
-  __shared__ int sRep[RREP];
   __shared__ double sRed[RW];
-  __shared__ int sDup;
-  const int R = g.R, M = g.M, N1 = g.N1, NQ = g.NM + g.NI, T = w.T, rs = w.rs;
+  __shared__ int sRi[RW];
+  __shared__ int sN, sEnd, sNext, sNRel, sNCls;
+  __shared__ int sReps[RCH];
+  const int M = g.M, N1 = g.N1, NM = g.NM, NI = g.NI, T = w.T, rs = w.rs;
   const unsigned nq = *w.rsq_n;
   for (unsigned qi = blockIdx.x; qi < nq; qi += gridDim.x) {
     const int b = w.rsq[qi];
@@ -973,137 +966,255 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
     const float vmin = vof(t32);
     const float E = RESCORE_EPS * fmaxf(1.f, vmin);
     const float hi = vmin + 2.f * E;
-    const double* Bm = w.Bm + (size_t)b * rs * R;
+    const float th = vmin - 2.f * E;  // case relevance: m64(t) >= v(t) - E >= vmin - E
+    const double* Bm = w.Bm + (size_t)b * rs * g.R;
     const double* Bmon = w.Bmon + (size_t)b * rs * M;
     const double* Y = w.Y + (size_t)b * rs * T;
     const uint8_t* inj = w.inj + (size_t)b * T * g.K;
-    double* n0b = w.n0b + (size_t)b * R;
-    double* n0m = w.n0m + (size_t)b * M;
-    const float* cm = w.cmax + (size_t)b * (N1 + NQ) * T;
+    const float* cm = w.cmax + (size_t)b * (N1 + NM + NI) * T;
+    const uint32_t* key = w.bkey + (size_t)b * N1;
     __syncthreads();  // the previous task's shared state is consumed
     if (tid < nd) {
       const int row = w.dead[(size_t)b * RMAX + tid];
       sdead[tid] = row;
       sdeadp[tid] = g.row_mon_pos[row];
     }
+    if (tid == 0) sNRel = 0;
+    __syncthreads();
+    // single cases that can reach th for some candidate (bkey_c bounds every pair of c)
+    for (int c0 = 0; w.ranked && c0 < N1; c0 += RT) {
+      const int c = c0 + tid;
+      const bool take = c < N1 && w.ranked && w.sc_ok[(size_t)b * N1 + c] && __uint_as_float(key[c]) >= th;
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (bal && lane == 0) sCnt[wid] = atomicAdd(&sNRel, __popc(bal));
+      __syncwarp();
+      const int base = __shfl_sync(0xffffffffu, sCnt[wid], 0);
+      const int k = base + __popc(bal & ((1u << lane) - 1u));
+      if (take && k < RREL) sRel[k] = c;
+      __syncwarp();
+    }
+    __syncthreads();
+    // too many, or no screening keys (screen off / every case in the TOP tile): test every
+    // case per class
+    const bool rel_all = !w.ranked || sNRel > RREL;
+    const int nrel = rel_all ? N1 : sNRel;
     double best64 = __longlong_as_double(0x7ff0000000000000ll);
-    int bestt = t32, nrep = 0;
+    int bestt = t32;
     unsigned long long nres = 0;
+    int t0 = 0;
     bool stop = false;
-    // FP64 metric of candidate t (whole CTA; v = its FP32 metric)
-    auto rescore = [&](int t, float v) -> double {
-      if (tid < rt) sY[tid] = Y[(size_t)tid * T + t];
+    while (t0 < tn && !stop) {
+      // ---- gather this pass's members, ascending (ballot compaction per RT candidates)
+      if (tid == 0) { sN = 0; sEnd = 0; sNext = tn; }
       __syncthreads();
-      double mx = 0.0;
-      for (int r = tid; r < R; r += RT) {
-        double val = 0.0;
-        if (!is_dead(sdead, nd, r)) {
-          val = g.f0[r];
-          for (int j = 0; j < rt; ++j) val = fma(Bm[(size_t)j * R + r], sY[j], val);
+      for (int tb = t0; tb < tn; tb += RT) {
+        const int n = sN;
+        if (sEnd || n > RCH - RT) {
+          if (tid == 0 && !sEnd) sNext = tb;
+          break;
         }
-        n0b[r] = val;
-        const int p = g.row_mon_pos[r];
-        if (p >= 0) {
-          n0m[p] = val;
-          mx = fmax(mx, fabs(val) * g.inv_rating[p]);
+        const int tt = tb + tid;
+        bool inb = false, known = false;
+        if (tt < tn) {
+          const float v = vof(tt);
+          inb = v <= hi && (double)v - (double)E < best64;
+          known = inb && pen && (double)m32[tt] + (double)E < cfg.penalty;
         }
+        // members past the first candidate with m64 = penalty cannot win
+        const unsigned kb = __ballot_sync(0xffffffffu, known);
+        if (lane == 0) sCnt[wid] = kb ? wid * 32 + __ffs(kb) - 1 : INT_MAX;
+        __syncthreads();
+        int firstk = INT_MAX;
+        for (int i = 0; i < RW; ++i) firstk = min(firstk, sCnt[i]);
+        __syncthreads();
+        if (tid > firstk) inb = false;
+        const unsigned bal = __ballot_sync(0xffffffffu, inb);
+        if (lane == 0) sCnt[wid] = __popc(bal);
+        __syncthreads();
+        int off = n, cnt = 0;
+        for (int i = 0; i < RW; ++i) {
+          off += i < wid ? sCnt[i] : 0;
+          cnt += sCnt[i];
+        }
+        if (inb) {
+          const int k = off + __popc(bal & ((1u << lane) - 1u));
+          sMem[k] = tt;
+          sKnown[k] = known;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          sN = n + cnt;
+          if (firstk != INT_MAX) { sEnd = 1; sNext = tn; }
+        }
+        __syncthreads();
       }
       __syncthreads();
-      const float th = v - 2.f * E;
-      // single cases: lanes test 32 cases, the warp sweeps the rows of each relevant one
-      for (int c0 = wid * 32; c0 < N1; c0 += RT) {
-        const int c = c0 + lane;
-        bool take = false;
-        if (c < N1 && w.sc_ok[(size_t)b * N1 + c]) {
-          const float ub = pair_evaluated(g, w, b, c, t) ? cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
-          take = ub >= th;
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, take);
-        while (todo) {
-          const int cc = c0 + __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int rowc = g.sc_row[cc], ownp = g.row_mon_pos[rowc];
-          const double idn = 1.0 / w.den[(size_t)b * N1 + cc], sc = n0b[rowc];
-          const double* Wc = w.Wsc + ((size_t)b * N1 + cc) * rs;
-          const double* Dc = g.DM64 + (size_t)cc * M;
-          for (int p = lane; p < M; p += 32) {
-            if (is_dead(sdeadp, nd, p)) continue;
-            double dv = Dc[p];
-            for (int j = 0; j < rt; ++j) dv = fma(Bmon[(size_t)j * M + p], Wc[j], dv);
-            const double f = single_flow(n0m[p], dv, idn, sc, p == ownp);
-            mx = fmax(mx, fabs(f) * g.inv_rating[p]);
-          }
-        }
+      const int n = sN;
+      t0 = sNext;
+      stop = sEnd;
+      __syncthreads();  // sN / sNext / sEnd are read before the next pass resets them
+      if (n == 0) continue;
+      // ---- classes of bitwise-equal y_t
+      for (int i = tid; i < n; i += RT) {
+        unsigned long long h = 0x243f6a8885a308d3ull;
+        const int t = sMem[i];
+        for (int j = 0; j < rt; ++j) h = mix64(h, (unsigned long long)__double_as_longlong(Y[(size_t)j * T + t]));
+        sHash[i] = sKnown[i] ? 0ull : (h | 1ull);
+        sM64[i] = sKnown[i] ? (unsigned long long)__double_as_longlong(cfg.penalty) : 0ull;
       }
-      // multi-branch and injection cases: a warp per relevant case
-      for (int q = wid; q < NQ; q += RW) {
-        const bool feas = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
-        if (!feas || !(cm[(size_t)(N1 + q) * T + t] >= th)) continue;
-        mx = fmax(mx, other_case_max(g, w, b, q, t, n0b, sdead, nd, sMinv[wid]));
-      }
-      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) sRed[wid] = mx;
+      if (tid == 0) sNCls = 0;
       __syncthreads();
-      mx = sRed[0];
-      for (int i = 1; i < RW; ++i) mx = fmax(mx, sRed[i]);
-      return pen ? fmax(mx, cfg.penalty) : mx;
-    };
-    for (int t0 = 0; t0 < tn && !stop; t0 += RT) {
-      // the chunk's band members, ascending
-      const int tt = t0 + tid;
-      const bool inb = tt < tn && vof(tt) <= hi;
-      const unsigned bal = __ballot_sync(0xffffffffu, inb);
-      if (lane == 0) sCnt[wid] = __popc(bal);
-      __syncthreads();
-      int off = 0, cnt = 0;
-      for (int i = 0; i < RW; ++i) {
-        off += i < wid ? sCnt[i] : 0;
-        cnt += sCnt[i];
-      }
-      if (inb) sList[off + __popc(bal & ((1u << lane) - 1u))] = tt;
-      __syncthreads();
-      for (int i = 0; i < cnt; ++i) {
-        const int t = sList[i];
-        const float v = vof(t);
-        if ((double)v - (double)E >= best64) continue;
-        double m64;
-        if (pen && (double)m32[t] + (double)E < cfg.penalty) {
-          m64 = cfg.penalty;
-        } else {
-          if (tid == 0) sDup = 0;
-          __syncthreads();
-          for (int k = tid; k < nrep; k += RT) {
-            const int u = sRep[k];
+      for (int i = tid; i < n; i += RT) {
+        int rep = i;
+        if (!sKnown[i]) {
+          const int t = sMem[i];
+          for (int k = 0; k < i; ++k) {
+            if (sHash[k] != sHash[i]) continue;
+            const int u = sMem[k];
             bool same = true;
             for (int j = 0; j < rt && same; ++j)
               same = __double_as_longlong(Y[(size_t)j * T + t]) == __double_as_longlong(Y[(size_t)j * T + u]);
-            for (int qq = 0; qq < g.NI && same; ++qq) {
-              const int sl = g.ic_slot[qq];
-              if (sl >= 0) same = inj[(size_t)t * g.K + sl] == inj[(size_t)u * g.K + sl];
-            }
-            if (same) sDup = 1;
+            if (same) { rep = k; break; }
           }
-          __syncthreads();
-          const int dup = sDup;
-          __syncthreads();  // every thread has read sDup before thread 0 clears it again
-          if (dup) continue;
-          m64 = rescore(t, v);
-          ++nres;
-          if (nrep < RREP) {
-            if (tid == 0) sRep[nrep] = t;
-            ++nrep;
-          }
+          if (rep == i) sReps[atomicAdd(&sNCls, 1)] = i;
         }
-        if (m64 < best64) {
-          best64 = m64;
-          bestt = t;
-        }
-        if (pen && best64 == cfg.penalty) {
-          stop = true;
-          break;
-        }
+        sCls[i] = sKnown[i] ? -1 : rep;
       }
-      __syncthreads();  // sList and sCnt are rewritten by the next chunk
+      __syncthreads();
+      // ---- evaluate each class once, a warp per class
+      const int ncls = sNCls;
+      for (int ci = wid; ci < ncls; ci += RW) {
+        const int i = sReps[ci], t = sMem[i];
+        double* y = sY[wid];
+        if (lane < rt) y[lane] = Y[(size_t)lane * T + t];
+        __syncwarp();
+        // N-0 on monitored rows
+        double mx = 0.0;
+#pragma unroll 4
+        for (int p = lane; p < M; p += 32) {
+          if (is_dead(sdeadp, nd, p)) continue;
+          double v = g.f0[g.mon_row[p]];
+          for (int j = 0; j < rt; ++j) v = fma(Bmon[(size_t)j * M + p], y[j], v);
+          mx = fmax(mx, fabs(v) * g.inv_rating[p]);
+        }
+        // single cases whose bound for this class reaches th
+        for (int k0 = 0; k0 < nrel; k0 += 32) {
+          const int kk = k0 + lane;
+          bool take = false;
+          int c = 0;
+          if (kk < nrel) {
+            c = rel_all ? kk : sRel[kk];
+            if (!rel_all || (w.sc_ok[(size_t)b * N1 + c] && (!w.ranked || __uint_as_float(key[c]) >= th))) {
+              const float ub = pair_evaluated(g, w, b, c, t) ? cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
+              take = ub >= th;
+            }
+          }
+          unsigned todo = __ballot_sync(0xffffffffu, take);
+          while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int cc = __shfl_sync(0xffffffffu, c, src);
+            const int rowc = g.sc_row[cc], ownp = g.row_mon_pos[rowc];
+            const double idn = 1.0 / w.den[(size_t)b * N1 + cc];
+            const double sc = n0_at(g, Bm, y, rt, sdead, nd, rowc);
+            const double* Wc = w.Wsc + ((size_t)b * N1 + cc) * rs;
+            const double* Dc = g.DM64 + (size_t)cc * M;
+#pragma unroll 2
+            for (int p = lane; p < M; p += 32) {
+              if (is_dead(sdeadp, nd, p)) continue;
+              double nv = g.f0[g.mon_row[p]];
+              double dv = Dc[p];
+              for (int j = 0; j < rt; ++j) {
+                const double bj = Bmon[(size_t)j * M + p];
+                nv = fma(bj, y[j], nv);
+                dv = fma(bj, Wc[j], dv);
+              }
+              const double f = single_flow(nv, dv, idn, sc, p == ownp);
+              mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+            }
+          }
+        }
+        // multi-branch cases
+        for (int q = 0; q < NM; ++q) {
+          if (!w.mc_ok[(size_t)b * NM + q] || !(cm[(size_t)(N1 + q) * T + t] >= th)) continue;
+          const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+          for (int e = lane; e < m * m; e += 32) sMinv[wid][e] = w.minv[((size_t)b * NM + q) * MMAX * MMAX + e];
+          __syncwarp();
+          double sv[MMAX];
+          for (int j = 0; j < m; ++j) sv[j] = n0_at(g, Bm, y, rt, sdead, nd, g.mb_row[st + j]);
+          for (int p = lane; p < M; p += 32) {
+            const int row = g.mon_row[p];
+            if (is_dead(sdead, nd, row)) continue;
+            int own;
+            const double f = multi_flow(g, w, b, st, m, row, n0_at(g, Bm, y, rt, sdead, nd, row), sv, sMinv[wid], Bm, rt, own);
+            mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+          }
+          __syncwarp();
+        }
+        mx = warp_max(mx);
+        const unsigned long long ab = (unsigned long long)__double_as_longlong(mx);
+        for (int k = lane; k < n; k += 32)
+          if (sCls[k] == i) atomicMax(&sM64[k], ab);
+        // injection cases, once per slot-bit value some member of the class needs
+        for (int pr = 0; pr < 2 * NI; ++pr) {
+          const int q = pr >> 1;
+          const bool bit = pr & 1;
+          const int sl = g.ic_slot[q];
+          if (sl < 0 && bit) continue;  // a fixed column: no bit dependence
+          bool need = false;
+          for (int k = lane; k < n; k += 32) {
+            if (sCls[k] != i) continue;
+            const int u = sMem[k];
+            const bool ub = sl >= 0 && inj[(size_t)u * g.K + sl];
+            need |= ub == bit && cm[(size_t)(N1 + NM + q) * T + u] >= th;
+          }
+          if (!__any_sync(0xffffffffu, need)) continue;
+          const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
+          const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * NI + q) * rs;
+          const double sp = g.ic_sp[q];
+          double iv = 0.0;
+          for (int p = lane; p < M; p += 32) {
+            const int row = g.mon_row[p];
+            if (is_dead(sdead, nd, row)) continue;
+            const double f = inj_flow(g, ca, coef, sp, row, n0_at(g, Bm, y, rt, sdead, nd, row), Bm, rt);
+            iv = fmax(iv, fabs(f) * g.inv_rating[p]);
+          }
+          const unsigned long long vb = (unsigned long long)__double_as_longlong(warp_max(iv));
+          for (int k = lane; k < n; k += 32) {
+            if (sCls[k] != i) continue;
+            const bool ub = sl >= 0 && inj[(size_t)sMem[k] * g.K + sl];
+            if (ub == bit) atomicMax(&sM64[k], vb);
+          }
+        }
+        __syncwarp();
+      }
+      nres += ncls;
+      __syncthreads();
+      // ---- the pass's first FP64 argmin (penalty floor), then the running minimum
+      double bv = __longlong_as_double(0x7ff0000000000000ll);
+      int bi = INT_MAX;
+      for (int k = tid; k < n; k += RT) {
+        double v = __longlong_as_double((long long)sM64[k]);
+        if (pen) v = fmax(v, cfg.penalty);
+        if (v < bv) { bv = v; bi = k; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { sRed[wid] = bv; sRi[wid] = bi; }
+      __syncthreads();
+      bv = sRed[0];
+      bi = sRi[0];
+      for (int k = 1; k < RW; ++k)
+        if (sRed[k] < bv || (sRed[k] == bv && sRi[k] < bi)) { bv = sRed[k]; bi = sRi[k]; }
+      if (bv < best64) {
+        best64 = bv;
+        bestt = sMem[bi];
+      }
+      if (pen && best64 == cfg.penalty) stop = true;
+      __syncthreads();  // sMem / sCls / sM64 are rewritten by the next pass
     }
     if (tid == 0) {
       w.best[b] = bestt;

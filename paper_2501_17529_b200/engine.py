@@ -492,7 +492,7 @@ class BatchOutput:
         self._lf = np.zeros(1, dtype=np.int64)
         self._bsdf = np.zeros(1, dtype=np.int64)
         self._pairs = np.zeros(1, dtype=np.int64)
-        # [0] candidates re-scored in FP64, [1] winners the re-score replaced,
+        # [0] y-classes re-scored in FP64, [1] winners the re-score replaced,
         # [2] tasks with more than one candidate in the near-tie band
         self.rescore_stats = np.zeros(3, dtype=np.int64)
         self.stage_ms = [0.0] * N_STAGES
