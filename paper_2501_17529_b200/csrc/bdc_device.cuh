@@ -135,6 +135,7 @@ struct Work {
   int* rsq;       // (Wb)          tasks whose winner band holds more than one candidate
   unsigned* rsq_n;  // their number (device counter, reset per wave)
   int screen;     // 1 = exact dominance screen on
+  int rescore_full;  // 1 = k_rescore evaluates every class over every row (tests)
   int rsel_cta;   // 1: winner report selection always CTA-per-task (test knob BDC_RSEL_CTA)
   int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)

@@ -311,14 +311,19 @@ __global__ void k_select(DevGrid g, DevCfg cfg, Work w) {
   }
   // near-tie band: candidates whose FP32 metric lies within 2 E of the minimum may be the
   // FP64 argmin (|m32 - m64| <= E); more than one -> queue the task for k_rescore
-  const float hi = bv + 2.f * RESCORE_EPS * fmaxf(1.f, bv);
+  // With islanded cases, a winner whose m32 + E lies below the penalty has m64 = penalty
+  // exactly, the smallest metric possible: only an earlier band member could tie it.
+  const float E = RESCORE_EPS * fmaxf(1.f, bv);
+  const float hi = bv + 2.f * E;
+  const bool exact = pen && (double)__uint_as_float(w.m32[(size_t)b * T + bi]) + (double)E < cfg.penalty;
   int nband = 0;
   for (int t = lane; t < tn; t += 32) {
     float v = __uint_as_float(w.m32[(size_t)b * T + t]);
     if (pen) v = fmaxf(v, penalty);
-    nband += v <= hi;
+    nband += v <= hi && (!exact || t < bi);
   }
   for (int o = 16; o; o >>= 1) nband += __shfl_xor_sync(0xffffffffu, nband, o);
+  if (exact && nband > 0) ++nband;  // the winner itself
   if (lane == 0) {
     w.best[b] = bi;
     w.feasible[b] = 1;

@@ -901,17 +901,24 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
 //     smallest possible metric, so no later candidate can win and the walk ends with it;
 //   * every other member is re-evaluated in FP64 through the winner report's flow
 //     expressions (the same bits as k_rsel / k_rsweep), so the metric reported for the
-//     chosen candidate is the very value it was chosen by.  The flows of N-0, single- and
-//     multi-branch cases depend on the candidate only through its rank coefficients y_t
-//     (n0 = f0 + B'' y_t, solver.py:575-595), an injection case's additionally through its
-//     own slot bit (solver.py:619-622, 642-649).  Members are grouped by bitwise-equal y_t;
-//     each class is evaluated once, by one warp (N-0 and every single/multi case whose FP32
-//     upper bound reaches th = vmin - 2E), and each injection case once per slot-bit value
-//     present in the class.  Single cases are pre-filtered per task by their screening key
-//     (bkey_c >= every pair bound of case c).
+//     chosen candidate is the very value it was chosen by.
+// The flows of N-0, single- and multi-branch cases depend on the candidate only through
+// its rank coefficients y_t (n0 = f0 + B'' y_t, solver.py:575-595), an injection case's
+// additionally through its own slot bit (solver.py:619-622, 642-649).  Members are grouped
+// by bitwise-equal y_t (classes).  Every element that can reach th = vmin - 2E for some
+// class is found by ONE pass at the first class's y0: an N-0 or single-case flow moves by
+// at most |B''(r,:)| dy (+ |L(r,c)| |B''(r_c,:)| dy) between classes, dy_j = max over the
+// pass's classes |y_j - y0_j|, so elements with |F(y0)|/rating + that bound below th - E
+// can never be a class maximum that matters (m64 >= vmin - E).  Each class is then
+// evaluated on that short "hot" list only (a warp per class), with the same per-element
+// expression, so its maximum is the exact FP64 value whenever it is >= th.  Multi-branch
+// cases and injection cases (per slot-bit value) are evaluated in full when their FP32
+// maximum reaches th.  Single cases are pre-filtered per task by their screening key
+// (bkey_c >= every pair bound of case c).  A hot list that overflows falls back to the
+// full per-class evaluation (warp_class_max).
 namespace {
-constexpr int RCH = 2 * RT;   // band members per pass
-constexpr int RREL = 512;     // single cases listed per task (more: every case is tested)
+constexpr int RREL = 512;   // single cases listed per task (more: full per-class evaluation)
+constexpr int RHOT = 256;   // hot (case, row) elements per pass
 
 // N-0 flow of `row` for rank coefficients y (the k_rsel expression; 0 on disconnected rows)
 __device__ __forceinline__ double n0_at(const DevGrid& g, const double* Bm, const double* y, int rt,
@@ -931,26 +938,149 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long h, unsign
   h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
   return h * 0xff51afd7ed558ccdull;
 }
+
+__device__ __forceinline__ unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
+
+// Per-task inputs of a class evaluation
+struct RsTask {
+  int b, rt, nd, T;
+  float th;
+  const double *Bm, *Bmon;
+  const float* cm;
+  const uint32_t* key;
+  const int *sdead, *sdeadp;
+};
+
+// FP64 |F|/rating of one element for coefficients y: c < 0 the N-0 flow at monitored
+// position p, else single case c at p (the expressions of warp_class_max, element by element)
+__device__ __forceinline__ double elem_value(const DevGrid& g, const Work& w, const RsTask& k, const double* y,
+                                             int c, int p) {
+  const int M = g.M, rt = k.rt;
+  double nv = g.f0[g.mon_row[p]];
+  if (c < 0) {
+    for (int j = 0; j < rt; ++j) nv = fma(k.Bmon[(size_t)j * M + p], y[j], nv);
+    return fabs(nv) * g.inv_rating[p];
+  }
+  const int rowc = g.sc_row[c], ownp = g.row_mon_pos[rowc];
+  const double idn = 1.0 / w.den[(size_t)k.b * g.N1 + c];
+  const double sc = n0_at(g, k.Bm, y, rt, k.sdead, k.nd, rowc);
+  const double* Wc = w.Wsc + ((size_t)k.b * g.N1 + c) * w.rs;
+  double dv = g.DM64[(size_t)c * M + p];
+  for (int j = 0; j < rt; ++j) {
+    const double bj = k.Bmon[(size_t)j * M + p];
+    nv = fma(bj, y[j], nv);
+    dv = fma(bj, Wc[j], dv);
+  }
+  return fabs(single_flow(nv, dv, idn, sc, p == ownp)) * g.inv_rating[p];
+}
+
+// FP64 max over the multi-branch cases whose FP32 maximum for candidate t reaches th (one
+// warp); `mask` (q < 32) lists them when the caller has tested them already
+__device__ double warp_multi_max(const DevGrid& g, const Work& w, const RsTask& k, int t, const double* y,
+                                 double* sMinv, unsigned mask = 0xffffffffu) {
+  const int lane = threadIdx.x & 31;
+  const int M = g.M, N1 = g.N1, NM = g.NM, rt = k.rt, nd = k.nd, b = k.b;
+  double mx = 0.0;
+  for (int q = 0; q < NM; ++q) {
+    if (q < 32 && !((mask >> q) & 1u)) continue;
+    if (!w.mc_ok[(size_t)b * NM + q] || !(k.cm[(size_t)(N1 + q) * k.T + t] >= k.th)) continue;
+    const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
+    for (int e = lane; e < m * m; e += 32) sMinv[e] = w.minv[((size_t)b * NM + q) * MMAX * MMAX + e];
+    __syncwarp();
+    double sv[MMAX];
+    for (int j = 0; j < m; ++j) sv[j] = n0_at(g, k.Bm, y, rt, k.sdead, nd, g.mb_row[st + j]);
+    for (int p = lane; p < M; p += 32) {
+      const int row = g.mon_row[p];
+      if (is_dead(k.sdead, nd, row)) continue;
+      int own;
+      const double f = multi_flow(g, w, b, st, m, row, n0_at(g, k.Bm, y, rt, k.sdead, nd, row), sv, sMinv, k.Bm, rt, own);
+      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+    }
+    __syncwarp();
+  }
+  return warp_max(mx);
+}
+
+// FP64 max over N-0 and the relevant single / multi-branch cases for coefficients y (one
+// warp, every monitored row; candidate t is any member of the class).  Single cases come
+// from rel[0..nrel) or, with rel_all, from every case with a screening key >= th.
+__device__ double warp_class_max(const DevGrid& g, const Work& w, const RsTask& k, int t, const double* y,
+                                 const int* rel, int nrel, bool rel_all, double* sMinv) {
+  const int lane = threadIdx.x & 31;
+  const int M = g.M, N1 = g.N1, nd = k.nd, b = k.b, T = k.T;
+  double mx = 0.0;
+  for (int p = lane; p < M; p += 32)
+    if (!is_dead(k.sdeadp, nd, p)) mx = fmax(mx, elem_value(g, w, k, y, -1, p));
+  const int ncand = rel_all ? N1 : nrel;
+  for (int k0 = 0; k0 < ncand; k0 += 32) {
+    const int kk = k0 + lane;
+    bool take = false;
+    int c = 0;
+    if (kk < ncand) {
+      c = rel_all ? kk : rel[kk];
+      if (!rel_all || (w.sc_ok[(size_t)b * N1 + c] && (!w.ranked || __uint_as_float(k.key[c]) >= k.th))) {
+        const float ub = pair_evaluated(g, w, b, c, t) ? k.cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
+        take = ub >= k.th;
+      }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, take);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int cc = __shfl_sync(0xffffffffu, c, src);
+      for (int p = lane; p < M; p += 32)
+        if (!is_dead(k.sdeadp, nd, p)) mx = fmax(mx, elem_value(g, w, k, y, cc, p));
+    }
+  }
+  return fmax(warp_max(mx), warp_multi_max(g, w, k, t, y, sMinv));
+}
+
+// FP64 max |F|/rating of injection case q with slot bit `bit` for coefficients y (one warp)
+__device__ double warp_inj_max(const DevGrid& g, const Work& w, const RsTask& k, int q, bool bit, const double* y) {
+  const int lane = threadIdx.x & 31;
+  const int sl = g.ic_slot[q];
+  const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
+  const double* coef = (bit ? w.cib : w.cia) + ((size_t)k.b * g.NI + q) * w.rs;
+  const double sp = g.ic_sp[q];
+  double iv = 0.0;
+  for (int p = lane; p < g.M; p += 32) {
+    const int row = g.mon_row[p];
+    if (is_dead(k.sdead, k.nd, row)) continue;
+    const double f = inj_flow(g, ca, coef, sp, row, n0_at(g, k.Bm, y, k.rt, k.sdead, k.nd, row), k.Bm, k.rt);
+    iv = fmax(iv, fabs(f) * g.inv_rating[p]);
+  }
+  return warp_max(iv);
+}
 }  // namespace
 
-__global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 64 ? 12 : 3) k_rescore(DevGrid g, DevCfg cfg, Work w) {
+  constexpr int NW = NT / 32;
+  constexpr int RCH = NT == 64 ? 128 : 256;  // band members per pass
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __shared__ int sdead[RMAX], sdeadp[RMAX];
-  __shared__ double sY[RW][RMAX];             // the warp's class coefficients y_t
-  __shared__ double sMinv[RW][MMAX * MMAX];
+  __shared__ double sYw[NW][RMAX];            // the warp's class coefficients y_t
+  __shared__ double sMinv[NW][MMAX * MMAX];
   __shared__ int sRel[RREL];                  // single cases with bkey >= th
+  __shared__ int sRel2[RREL];                 // ... that reach th for some class of the pass
   __shared__ int sMem[RCH];                   // this pass's members (candidates, ascending)
   __shared__ int sCls[RCH];                   // index of the member's class representative
+  __shared__ int sReps[RCH];                  // class representatives
   __shared__ unsigned char sKnown[RCH];       // m64 known without evaluation (= penalty)
   __shared__ unsigned long long sHash[RCH];   // hash of the member's y_t bits
   __shared__ unsigned long long sM64[RCH];    // FP64 metric bits (non-negative: ordered as integers)
-  __shared__ int sCnt[RW];
-  __shared__ double sRed[RW];
-  __shared__ int sRi[RW];
-  __shared__ int sN, sEnd, sNext, sNRel, sNCls;
-  __shared__ int sReps[RCH];
+  __shared__ unsigned sNeedI[RCH], sBitI[RCH];  // injection cases a member needs / its slot bits
+  __shared__ unsigned sNeedM[RCH];              // multi-branch cases a member needs
+  __shared__ double sY0[RMAX];                // y of the pass's reference class
+  __shared__ unsigned long long sDy[RMAX];    // max over the pass's classes |y_j - y0_j|
+  __shared__ int sHotC[RHOT], sHotP[RHOT];    // hot elements (case or -1 for N-0, monitored pos)
+  __shared__ int sCnt[NW];
+  __shared__ double sRed[NW];
+  __shared__ int sRi[NW];
+  __shared__ int sN, sEnd, sNext, sNRel, sNRel2, sNCls, sNHot, sI0;
   const int M = g.M, N1 = g.N1, NM = g.NM, NI = g.NI, T = w.T, rs = w.rs;
   const unsigned nq = *w.rsq_n;
+  const bool full_env = w.rescore_full != 0;
   for (unsigned qi = blockIdx.x; qi < nq; qi += gridDim.x) {
     const int b = w.rsq[qi];
     const int rt = w.rank[b], nd = w.ndead[b];
@@ -967,6 +1097,7 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
     const float E = RESCORE_EPS * fmaxf(1.f, vmin);
     const float hi = vmin + 2.f * E;
     const float th = vmin - 2.f * E;  // case relevance: m64(t) >= v(t) - E >= vmin - E
+    const double hot_th = (double)th - (double)E;
     const double* Bm = w.Bm + (size_t)b * rs * g.R;
     const double* Bmon = w.Bmon + (size_t)b * rs * M;
     const double* Y = w.Y + (size_t)b * rs * T;
@@ -982,9 +1113,9 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
     if (tid == 0) sNRel = 0;
     __syncthreads();
     // single cases that can reach th for some candidate (bkey_c bounds every pair of c)
-    for (int c0 = 0; w.ranked && c0 < N1; c0 += RT) {
+    for (int c0 = 0; w.ranked && c0 < N1; c0 += NT) {
       const int c = c0 + tid;
-      const bool take = c < N1 && w.ranked && w.sc_ok[(size_t)b * N1 + c] && __uint_as_float(key[c]) >= th;
+      const bool take = c < N1 && w.sc_ok[(size_t)b * N1 + c] && __uint_as_float(key[c]) >= th;
       const unsigned bal = __ballot_sync(0xffffffffu, take);
       if (bal && lane == 0) sCnt[wid] = atomicAdd(&sNRel, __popc(bal));
       __syncwarp();
@@ -994,22 +1125,23 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
       __syncwarp();
     }
     __syncthreads();
-    // too many, or no screening keys (screen off / every case in the TOP tile): test every
-    // case per class
+    // too many, or no screening keys (screen off / every case in the TOP tile): full
+    // per-class evaluation over every case
     const bool rel_all = !w.ranked || sNRel > RREL;
     const int nrel = rel_all ? N1 : sNRel;
+    const RsTask tk{b, rt, nd, T, th, Bm, Bmon, cm, key, sdead, sdeadp};
     double best64 = __longlong_as_double(0x7ff0000000000000ll);
     int bestt = t32;
     unsigned long long nres = 0;
     int t0 = 0;
     bool stop = false;
     while (t0 < tn && !stop) {
-      // ---- gather this pass's members, ascending (ballot compaction per RT candidates)
+      // ---- gather this pass's members, ascending (ballot compaction per NT candidates)
       if (tid == 0) { sN = 0; sEnd = 0; sNext = tn; }
       __syncthreads();
-      for (int tb = t0; tb < tn; tb += RT) {
+      for (int tb = t0; tb < tn; tb += NT) {
         const int n = sN;
-        if (sEnd || n > RCH - RT) {
+        if (sEnd || n > RCH - NT) {
           if (tid == 0 && !sEnd) sNext = tb;
           break;
         }
@@ -1025,14 +1157,14 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
         if (lane == 0) sCnt[wid] = kb ? wid * 32 + __ffs(kb) - 1 : INT_MAX;
         __syncthreads();
         int firstk = INT_MAX;
-        for (int i = 0; i < RW; ++i) firstk = min(firstk, sCnt[i]);
+        for (int i = 0; i < NW; ++i) firstk = min(firstk, sCnt[i]);
         __syncthreads();
         if (tid > firstk) inb = false;
         const unsigned bal = __ballot_sync(0xffffffffu, inb);
         if (lane == 0) sCnt[wid] = __popc(bal);
         __syncthreads();
         int off = n, cnt = 0;
-        for (int i = 0; i < RW; ++i) {
+        for (int i = 0; i < NW; ++i) {
           off += i < wid ? sCnt[i] : 0;
           cnt += sCnt[i];
         }
@@ -1055,16 +1187,31 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
       __syncthreads();  // sN / sNext / sEnd are read before the next pass resets them
       if (n == 0) continue;
       // ---- classes of bitwise-equal y_t
-      for (int i = tid; i < n; i += RT) {
+      for (int i = tid; i < n; i += NT) {
         unsigned long long h = 0x243f6a8885a308d3ull;
         const int t = sMem[i];
-        for (int j = 0; j < rt; ++j) h = mix64(h, (unsigned long long)__double_as_longlong(Y[(size_t)j * T + t]));
+        for (int j = 0; j < rt; ++j) h = mix64(h, dbits(Y[(size_t)j * T + t]));
         sHash[i] = sKnown[i] ? 0ull : (h | 1ull);
-        sM64[i] = sKnown[i] ? (unsigned long long)__double_as_longlong(cfg.penalty) : 0ull;
+        sM64[i] = sKnown[i] ? dbits(cfg.penalty) : 0ull;
+        // injection cases whose FP32 maximum for t reaches th, and t's slot bit of each
+        unsigned need = 0u, bits = 0u;
+        for (int q = 0; q < NI && !sKnown[i]; ++q) {
+          const int sl = g.ic_slot[q];
+          const bool bit = sl >= 0 && inj[(size_t)t * g.K + sl];
+          if (cm[(size_t)(N1 + NM + q) * T + t] >= th) need |= q < 32 ? 1u << q : 0u;
+          bits |= (bit && q < 32) ? 1u << q : 0u;
+        }
+        sNeedI[i] = NI > 32 ? 0xffffffffu : need;
+        sBitI[i] = bits;
+        unsigned mneed = NM > 32 ? 0xffffffffu : 0u;  // multi-branch cases reaching th (y only)
+        for (int q = 0; q < NM && q < 32 && !sKnown[i]; ++q)
+          if (w.mc_ok[(size_t)b * NM + q] && cm[(size_t)(N1 + q) * T + t] >= th) mneed |= 1u << q;
+        sNeedM[i] = mneed;
       }
-      if (tid == 0) sNCls = 0;
+      if (tid == 0) { sNCls = 0; sNHot = 0; sNRel2 = 0; sI0 = INT_MAX; }
+      if (tid < RMAX) sDy[tid] = 0ull;
       __syncthreads();
-      for (int i = tid; i < n; i += RT) {
+      for (int i = tid; i < n; i += NT) {
         int rep = i;
         if (!sKnown[i]) {
           const int t = sMem[i];
@@ -1072,93 +1219,119 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
             if (sHash[k] != sHash[i]) continue;
             const int u = sMem[k];
             bool same = true;
-            for (int j = 0; j < rt && same; ++j)
-              same = __double_as_longlong(Y[(size_t)j * T + t]) == __double_as_longlong(Y[(size_t)j * T + u]);
+            for (int j = 0; j < rt && same; ++j) same = dbits(Y[(size_t)j * T + t]) == dbits(Y[(size_t)j * T + u]);
             if (same) { rep = k; break; }
           }
-          if (rep == i) sReps[atomicAdd(&sNCls, 1)] = i;
+          if (rep == i) {
+            sReps[atomicAdd(&sNCls, 1)] = i;
+            atomicMin(&sI0, i);
+          }
         }
         sCls[i] = sKnown[i] ? -1 : rep;
       }
       __syncthreads();
-      // ---- evaluate each class once, a warp per class
       const int ncls = sNCls;
-      for (int ci = wid; ci < ncls; ci += RW) {
+      nres += ncls;
+      bool hot_ok = false;
+      if (ncls > 0 && !rel_all && !full_env) {
+        // ---- the hot elements, from one pass at the first class's y0
+        const int tr = sMem[sI0];
+        if (tid < rt) sY0[tid] = Y[(size_t)tid * T + tr];
+        __syncthreads();
+        for (int e = tid; e < ncls * rt; e += NT) {
+          const int j = e % rt, t = sMem[sReps[e / rt]];
+          atomicMax(&sDy[j], dbits(fabs(Y[(size_t)j * T + t] - sY0[j])));
+        }
+        for (int kk = tid; kk < nrel; kk += NT) sRel2[kk] = 0;
+        __syncthreads();
+        // single cases some class of the pass can take to th
+        for (int e = tid; e < nrel * ncls; e += NT) {
+          const int kk = e / ncls, c = sRel[kk], t = sMem[sReps[e % ncls]];
+          const float ub = pair_evaluated(g, w, b, c, t) ? cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
+          if (ub >= th) sRel2[kk] = -1 - c;  // marked (any writer)
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int m = 0;
+          for (int kk = 0; kk < nrel; ++kk)
+            if (sRel2[kk] < 0 && sRel2[kk] == -1 - sRel[kk]) sRel2[m++] = sRel[kk];
+          sNRel2 = m;
+        }
+        __syncthreads();
+        const double* dy = reinterpret_cast<const double*>(sDy);
+        // N-0 rows
+        for (int p = tid; p < M; p += NT) {
+          if (is_dead(sdeadp, nd, p)) continue;
+          double mv = 0.0;
+          for (int j = 0; j < rt; ++j) mv = fma(fabs(Bmon[(size_t)j * M + p]), dy[j], mv);
+          const double v = elem_value(g, w, tk, sY0, -1, p);
+          if (v + (mv * g.inv_rating[p]) * (1.0 + 1e-9) >= hot_th) {
+            const int h = atomicAdd(&sNHot, 1);
+            if (h < RHOT) { sHotC[h] = -1; sHotP[h] = p; }
+          }
+        }
+        // single cases, a warp each
+        for (int kk = wid; kk < sNRel2; kk += NW) {
+          const int c = sRel2[kk];
+          const int rowc = g.sc_row[c], ownp = g.row_mon_pos[rowc];
+          const double idn = 1.0 / w.den[(size_t)b * N1 + c];
+          double ms = 0.0;  // bound of the move of n0(r_c)
+          if (!is_dead(sdead, nd, rowc))
+            for (int j = 0; j < rt; ++j) ms = fma(fabs(Bm[(size_t)j * g.R + rowc]), dy[j], ms);
+          const double* Wc = w.Wsc + ((size_t)b * N1 + c) * rs;
+          for (int p = lane; p < M; p += 32) {
+            if (is_dead(sdeadp, nd, p) || p == ownp) continue;  // the own row's flow is exactly 0
+            double mv = 0.0, dv = g.DM64[(size_t)c * M + p];
+            for (int j = 0; j < rt; ++j) {
+              const double bj = Bmon[(size_t)j * M + p];
+              mv = fma(fabs(bj), dy[j], mv);
+              dv = fma(bj, Wc[j], dv);
+            }
+            mv = fma(fabs(dv * idn), ms, mv);
+            const double v = elem_value(g, w, tk, sY0, c, p);
+            if (v + (mv * g.inv_rating[p]) * (1.0 + 1e-9) >= hot_th) {
+              const int h = atomicAdd(&sNHot, 1);
+              if (h < RHOT) { sHotC[h] = c; sHotP[h] = p; }
+            }
+          }
+        }
+        __syncthreads();
+        hot_ok = sNHot <= RHOT;
+      }
+      // ---- evaluate each class once, a warp per class
+      const int nhot = sNHot;
+      for (int ci = wid; ci < ncls; ci += NW) {
         const int i = sReps[ci], t = sMem[i];
-        double* y = sY[wid];
+        double* y = sYw[wid];
         if (lane < rt) y[lane] = Y[(size_t)lane * T + t];
         __syncwarp();
-        // N-0 on monitored rows
-        double mx = 0.0;
-#pragma unroll 4
-        for (int p = lane; p < M; p += 32) {
-          if (is_dead(sdeadp, nd, p)) continue;
-          double v = g.f0[g.mon_row[p]];
-          for (int j = 0; j < rt; ++j) v = fma(Bmon[(size_t)j * M + p], y[j], v);
-          mx = fmax(mx, fabs(v) * g.inv_rating[p]);
+        double mx;
+        if (hot_ok) {
+          mx = 0.0;
+          for (int h = lane; h < nhot; h += 32) mx = fmax(mx, elem_value(g, w, tk, y, sHotC[h], sHotP[h]));
+          mx = warp_max(mx);
+          if (sNeedM[i]) mx = fmax(mx, warp_multi_max(g, w, tk, t, y, sMinv[wid], sNeedM[i]));
+        } else {
+          mx = warp_class_max(g, w, tk, t, y, sRel, nrel, rel_all, sMinv[wid]);
         }
-        // single cases whose bound for this class reaches th
-        for (int k0 = 0; k0 < nrel; k0 += 32) {
-          const int kk = k0 + lane;
-          bool take = false;
-          int c = 0;
-          if (kk < nrel) {
-            c = rel_all ? kk : sRel[kk];
-            if (!rel_all || (w.sc_ok[(size_t)b * N1 + c] && (!w.ranked || __uint_as_float(key[c]) >= th))) {
-              const float ub = pair_evaluated(g, w, b, c, t) ? cm[(size_t)c * T + t] : pair_bound(g, w, b, c, t);
-              take = ub >= th;
-            }
-          }
-          unsigned todo = __ballot_sync(0xffffffffu, take);
-          while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int cc = __shfl_sync(0xffffffffu, c, src);
-            const int rowc = g.sc_row[cc], ownp = g.row_mon_pos[rowc];
-            const double idn = 1.0 / w.den[(size_t)b * N1 + cc];
-            const double sc = n0_at(g, Bm, y, rt, sdead, nd, rowc);
-            const double* Wc = w.Wsc + ((size_t)b * N1 + cc) * rs;
-            const double* Dc = g.DM64 + (size_t)cc * M;
-#pragma unroll 2
-            for (int p = lane; p < M; p += 32) {
-              if (is_dead(sdeadp, nd, p)) continue;
-              double nv = g.f0[g.mon_row[p]];
-              double dv = Dc[p];
-              for (int j = 0; j < rt; ++j) {
-                const double bj = Bmon[(size_t)j * M + p];
-                nv = fma(bj, y[j], nv);
-                dv = fma(bj, Wc[j], dv);
-              }
-              const double f = single_flow(nv, dv, idn, sc, p == ownp);
-              mx = fmax(mx, fabs(f) * g.inv_rating[p]);
-            }
-          }
-        }
-        // multi-branch cases
-        for (int q = 0; q < NM; ++q) {
-          if (!w.mc_ok[(size_t)b * NM + q] || !(cm[(size_t)(N1 + q) * T + t] >= th)) continue;
-          const int st = g.mc_start[q], m = g.mc_start[q + 1] - st;
-          for (int e = lane; e < m * m; e += 32) sMinv[wid][e] = w.minv[((size_t)b * NM + q) * MMAX * MMAX + e];
-          __syncwarp();
-          double sv[MMAX];
-          for (int j = 0; j < m; ++j) sv[j] = n0_at(g, Bm, y, rt, sdead, nd, g.mb_row[st + j]);
-          for (int p = lane; p < M; p += 32) {
-            const int row = g.mon_row[p];
-            if (is_dead(sdead, nd, row)) continue;
-            int own;
-            const double f = multi_flow(g, w, b, st, m, row, n0_at(g, Bm, y, rt, sdead, nd, row), sv, sMinv[wid], Bm, rt, own);
-            mx = fmax(mx, fabs(f) * g.inv_rating[p]);
-          }
-          __syncwarp();
-        }
-        mx = warp_max(mx);
-        const unsigned long long ab = (unsigned long long)__double_as_longlong(mx);
+        const unsigned long long ab = dbits(mx);
         for (int k = lane; k < n; k += 32)
           if (sCls[k] == i) atomicMax(&sM64[k], ab);
         // injection cases, once per slot-bit value some member of the class needs
-        for (int pr = 0; pr < 2 * NI; ++pr) {
+        unsigned need1 = 0u, need0 = 0u;  // (q, bit) pairs the class's members need
+        for (int k = lane; k < n; k += 32) {
+          if (sCls[k] != i) continue;
+          need1 |= sNeedI[k] & sBitI[k];
+          need0 |= sNeedI[k] & ~sBitI[k];
+        }
+        for (int o = 16; o; o >>= 1) {
+          need1 |= __shfl_xor_sync(0xffffffffu, need1, o);
+          need0 |= __shfl_xor_sync(0xffffffffu, need0, o);
+        }
+        for (int pr = 0; (need0 | need1) && pr < 2 * NI; ++pr) {
           const int q = pr >> 1;
           const bool bit = pr & 1;
+          if (q < 32 && !(((bit ? need1 : need0) >> q) & 1u)) continue;
           const int sl = g.ic_slot[q];
           if (sl < 0 && bit) continue;  // a fixed column: no bit dependence
           bool need = false;
@@ -1169,17 +1342,7 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
             need |= ub == bit && cm[(size_t)(N1 + NM + q) * T + u] >= th;
           }
           if (!__any_sync(0xffffffffu, need)) continue;
-          const int ca = sl >= 0 ? g.slot_col[sl] : g.ic_col[q];
-          const double* coef = (bit ? w.cib : w.cia) + ((size_t)b * NI + q) * rs;
-          const double sp = g.ic_sp[q];
-          double iv = 0.0;
-          for (int p = lane; p < M; p += 32) {
-            const int row = g.mon_row[p];
-            if (is_dead(sdead, nd, row)) continue;
-            const double f = inj_flow(g, ca, coef, sp, row, n0_at(g, Bm, y, rt, sdead, nd, row), Bm, rt);
-            iv = fmax(iv, fabs(f) * g.inv_rating[p]);
-          }
-          const unsigned long long vb = (unsigned long long)__double_as_longlong(warp_max(iv));
+          const unsigned long long vb = dbits(warp_inj_max(g, w, tk, q, bit, y));
           for (int k = lane; k < n; k += 32) {
             if (sCls[k] != i) continue;
             const bool ub = sl >= 0 && inj[(size_t)sMem[k] * g.K + sl];
@@ -1188,12 +1351,11 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
         }
         __syncwarp();
       }
-      nres += ncls;
       __syncthreads();
       // ---- the pass's first FP64 argmin (penalty floor), then the running minimum
       double bv = __longlong_as_double(0x7ff0000000000000ll);
       int bi = INT_MAX;
-      for (int k = tid; k < n; k += RT) {
+      for (int k = tid; k < n; k += NT) {
         double v = __longlong_as_double((long long)sM64[k]);
         if (pen) v = fmax(v, cfg.penalty);
         if (v < bv) { bv = v; bi = k; }
@@ -1207,7 +1369,7 @@ __global__ void __launch_bounds__(RT) k_rescore(DevGrid g, DevCfg cfg, Work w) {
       __syncthreads();
       bv = sRed[0];
       bi = sRi[0];
-      for (int k = 1; k < RW; ++k)
+      for (int k = 1; k < NW; ++k)
         if (sRed[k] < bv || (sRed[k] == bv && sRi[k] < bi)) { bv = sRed[k]; bi = sRi[k]; }
       if (bv < best64) {
         best64 = bv;
@@ -1339,12 +1501,23 @@ void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
 }
 
 void launch_rescore(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
-  // persistent CTAs over the device-side queue k_select filled
+  // persistent CTAs over the device-side queue k_select filled: two warps per task on small
+  // grids (a few classes, short rows), eight on large ones
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::max(1, std::min(w.Wb, 4 * nsm));
-  k_rescore<<<grid, RT, 0, s>>>(g, c, w);
+  // tests: force a CTA size (BDC_RESCORE_NT) or the full per-class evaluation instead of
+  // the hot elements (BDC_RESCORE_FULL=1); both must give bit-identical winners
+  const char* nt_env = getenv("BDC_RESCORE_NT");
+  const char* full_env = getenv("BDC_RESCORE_FULL");
+  Work wr = w;
+  wr.rescore_full = full_env && full_env[0] == '1';
+  const int nt = nt_env ? atoi(nt_env) : (g.M <= 512 ? 64 : 256);
+  if (nt == 64) {
+    k_rescore<64><<<std::max(1, std::min(w.Wb, 16 * nsm)), 64, 0, s>>>(g, c, wr);
+  } else {
+    k_rescore<256><<<std::max(1, std::min(w.Wb, 4 * nsm)), 256, 0, s>>>(g, c, wr);
+  }
 }
 
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,

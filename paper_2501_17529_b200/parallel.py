@@ -78,6 +78,46 @@ def all_gather_tasks(local: dict, n_tasks: int, group=None, device=None) -> dict
     return out
 
 
+def all_gather_device(local: dict, group=None) -> dict:
+    """All-gather per-task device tensors of equal shard size (first axis = task) into
+    full-batch device tensors, one ``all_gather_into_tensor`` per field (NCCL over
+    NVLink): the collective of the device-resident path, nothing leaves HBM."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = {}
+    for name, t in local.items():
+        full = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(full, t.contiguous(), group=group)
+        out[name] = full
+    return out
+
+
+def solve_shard(
+    splits: np.ndarray,
+    discos: np.ndarray,
+    inj: np.ndarray,
+    n_tasks: int,
+    solver: Callable,
+    group=None,
+    device=None,
+) -> dict:
+    """Solve this rank's already-sliced shard (``shard_range(n_tasks, rank, world)``) and
+    all-gather the results: the full-batch arrays on every rank plus the job-wide
+    loadflow total."""
+    import torch
+    import torch.distributed as dist
+
+    out = solver(splits, discos, inj)
+    local = {name: getattr(out, name) for name in RESULT_FIELDS}
+    full = all_gather_tasks(local, n_tasks, group=group, device=device)
+    lf = torch.tensor([float(out.loadflows)], dtype=torch.float64, device=device)
+    dist.all_reduce(lf, group=group)
+    full["loadflows"] = int(lf.item())
+    return full
+
+
 def solve_sharded(
     splits: np.ndarray,
     discos: np.ndarray,
@@ -92,20 +132,13 @@ def solve_sharded(
     arrays (``engine.BatchOutput``) and a ``loadflows`` count.  Returns the
     full-batch arrays on every rank plus the job-wide loadflow total.
     """
-    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     B = inj.shape[0]
     a, b = shard_range(B, rank, world)
-    out = solver(splits[a:b], discos[a:b], inj[a:b])
-    local = {name: getattr(out, name) for name in RESULT_FIELDS}
-    full = all_gather_tasks(local, B, group=group, device=device)
-    lf = torch.tensor([float(out.loadflows)], dtype=torch.float64, device=device)
-    dist.all_reduce(lf, group=group)
-    full["loadflows"] = int(lf.item())
-    return full
+    return solve_shard(splits[a:b], discos[a:b], inj[a:b], B, solver, group=group, device=device)
 
 
 def engine_solver(session) -> Callable:

@@ -256,7 +256,8 @@ def test_wave_split_is_invisible(name, sessions):
 def test_report_select_variants_agree(name, sessions, monkeypatch):
     """The warp-per-task winner-report selection (small grids) and the CTA-per-task one
     (large grids, forced here with BDC_RSEL_CTA=1) give bit-identical results, and so do
-    the report sweep's one-case and four-case warp variants (BDC_RSWEEP_CQ)."""
+    the report sweep's one-case and four-case warp variants (BDC_RSWEEP_CQ) and the two
+    FP64 re-score variants (BDC_RESCORE_NT, BDC_RESCORE_FULL)."""
     case = next(c for c in CASES if c["name"] == name)
     sess = sessions(case)
     arr, _ = load_case(name)
@@ -269,6 +270,13 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     assert np.array_equal(warp.best, cta.best)
     assert np.array_equal(warp.metric, cta.metric, equal_nan=True)
     assert warp.reports() == cta.reports()
+    # the FP64 near-tie re-score: 2- vs 8-warp CTAs, hot elements vs every row of every class
+    for env in (("BDC_RESCORE_NT", "256"), ("BDC_RESCORE_FULL", "1")):
+        monkeypatch.setenv(*env)
+        alt = eng.solve(*args)
+        monkeypatch.delenv(env[0])
+        assert np.array_equal(warp.best, alt.best), env
+        assert np.array_equal(warp.metric, alt.metric, equal_nan=True), env
     for cq in ("1", "4"):
         monkeypatch.setenv("BDC_RSWEEP_CQ", cq)
         alt = eng.solve(*args)

@@ -67,6 +67,16 @@ def _worker(rank, port, out_path):
     arr = np.load(golden_path("fixture_b.npz"))
     s, d, i = arr["splits"][:21], arr["disconnections"][:21], arr["injection_sets"][:21]
     full = solve_sharded(s, d, i, lambda a, b, c: _PortOut(grid, base, cfg, a, b, c))
+    # the device-resident gather of the bench's timed path (gloo here, NCCL on GPUs)
+    import torch
+
+    from paper_2501_17529_b200.parallel import all_gather_device
+
+    loc = {"metric": torch.full((3,), float(rank), dtype=torch.float64),
+           "n1_case": torch.arange(6, dtype=torch.int32).reshape(3, 2) + 100 * rank}
+    g = all_gather_device(loc)
+    assert g["metric"].tolist() == [0.0] * 3 + [1.0] * 3
+    assert g["n1_case"][3:].tolist() == (torch.arange(6, dtype=torch.int32).reshape(3, 2) + 100).tolist()
     if rank == 0:
         np.savez(out_path, **{k: v for k, v in full.items() if k != "loadflows"}, loadflows=full["loadflows"])
     dist.barrier()
