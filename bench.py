@@ -54,13 +54,19 @@ WORKLOADS = {
     "g1k": ("g1k", 8192, 128, 3, 0),
     "g3k": ("g3k", 1024, 32, 8, 0),
     "g10k": ("g10k", 64, 64, 3, 0),
+    # BASELINE configs[2] (config C): 10^6 topologies x 128 over 8 GPUs, 125,000 per GPU,
+    # drawn on the device (taskgen.random_tasks_device)
+    "g1k_c": ("g1k", 125000, 128, 3, 0),
 }
+DEVICE_TASKS = {"g1k_c"}
 DESCR = {
     "g14": "IEEE-14-sized synthetic grid, 1024 topologies x 16 injections, 2 splits, full N-1",
     "g118": "IEEE-118-sized synthetic grid, 65536 topologies x 64 injections, 3 splits, full N-1",
     "g1k": "1000-bus synthetic grid, topologies x 128 injections, 3 splits, full N-1",
     "g3k": "3000-bus synthetic grid, multi-split (k=8) topologies x 32 injections, full N-1",
     "g10k": "10k-bus synthetic grid, topologies x 64 injections, 3 splits, full N-1",
+    "g1k_c": "1000-bus synthetic grid, 10^6 topologies over 8 GPUs (125,000 per GPU) x 128 injections, "
+    "3 splits, full N-1, tasks drawn on the device",
 }
 
 
@@ -414,16 +420,32 @@ def run_ours(args):
     if args.candidates:
         T = args.candidates
     # the job's batch is ws * tasks topologies; this rank's shard (parallel.shard_range of
-    # the concatenation) is drawn with its own seed
-    grid, splits, discos, inj = make_workload(args.config, rank, tasks, T)
+    # the concatenation) is drawn with its own seed, on the host (the reference's
+    # generator semantics) or on the device (taskgen, bdc_draw_tasks)
+    from paper_2501_17529_b200 import synth
+
+    grid = synth.make_grid(spec, seed=0)
     sess = session_open(grid, device=local)
     eng = sess.engine
     eng.screen = not args.no_screen
+    device_tasks = args.device_tasks or args.config in DEVICE_TASKS
+    gen_s = None
+    if device_tasks:
+        from paper_2501_17529_b200.taskgen import random_tasks_device, to_host
+
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        t_spl, t_dis, t_inj, draws = random_tasks_device(sess, tasks, T, k, 1000 + rank, n_disconnections=d)
+        torch.cuda.synchronize()
+        gen_s = time.perf_counter() - g0
+        splits, discos, inj = to_host(t_spl, t_dis, t_inj)
+    else:
+        splits, discos, inj = synth.random_task_arrays(grid, tasks, T, k, seed=1000 + rank, n_disconnections=d)
+        t_spl = torch.from_numpy(splits.view(np.uint8)).to(dev)
+        t_dis = torch.from_numpy(discos).to(dev)
+        t_inj = torch.from_numpy(inj.view(np.uint8)).to(dev)
     max_rank = eng.check_batch(splits.view(np.uint8), discos)
     B = splits.shape[0]
-    t_spl = torch.from_numpy(splits.view(np.uint8)).to(dev)
-    t_dis = torch.from_numpy(discos).to(dev)
-    t_inj = torch.from_numpy(inj.view(np.uint8)).to(dev)
     kg = sess.config.topk_global
     ncw = max(1, (len(grid.contingencies) + 31) // 32)
     outs = {
@@ -632,11 +654,15 @@ def run_ours(args):
             "note": "FP64 re-score of every candidate within 2 RESCORE_EPS of the FP32 minimum, grouped by "
             "bitwise-equal rank coefficients (k_rescore); best_injection = first FP64 argmin",
         },
+        "tasks": {"generated_on": "device (taskgen.random_tasks_device, bdc_draw_tasks)" if device_tasks else
+                  "host (synth.random_task_arrays)", "generate_s": gen_s},
         "gpu_launches": int(launches),
         "clocks": clk,
         "loadflows_per_step": lf_all / args.steps,
         "feasible_tasks": int(fe.sum()),
     }
+    if args.check < 0:
+        args.check = {"g14": 64, "g118": 64, "g1k": 32, "g1k_c": 32, "g3k": 16, "g10k": 4}.get(args.config, 8)
     if args.check > 0:
         try:
             line["parity_sample"] = parity_sample(grid, splits, discos, inj, res_metric, res_best, res_feas, args.check)
@@ -681,8 +707,10 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-screen", action="store_true", help="brute-force every (case, candidate) pair")
-    ap.add_argument("--check", type=int, default=64,
-                    help="re-solve this many tasks of the timed batch with the CPU oracle (parity_sample); 0 = off")
+    ap.add_argument("--device-tasks", action="store_true", help="draw the tasks on the GPU (taskgen)")
+    ap.add_argument("--check", type=int, default=-1,
+                    help="re-solve this many tasks of the timed batch with the CPU oracle (parity_sample); "
+                    "0 = off, -1 = by grid size (64 at G14/G118 ... 4 at G10k)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_self_launch(args))

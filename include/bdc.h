@@ -18,6 +18,8 @@
  *                           (_injection_stage :766), winner report (:652).
  *   bdc_probe_flows      <- batchdc.candidate_case_flows (solver.py:919-958):
  *                           every flow vector of one task, for parity checks.
+ *   bdc_draw_tasks       <- batchdc.bench.random_tasks (src/batchdc/bench.py:33-91),
+ *                           drawn on the device.
  *   bdc_scan_tasks       <- the rank / outage-cap checks of canonicalize_task and
  *                           _branch_stage (solver.py:148-197, 390-394), vectorised.
  *   bdc_session_destroy  <- (session lifetime end; the reference relies on GC)
@@ -205,6 +207,20 @@ int bdc_probe_flows(BdcSession* session, const uint8_t* splits, const int64_t* d
 int bdc_scan_tasks(BdcSession* session, const uint8_t* splits, const int64_t* discos,
                    int64_t B, int32_t D, int32_t* max_rank, int32_t* max_disc,
                    int32_t* max_active_slots);
+
+/* Device-side random tasks (batchdc.bench.random_tasks, bench.py:33-91): the
+ * reference's distribution drawn on the GPU into the session array layout.
+ * All array pointers are DEVICE pointers: splits (B,S,E) u8, discos (B,D) i64
+ * (NULL when D = 0), inj (B,T,K) u8 (NULL: topology only).  attempt (B) i32
+ * (NULL = 0) is each task's draw number and redraw (B) u8 (NULL = every task)
+ * selects the tasks whose topology is (re)drawn -- the caller's acceptance loop
+ * redraws the tasks the engine reports as degenerate/singular/islanding
+ * (bench.py:96-110).  Counter-based (Philox4x32-10): deterministic per seed.
+ * Runs on `stream` (NULL: the default stream); no synchronisation. */
+int bdc_draw_tasks(BdcSession* session, uint64_t seed, int64_t B, int32_t T, int32_t E, int32_t D,
+                   int32_t n_splits, int32_t n_disconnections, const int32_t* attempt,
+                   const uint8_t* redraw, uint8_t* splits, int64_t* discos, uint8_t* inj,
+                   void* stream);
 
 /* Set the wave size cap (tasks per device wave); 0 = automatic. */
 int bdc_session_set_wave(BdcSession* session, int64_t max_tasks_per_wave);

@@ -8,7 +8,8 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["bdc_update.cu", "bdc_single.cu", "bdc_scale.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_capi.cu"]
+SOURCES = ["bdc_update.cu", "bdc_single.cu", "bdc_scale.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_gen.cu",
+           "bdc_capi.cu"]
 TARGET = os.path.join(HERE, "libbdc.so")
 FLAGS = [
     "-std=c++17",
@@ -47,13 +48,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     procs = []
     objs = []
+    headers = [os.path.join(HERE, "csrc", "bdc_device.cuh"), os.path.join(os.path.dirname(HERE), "include", "bdc.h")]
+    hdr_t = max(os.path.getmtime(h) for h in headers)
     for src in SOURCES:
         obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
-        cmd = [nvcc()] + FLAGS + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
+        path = os.path.join(HERE, "csrc", src)
+        objs.append(obj)
+        # incremental unless forced: a unit is rebuilt when it or a shared header is newer
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), hdr_t):
+            continue
+        cmd = [nvcc()] + FLAGS + ["-c", "-o", obj, path]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd)))
-        objs.append(obj)
     failed = [src for src, p in procs if p.wait() != 0]
     if failed:
         raise RuntimeError(f"nvcc failed on {failed}")

@@ -390,6 +390,27 @@ int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, 
   return BDC_OK;
 }
 
+int bdc_draw_tasks(BdcSession* s, uint64_t seed, int64_t B, int32_t T, int32_t E, int32_t D, int32_t n_splits,
+                   int32_t n_disc, const int32_t* attempt, const uint8_t* redraw, uint8_t* splits,
+                   int64_t* discos, uint8_t* inj, void* stream) {
+  if (!s) return fail(BDC_EINVAL, "null session");
+  if (B < 0 || T < 0 || D < 0 || n_splits < 0 || n_disc < 0) return fail(BDC_EINVAL, "negative size");
+  if (B == 0) return BDC_OK;
+  if (!splits || (D > 0 && !discos))
+    return fail(BDC_EINVAL, "missing output pointer");
+  if (E < s->g.E) return fail(BDC_EINVAL, "split width E is smaller than the widest substation");
+  if (n_splits > RMAX || n_disc > MMAX || n_disc > D) return fail(BDC_ELIMIT, "too many splits or disconnections");
+  cudaError_t e = cudaSetDevice(s->device);
+  if (e != cudaSuccess) return fail(BDC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  GenArgs a{};
+  a.B = B; a.T = T; a.E = E; a.D = D; a.n_splits = n_splits; a.n_disc = n_disc;
+  a.k0 = (uint32_t)seed; a.k1 = (uint32_t)(seed >> 32);
+  a.attempt = attempt; a.redraw = redraw; a.splits = splits; a.discos = discos; a.inj = inj;
+  e = launch_draw(s->g, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(BDC_ECUDA, std::string("bdc_draw_tasks: ") + cudaGetErrorString(e));
+  return BDC_OK;
+}
+
 int bdc_session_set_wave(BdcSession* s, int64_t cap) {
   if (!s) return fail(BDC_EINVAL, "null session");
   s->wave_cap = cap;

@@ -331,6 +331,19 @@ void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_rescore(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+
+// Device task generation (bdc_gen.cu, bdc_draw_tasks)
+struct GenArgs {
+  int64_t B;
+  int T, E, D, n_splits, n_disc;
+  uint32_t k0, k1;         // Philox key (the seed)
+  const int32_t* attempt;  // (B) draw number per task, or null (0)
+  const uint8_t* redraw;   // (B) 1 = draw this task's topology, or null (all)
+  uint8_t* splits;         // (B, S, E)
+  int64_t* discos;         // (B, D) or null
+  uint8_t* inj;            // (B, T, K) or null (topology only)
+};
+cudaError_t launch_draw(const DevGrid& g, const GenArgs& a, cudaStream_t s);
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s);
 int kernels_per_wave(const DevGrid& g, const Work& w);

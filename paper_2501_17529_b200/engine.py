@@ -124,6 +124,7 @@ EXPORTS = (
     "bdc_probe_flows",
     "bdc_session_set_wave",
     "bdc_scan_tasks",
+    "bdc_draw_tasks",
 )
 
 _lib = None
@@ -151,6 +152,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.bdc_probe_flows.argtypes = [_P, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P, _P, _P]
         lib.bdc_session_set_wave.argtypes = [_P, ctypes.c_int64]
         lib.bdc_scan_tasks.argtypes = [_P, _P, _P, ctypes.c_int64, ctypes.c_int32, _P, _P, _P]
+        lib.bdc_draw_tasks.argtypes = [_P, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, _P, _P]
         _lib = lib
         return lib
 
