@@ -64,6 +64,13 @@ struct Stream {
 };
 
 constexpr uint32_t P_SUBS = 1, P_BITS = 2, P_DISC = 3, P_INJ = 4;
+
+// a branch the reference can disconnect: a retained PTDF row with both endpoint columns
+// (folded ones raise ValidationError, which random_tasks rejects, bench.py:108-109)
+__device__ __forceinline__ bool outageable(const DevGrid& g, int k) {
+  const int r = g.branch_row[k];
+  return r >= 0 && g.row_from[r] >= 0 && g.row_to[r] >= 0;
+}
 constexpr int GEN_SMAX = 4096;  // eligible substations staged in shared memory
 
 // Topology draw of the masked tasks: one warp per task.  Clears the task's (S, E) split
@@ -74,12 +81,12 @@ __global__ void k_gen_topo(DevGrid g, GenArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) { nel = 0; nret = 0; }
   __syncthreads();
-  // branches retained in the PTDF rows (a disconnection of a folded branch is a
-  // ValidationError the reference rejects, bench.py:108-109: drawing among the retained
-  // ones directly gives the same conditional distribution)
+  // branches that can be disconnected (a disconnection of a folded branch is a
+  // ValidationError the reference rejects, bench.py:108-109: drawing among the others
+  // directly gives the same conditional distribution)
   {
     int c = 0;
-    for (int k = threadIdx.x; k < g.NBR; k += blockDim.x) c += g.branch_row[k] >= 0;
+    for (int k = threadIdx.x; k < g.NBR; k += blockDim.x) c += outageable(g, k);
     atomicAdd(&nret, c);
   }
   // eligible substations (>= 2 branch elements), ascending: the reference's `eligible`
@@ -158,7 +165,7 @@ __global__ void k_gen_topo(DevGrid g, GenArgs a) {
       if (nr != g.NBR) {  // the pick[i]-th retained branch
         int c = -1;
         for (int k = 0; k < g.NBR; ++k)
-          if (g.branch_row[k] >= 0 && ++c == pick[i]) { br = k; break; }
+          if (outageable(g, k) && ++c == pick[i]) { br = k; break; }
       }
       dc[i] = br;
     }

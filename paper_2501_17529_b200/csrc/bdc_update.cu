@@ -294,10 +294,15 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
     if (tid == 0)
       for (int i = 0; i < d; ++i) {
         int row = s.orow[i];
+        if (row < 0) { s.fail = BDC_TASK_DETACHED; s.farg = -4; break; }
         s.ofc[i] = curcol(s, rh_key, rh_col, row, 0, g.row_from[row]);
         s.otc[i] = curcol(s, rh_key, rh_col, row, 1, g.row_to[row]);
+        // a folded endpoint column cannot be outaged (the host raises the reference's
+        // ValidationError first, Engine._check_outage_columns); never read column -1
+        if (s.ofc[i] < 0 || s.otc[i] < 0) { s.fail = BDC_TASK_DETACHED; s.farg = -4; }
       }
     __syncthreads();
+    if (s.fail) goto done;
     if (cfg.method == 0) {
       // MODF: one d x d inner system against the post-split matrix (factors.py:373-425)
       // rhs[i][r] = P'[r, f'_i] - P'[r, t'_i] into B slots k+i

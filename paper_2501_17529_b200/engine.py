@@ -212,6 +212,7 @@ class Engine:
                 slots_per_sub[si] += 1
         self.slots_per_sub = slots_per_sub
         branch_row = np.ascontiguousarray(base.branch_rows.astype(np.int32))
+        self.branch_row = branch_row
         self._keep = keep = {}
 
         def arr(name, a, dt):
@@ -315,6 +316,8 @@ class Engine:
         if rc != 0:
             raise EngineUnavailable(f"bdc_scan_tasks failed ({rc}): {_err(self.lib)}")
         rmax, dmax, amax = int(mr.value), int(md.value), int(ma.value)
+        if dmax > 0:
+            self._check_outage_columns(dc)
         if rmax > MAX_RANK:
             raise ValidationError(
                 f"a task applies {rmax} splits + disconnections; the engine supports {MAX_RANK}"
@@ -329,6 +332,33 @@ class Engine:
                 f"a task moves {amax} injection slots; the engine supports {MAX_ACTIVE_SLOTS}"
             )
         return max(rmax, 1)
+
+    def _check_outage_columns(self, discos: np.ndarray) -> None:
+        """A disconnection needs a retained row with both endpoint columns present: the
+        reference raises ValidationError for the batch otherwise (`factors.py:65-67`,
+        `compute_modf` `:391-392`, `lodf_column` `:345-346`), for the first such task."""
+        tb = self.tables
+        d = discos[discos >= 0] if discos.size else discos
+        if not d.size:
+            return
+        rows = self.branch_row[d]
+        bad_rows = rows < 0
+        safe = np.where(bad_rows, 0, rows)
+        folded = (np.asarray(tb.row_from)[safe] < 0) | (np.asarray(tb.row_to)[safe] < 0)
+        if not (bad_rows | folded).any():
+            return
+        for b in range(discos.shape[0]):
+            for k in discos[b]:
+                k = int(k)
+                if k < 0:
+                    continue
+                r = int(self.branch_row[k])
+                if r < 0:
+                    raise ValidationError(f"branch {k} has no retained PTDF row")
+                if tb.row_from[r] < 0 or tb.row_to[r] < 0:
+                    if self.config.multi_outage_method == "sequential":
+                        raise ValidationError(f"branch {k}: endpoint column folded, cannot outage")
+                    raise ValidationError("outage branch endpoint column folded")
 
     # ------------------------------------------------------------------ solve
     def solve(

@@ -30,7 +30,7 @@ import numpy as np
 import scipy.sparse as sp
 from scipy.sparse.csgraph import connected_components
 
-from .grid import Grid
+from .grid import Grid, static_injection_fold
 from .io import grid_from_dict
 
 
@@ -197,6 +197,15 @@ def make_grid(spec: GridSpec | str, seed: int = 0) -> Grid:
 
 
 # ----------------------------------------------------------------------------- tasks
+def folded_branches(grid: Grid) -> np.ndarray:
+    """Branches with an endpoint folded into the static column of the base PTDF
+    (`reduce_static`, factors.py:219-275): they cannot be disconnected."""
+    static = np.array(sorted(static_injection_fold(grid).static_nodes), dtype=np.int64)
+    if not len(static):
+        return np.zeros(grid.n_branches, dtype=bool)
+    return np.isin(grid.from_nodes, static) | np.isin(grid.to_nodes, static)
+
+
 def _feasible_mask(grid: Grid, splits: np.ndarray, discos: np.ndarray) -> np.ndarray:
     """N-0 feasibility of each task: no degenerate split and a connected topology."""
     B = splits.shape[0]
@@ -295,6 +304,10 @@ def random_task_arrays(
         inj = rng.integers(0, 2, size=(n, ti_size, K)).astype(bool)
         if reject_infeasible:
             keep = _feasible_mask(grid, splits, discos)
+            if n_disconnections:
+                # a branch with a folded endpoint cannot be disconnected (ValidationError in
+                # the reference, which random_tasks rejects, bench.py:108-109)
+                keep &= ~folded_branches(grid)[discos].any(axis=1)
             splits, discos, inj = splits[keep], discos[keep], inj[keep]
         take = min(len(splits), n_tasks - have)
         out_s.append(splits[:take])

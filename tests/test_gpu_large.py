@@ -228,3 +228,28 @@ def test_multi_device_sessions():
     outs = [solve_batch_output(session_open(grid, device=d), splits, discos, inj) for d in range(2)]
     assert np.array_equal(outs[0].best, outs[1].best)
     assert np.array_equal(outs[0].metric, outs[1].metric, equal_nan=True)
+
+
+def test_folded_endpoint_disconnection_raises():
+    """Disconnecting a branch whose endpoint column is folded into the static column is a
+    batch-level ValidationError in the reference (compute_modf, factors.py:391-392;
+    lodf_column :345-346), raised before any device work -- and never an out-of-bounds
+    column read on the device."""
+    from dataclasses import replace
+
+    from paper_2501_17529_b200 import synth
+    from paper_2501_17529_b200.errors import ValidationError
+    from paper_2501_17529_b200.session import session_open, solve_batch
+
+    grid = synth.make_grid("g1k", seed=0)
+    folded = np.flatnonzero(synth.folded_branches(grid))
+    assert len(folded)
+    sess = session_open(grid)
+    splits, discos, inj = synth.random_task_arrays(grid, 3, 4, 2, seed=9, n_disconnections=1)
+    discos = discos.copy()
+    discos[1, 0] = folded[0]
+    with pytest.raises(ValidationError, match="outage branch endpoint column folded"):
+        solve_batch(sess, splits, discos, inj)
+    seq = session_open(grid, replace(sess.config, multi_outage_method="sequential"))
+    with pytest.raises(ValidationError, match="endpoint column folded, cannot outage"):
+        solve_batch(seq, splits, discos, inj)
