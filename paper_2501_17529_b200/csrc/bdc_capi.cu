@@ -468,7 +468,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_s32 = L.add(g.s_mon ? 16 : B * (size_t)g.N1 * T * 4), o_bk = L.add(B * (size_t)g.N1 * 4);
   size_t o_rmx = L.add(B * (size_t)(g.M > 0 ? g.M : 1) * 4);
   size_t o_top = L.add(B * (size_t)TOPC * 4), o_done = L.add(B * (size_t)g.N1);
-  const int nslot = RSEL_WARPS + (g.N1 + RCW - 1) / RCW;
+  const int nslot = RSEL_WARPS + (g.N1 + RCW_MIN - 1) / RCW_MIN;
   size_t o_rl = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_rc = L.add(B * 4), o_th = L.add(B * 4);
   size_t o_pc = L.add(B * nslot * KMAX * 4), o_pp = L.add(B * nslot * KMAX * 4);
   size_t o_pf = L.add(B * nslot * KMAX * 8), o_pr = L.add(B * nslot * KMAX * 8), o_pm = L.add(B * nslot * 8);
@@ -520,6 +520,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.queue = (int2*)(base + o_q);
   x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
   x.rlist = (int*)(base + o_rl); x.rcnt = (int*)(base + o_rc); x.theta = (float*)(base + o_th); x.nslot = nslot;
+  {  // wide tiles when tasks alone fill the GPU (tests force either: BDC_RSWEEP_WIDE=0/1)
+    const char* wide = std::getenv("BDC_RSWEEP_WIDE");
+    x.rcw = wide ? (wide[0] == '1' ? RCW : RCW_MIN) : (Wb >= 1024 ? RCW : RCW_MIN);
+  }
   x.pcase = (int*)(base + o_pc); x.ppos = (int*)(base + o_pp);
   x.pflow = (double*)(base + o_pf); x.prel = (double*)(base + o_pr); x.pmax = (double*)(base + o_pm);
   return L.total;

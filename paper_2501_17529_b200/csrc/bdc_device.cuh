@@ -57,7 +57,10 @@ __host__ __device__ inline int screen_block_rows(int M) {
   const int per = (M + SB - 1) / SB;
   return ((per + 31) / 32) * 32 > 0 ? ((per + 31) / 32) * 32 : 32;
 }
-constexpr int RCW = 64;         // single cases per CTA of the winner report sweep (8 per warp)
+// single cases per CTA of the winner report sweep: RCW on batches of many tasks (one CTA
+// per task covers most listings), RCW_MIN where few tasks must fill the GPU (Work::rcw)
+constexpr int RCW = 160;
+constexpr int RCW_MIN = 64;
 constexpr int RSEL_WARPS = 8;   // partial report lists written by the report-select kernel
 
 // Grid tables, device-resident for the session lifetime.
@@ -159,7 +162,8 @@ struct Work {
   int* rlist;     // (Wb, N1)      single cases the FP64 report must visit, ascending
   int* rcnt;      // (Wb)          their number
   float* theta;   // (Wb)          report floor: kg-th largest exact case max - 2 eps (or -1)
-  int nslot;      // RSEL_WARPS + ceil(N1 / RCW) partial lists per task
+  int nslot;      // RSEL_WARPS + ceil(N1 / RCW_MIN) partial lists per task
+  int rcw;        // single cases per k_rsweep CTA (RCW or RCW_MIN)
   int* pcase;     // (Wb, nslot, KMAX) contingency order of each partial entry
   int* ppos;      // (Wb, nslot, KMAX) monitored position
   double* pflow;  // (Wb, nslot, KMAX)

@@ -631,30 +631,31 @@ __global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCf
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
   const int n = w.rcnt[b];
-  if (tile * RCW >= n) return;
+  const int RC = w.rcw;
+  if (tile * RC >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kc = cfg.kc, kg = cfg.kg;
-  const int base = tile * RCW, ncs = min(n, base + RCW) - base;
+  const int base = tile * RC, ncs = min(n, base + RC) - base;
   extern __shared__ __align__(16) double rsm[];
   double* sB = rsm;                  // [2][rt][SRC] B'' on the chunk's monitored rows
   double* sN = sB + 2 * rs * SRC;    // [2][SRC] N-0 column
   double* sI = sN + 2 * SRC;         // [2][SRC] 1 / rating
-  double* sWc = sI + 2 * SRC;        // [RCW][rs] the cases' W rows
-  double* cRel = sWc + RCW * rs;     // [RCW][KC] each case's running top-kc
-  double* cFlow = cRel + RCW * KC;
-  double* sIdn = cFlow + RCW * KC;   // [RCW] 1 / den
-  double* sSc = sIdn + RCW;          // [RCW] N-0 flow of the outaged row
-  int* cPos = (int*)(sSc + RCW);     // [RCW][KC]
-  int* sC = cPos + RCW * KC;         // [RCW] case index
-  int* sOwn = sC + RCW;              // [RCW] monitored position of the outaged row
-  int* cN = sOwn + RCW;              // [RCW] entries in the case's list
+  double* sWc = sI + 2 * SRC;        // [RC][rs] the cases' W rows
+  double* cRel = sWc + RC * rs;     // [RC][KC] each case's running top-kc
+  double* cFlow = cRel + RC * KC;
+  double* sIdn = cFlow + RC * KC;   // [RC] 1 / den
+  double* sSc = sIdn + RC;          // [RC] N-0 flow of the outaged row
+  int* cPos = (int*)(sSc + RC);     // [RC][KC]
+  int* sC = cPos + RC * KC;         // [RC] case index
+  int* sOwn = sC + RC;              // [RC] monitored position of the outaged row
+  int* cN = sOwn + RC;              // [RC] entries in the case's list
   __shared__ WarpList wl[RW];
   __shared__ double wmax[RW];
   __shared__ int sdeadp[RMAX];  // monitored positions of the disconnected rows (-1: unmonitored)
   const int nd = w.ndead[b];
   if (tid < nd) sdeadp[tid] = g.row_mon_pos[w.dead[(size_t)b * RMAX + tid]];
   if (lane == 0) wl[wid].n = 0;
-  for (int i = tid; i < RCW; i += RT) {
+  for (int i = tid; i < RC; i += RT) {
     const int c = i < ncs ? w.rlist[(size_t)b * N1 + base + i] : -1;
     sC[i] = c;
     cN[i] = 0;
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCf
     }
     cp_commit();
   };
-  // chunk-outer, case-inner: the staged B'' chunk serves all RCW cases of the tile; each
+  // chunk-outer, case-inner: the staged B'' chunk serves all RC cases of the tile; each
   // warp evaluates CQ of its cases at once (the B'' loads shared by the CQ columns) and
   // folds each case's chunk top-kc into the case's running list
   const int nchunks = (M + SRC - 1) / SRC;
@@ -845,7 +846,7 @@ __global__ void k_rmerge(DevGrid g, DevCfg cfg, Work w) {
   const int b = gt >> 5, lane = gt & 31;
   if (b >= w.Wb || w.status[b] != 0) return;
   const int kg = cfg.kg;
-  const int nsl = RSEL_WARPS + (w.rcnt[b] + RCW - 1) / RCW;
+  const int nsl = RSEL_WARPS + (w.rcnt[b] + w.rcw - 1) / w.rcw;
   double mx = 0.0;
   for (int s = lane; s < nsl; s += 32) mx = fmax(mx, w.pmax[(size_t)b * w.nslot + s]);
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1458,9 +1459,9 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
 }
 
 namespace {
-size_t rsweep_dyn_bytes(int rs, int kc, int src) {
-  return (2 * (size_t)rs * src + 4 * (size_t)src + (size_t)RCW * rs + 2 * (size_t)RCW * kc + 2 * RCW) *
-             sizeof(double) + ((size_t)RCW * kc + 3 * RCW) * sizeof(int);
+size_t rsweep_dyn_bytes(int rs, int kc, int src, int rcw) {
+  return (2 * (size_t)rs * src + 4 * (size_t)src + (size_t)rcw * rs + 2 * (size_t)rcw * kc + 2 * rcw) *
+             sizeof(double) + ((size_t)rcw * kc + 3 * rcw) * sizeof(int);
 }
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
@@ -1477,8 +1478,8 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
     const char* cq_env = getenv("BDC_RSWEEP_CQ");
     const int cq = cq_env ? atoi(cq_env) : (g.M <= 2048 ? 1 : 4);
     const int rpl = cq == 1 && g.M <= 64 ? 2 : cq == 1 && g.M > 128 && g.M <= 192 ? 6 : 4;
-    const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl);
-    const dim3 grid(w.nslot - RSEL_WARPS, w.Wb);
+    const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl, w.rcw);
+    const dim3 grid((g.N1 + w.rcw - 1) / w.rcw, w.Wb);
     auto go = [&](auto kern) {
       smem_opt_in((const void*)kern, (int)dyn);
       kern<<<grid, RT, dyn, s>>>(g, c, w);

@@ -277,6 +277,11 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
         monkeypatch.delenv(env[0])
         assert np.array_equal(warp.best, alt.best), env
         assert np.array_equal(warp.metric, alt.metric, equal_nan=True), env
+    monkeypatch.setenv("BDC_RSWEEP_WIDE", "1")  # 160-case sweep tiles (batches >= 1024 tasks)
+    wide = eng.solve(*args)
+    monkeypatch.delenv("BDC_RSWEEP_WIDE")
+    assert np.array_equal(warp.metric, wide.metric, equal_nan=True)
+    assert warp.reports() == wide.reports()
     for cq in ("1", "4"):
         monkeypatch.setenv("BDC_RSWEEP_CQ", cq)
         alt = eng.solve(*args)
