@@ -20,6 +20,8 @@
  *                           every flow vector of one task, for parity checks.
  *   bdc_draw_tasks       <- batchdc.bench.random_tasks (src/batchdc/bench.py:33-91),
  *                           drawn on the device.
+ *   bdc_spd_solve        <- the SPD solve of batchdc.factors.compute_ptdf
+ *                           (src/batchdc/factors.py:161-216), on the device (8(f) row 3).
  *   bdc_scan_tasks       <- the rank / outage-cap checks of canonicalize_task and
  *                           _branch_stage (solver.py:148-197, 390-394), vectorised.
  *   bdc_session_destroy  <- (session lifetime end; the reference relies on GC)
@@ -221,6 +223,14 @@ int bdc_draw_tasks(BdcSession* session, uint64_t seed, int64_t B, int32_t T, int
                    int32_t n_splits, int32_t n_disconnections, const int32_t* attempt,
                    const uint8_t* redraw, uint8_t* splits, int64_t* discos, uint8_t* inj,
                    void* stream);
+
+/* Dense SPD solve on the device (the base-PTDF setup, compute_ptdf factors.py:161-216,
+ * i.e. scipy.linalg.solve(L, A^T, assume_a="pos") = LAPACK potrf + potrs): A (n x n,
+ * row-major, lower triangle read, overwritten by its Cholesky factor) and B (n x m,
+ * overwritten by A^-1 B) are DEVICE pointers; *info (device int) is set to 0 or to the
+ * first non-positive pivot's column + 1 (the caller reads it after synchronising).
+ * Runs on `stream` (NULL: the default stream). */
+int bdc_spd_solve(int device, double* A, int32_t n, double* B, int32_t m, int32_t* info, void* stream);
 
 /* Set the wave size cap (tasks per device wave); 0 = automatic. */
 int bdc_session_set_wave(BdcSession* session, int64_t max_tasks_per_wave);

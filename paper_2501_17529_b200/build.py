@@ -9,7 +9,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = ["bdc_update.cu", "bdc_single.cu", "bdc_scale.cu", "bdc_flows.cu", "bdc_report.cu", "bdc_gen.cu",
-           "bdc_capi.cu"]
+           "bdc_chol.cu", "bdc_capi.cu"]
 TARGET = os.path.join(HERE, "libbdc.so")
 FLAGS = [
     "-std=c++17",

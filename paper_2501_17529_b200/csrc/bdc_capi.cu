@@ -411,6 +411,16 @@ int bdc_draw_tasks(BdcSession* s, uint64_t seed, int64_t B, int32_t T, int32_t E
   return BDC_OK;
 }
 
+int bdc_spd_solve(int device, double* A, int32_t n, double* B, int32_t m, int32_t* info, void* stream) {
+  if (n < 0 || m < 0) return fail(BDC_EINVAL, "negative size");
+  if (n == 0) return BDC_OK;
+  if (!A || (m > 0 && !B) || !info) return fail(BDC_EINVAL, "missing pointer");
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = launch_spd_solve(A, n, B, m, info, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(BDC_ECUDA, std::string("bdc_spd_solve: ") + cudaGetErrorString(e));
+  return BDC_OK;
+}
+
 int bdc_session_set_wave(BdcSession* s, int64_t cap) {
   if (!s) return fail(BDC_EINVAL, "null session");
   s->wave_cap = cap;

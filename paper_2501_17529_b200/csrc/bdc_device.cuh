@@ -139,6 +139,7 @@ struct Work {
   unsigned* rsq_n;  // their number (device counter, reset per wave)
   int screen;     // 1 = exact dominance screen on
   int rescore_full;  // 1 = k_rescore evaluates every class over every row (tests)
+  int scale_tgfast;  // 1 = k_scale_tc rasterises task groups fastest (large D' tables)
   int rsel_cta;   // 1: winner report selection always CTA-per-task (test knob BDC_RSEL_CTA)
   int ptop;       // cases evaluated first (the TOP tile, ranked by screening key)
   int ranked;     // 1: top tile chosen by the screening key (screen on and N1 > ptop)
@@ -348,6 +349,11 @@ struct GenArgs {
   uint8_t* inj;            // (B, T, K) or null (topology only)
 };
 cudaError_t launch_draw(const DevGrid& g, const GenArgs& a, cudaStream_t s);
+
+// SPD solve A X = B on the device (bdc_chol.cu, bdc_spd_solve): A (n x n, row-major,
+// overwritten by its Cholesky factor), B (n x m, overwritten by X); info (device int):
+// 0, or the first non-positive pivot's column + 1
+cudaError_t launch_spd_solve(double* A, int n, double* B, int m, int* info, cudaStream_t s);
 void launch_probe(const DevGrid& g, const Work& w, double* n0, double* n1, uint8_t* ok,
                   cudaStream_t s);
 int kernels_per_wave(const DevGrid& g, const Work& w);

@@ -23,6 +23,8 @@
 // tasks); one elected thread issues the MMAs and commits them to an mbarrier.
 #include "bdc_device.cuh"
 
+#include <cstdlib>
+
 #include <cuda.h>
 
 #include <algorithm>
@@ -106,8 +108,12 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
   constexpr int ABYTES = SM_CASES * 32, BBYTES = SM_ROWS * 32;  // one K block of A / B
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, wg = wid >> 2;
   const int ci = (wid & 3) * 32 + lane;  // this thread's case within the tile (= TMEM lane)
-  const int c0 = blockIdx.x * SM_CASES, c = c0 + ci;
-  const int tb0 = blockIdx.y * TB;
+  // raster: case tile fastest (a task group's B operands stay in L2 across its case tiles)
+  // or, when the D' table outgrows L2, task group fastest (each D' slab is read from HBM
+  // once and shared in L2 by every task group)
+  const bool tgf = w.scale_tgfast != 0;
+  const int c0 = (tgf ? blockIdx.y : blockIdx.x) * SM_CASES, c = c0 + ci;
+  const int tb0 = (tgf ? blockIdx.x : blockIdx.y) * TB;
   const int rs = w.rs, M = g.M, N1 = g.N1, T = w.T;
   const int MB = screen_block_rows(M);
   extern __shared__ __align__(1024) unsigned char ssm_raw[];
@@ -370,8 +376,14 @@ void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   const int ncols = TB * SM_ROWS <= 64 ? 64 : (TB * SM_ROWS <= 128 ? 128 : 256);
   dyn = std::max(dyn, (size_t)(220 * 1024) / (size_t)(512 / ncols));
   smem_opt_in((const void*)k_scale_tc<TB, KB>, (int)dyn);
-  const dim3 grid((g.N1 + SM_CASES - 1) / SM_CASES, (w.Wb + TB - 1) / TB);
-  k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, w, *g.tm_ds);
+  const int nct = (g.N1 + SM_CASES - 1) / SM_CASES, ntg = (w.Wb + TB - 1) / TB;
+  // D' = N1 x Mp FP32: beyond ~96 MB (G10k: 676 MB) it no longer stays in the 126 MB L2
+  // while every task group streams it, so the task groups go fastest
+  Work wr = w;
+  const char* env = getenv("BDC_SCALE_RASTER");  // tests: 0 case tile / 1 task group fastest
+  wr.scale_tgfast = env ? (env[0] == '1') : ((size_t)g.N1 * g.Mp * 4 > ((size_t)96 << 20));
+  const dim3 grid(wr.scale_tgfast ? ntg : nct, wr.scale_tgfast ? nct : ntg);
+  k_scale_tc<TB, KB><<<grid, 2 * SM_CASES, dyn, s>>>(g, wr, *g.tm_ds);
 }
 }  // namespace
 

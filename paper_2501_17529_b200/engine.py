@@ -125,6 +125,7 @@ EXPORTS = (
     "bdc_session_set_wave",
     "bdc_scan_tasks",
     "bdc_draw_tasks",
+    "bdc_spd_solve",
 )
 
 _lib = None
@@ -152,6 +153,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.bdc_probe_flows.argtypes = [_P, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P, _P, _P]
         lib.bdc_session_set_wave.argtypes = [_P, ctypes.c_int64]
         lib.bdc_scan_tasks.argtypes = [_P, _P, _P, ctypes.c_int64, ctypes.c_int32, _P, _P, _P]
+        lib.bdc_spd_solve.argtypes = [ctypes.c_int, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P]
         lib.bdc_draw_tasks.argtypes = [_P, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, _P, _P]
         _lib = lib

@@ -82,8 +82,73 @@ def _laplacian(grid: Grid) -> tuple[np.ndarray, np.ndarray]:
     return lap, inc
 
 
-def compute_ptdf(grid: Grid, retained_rows: Optional[Sequence[int]] = None) -> PtdfMatrix:
-    """One SPD factorisation of the slack-reduced Laplacian (`factors.py:161-216`)."""
+def _spd_solve_device(lap, rhs, device: int):
+    """lap^-1 rhs for SPD `lap` on the GPU (`bdc_spd_solve`: blocked FP64 potrf + potrs,
+    csrc/bdc_chol.cu), the device counterpart of scipy.linalg.solve(assume_a="pos").
+    numpy arrays in -> numpy out; CUDA tensors in -> the solution as a CUDA tensor
+    (`lap` and `rhs` are overwritten)."""
+    import ctypes
+
+    import torch
+
+    from .engine import _err, load_library
+
+    lib = load_library()
+    on_dev = isinstance(lap, torch.Tensor)
+    n, m = lap.shape[0], rhs.shape[1]
+    dev = torch.device("cuda", device)
+    A = lap if on_dev else torch.from_numpy(np.ascontiguousarray(lap, dtype=np.float64)).to(dev)
+    B = rhs if on_dev else torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64)).to(dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    rc = lib.bdc_spd_solve(int(device), ctypes.c_void_p(A.data_ptr()), int(n), ctypes.c_void_p(B.data_ptr()),
+                           int(m), ctypes.c_void_p(info.data_ptr()), ctypes.c_void_p(st.cuda_stream))
+    if rc != 0:
+        raise SingularSystem(f"susceptance matrix factorization failed: {_err(lib)}")
+    bad = int(info.item())
+    if bad:
+        raise SingularSystem(
+            f"susceptance matrix factorization failed: {bad}-th leading minor not positive definite")
+    return B if on_dev else B.cpu().numpy()
+
+
+def _ptdf_values_device(grid: Grid, rows: np.ndarray, keep: np.ndarray, device: int) -> np.ndarray:
+    """PTDF values (len(rows), n_nodes) with the susceptance matrix and the incidence
+    right-hand side assembled on the device from the branch list (no dense host
+    matrices), solved by `bdc_spd_solve`, the slack column left at zero."""
+    import scipy.sparse as sps
+    import torch
+
+    dev = torch.device("cuda", device)
+    n, nk = grid.n_nodes, len(keep)
+    f, t, b = grid.from_nodes, grid.to_nodes, grid.susceptances
+    # Laplacian entries (duplicates -- parallel branches -- summed), slack row/column dropped
+    lap = sps.coo_matrix((np.concatenate([b, b, -b, -b]),
+                          (np.concatenate([f, t, f, t]), np.concatenate([f, t, t, f]))), shape=(n, n)).tocsr()
+    pos = np.full(n, -1, dtype=np.int64)
+    pos[keep] = np.arange(nk)
+    coo = lap[keep][:, keep].tocoo()
+    L = torch.zeros((nk, nk), dtype=torch.float64, device=dev)
+    L[torch.from_numpy(coo.row.astype(np.int64)).to(dev), torch.from_numpy(coo.col.astype(np.int64)).to(dev)] = \
+        torch.from_numpy(coo.data).to(dev)
+    # right-hand side A^T (nk x R): column r holds +b_r at its from node, -b_r at its to node
+    R = len(rows)
+    rhs = torch.zeros((nk, R), dtype=torch.float64, device=dev)
+    for ends, sign in ((f, 1.0), (t, -1.0)):
+        p = pos[ends[rows]]
+        ok = p >= 0
+        rhs[torch.from_numpy(p[ok]).to(dev), torch.from_numpy(np.flatnonzero(ok)).to(dev)] += \
+            torch.from_numpy(sign * b[rows][ok]).to(dev)
+    X = _spd_solve_device(L, rhs, device)
+    vals = torch.zeros((R, n), dtype=torch.float64, device=dev)
+    vals[:, torch.from_numpy(keep).to(dev)] = X.T
+    return vals.cpu().numpy()
+
+
+def compute_ptdf(grid: Grid, retained_rows: Optional[Sequence[int]] = None,
+                 device: Optional[int] = None) -> PtdfMatrix:
+    """One SPD factorisation of the slack-reduced Laplacian (`factors.py:161-216`); with
+    `device` the factorisation and solve run on that GPU."""
     if retained_rows is None:
         rows = np.arange(grid.n_branches, dtype=np.int64)
     else:
@@ -98,16 +163,19 @@ def compute_ptdf(grid: Grid, retained_rows: Optional[Sequence[int]] = None) -> P
                 "retained rows must include substation/contingency branches, "
                 f"missing {sorted(missing)}"
             )
-    lap, inc = _laplacian(grid)
     keep = np.array([i for i in range(grid.n_nodes) if i != grid.slack], dtype=np.int64)
-    try:
-        part = scipy.linalg.solve(
-            lap[np.ix_(keep, keep)], inc[rows][:, keep].T, assume_a="pos"
-        ).T
-    except (scipy.linalg.LinAlgError, np.linalg.LinAlgError) as exc:
-        raise SingularSystem(f"susceptance matrix factorization failed: {exc}") from exc
-    values = np.zeros((len(rows), grid.n_nodes))
-    values[:, keep] = part
+    if device is not None:
+        values = _ptdf_values_device(grid, rows, keep, device)
+    else:
+        lap, inc = _laplacian(grid)
+        try:
+            part = scipy.linalg.solve(
+                lap[np.ix_(keep, keep)], inc[rows][:, keep].T, assume_a="pos"
+            ).T
+        except (scipy.linalg.LinAlgError, np.linalg.LinAlgError) as exc:
+            raise SingularSystem(f"susceptance matrix factorization failed: {exc}") from exc
+        values = np.zeros((len(rows), grid.n_nodes))
+        values[:, keep] = part
     branch_rows = np.full(grid.n_branches, -1, dtype=np.int64)
     branch_rows[rows] = np.arange(len(rows))
     return PtdfMatrix(
@@ -165,10 +233,12 @@ def reduce_static(
 
 
 def prepare_base_ptdf(
-    grid: Grid, retained_rows: Optional[Sequence[int]] = None, fold_static: bool = True
+    grid: Grid, retained_rows: Optional[Sequence[int]] = None, fold_static: bool = True,
+    device: Optional[int] = None,
 ) -> PtdfMatrix:
-    """Factorise once and fold static injections (`factors.py:597-612`)."""
-    ptdf = compute_ptdf(grid, retained_rows)
+    """Factorise once and fold static injections (`factors.py:597-612`); `device` runs the
+    SPD solve on that GPU."""
+    ptdf = compute_ptdf(grid, retained_rows, device=device)
     if not fold_static:
         return ptdf
     fold = static_injection_fold(grid)

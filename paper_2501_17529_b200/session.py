@@ -69,9 +69,13 @@ class SolverSession:
 
 
 def session_open(
-    grid: GridSource, config: Optional[SolveConfig] = None, device: int = 0
+    grid: GridSource, config: Optional[SolveConfig] = None, device: int = 0, base_setup: str = "host"
 ) -> SolverSession:
-    """Load a grid, prepare its base PTDF once and upload it (`session.py:92-113`)."""
+    """Load a grid, prepare its base PTDF once and upload it (`session.py:92-113`).
+
+    ``base_setup="gpu"`` factorises the susceptance matrix on the session's GPU
+    (`bdc_spd_solve`) instead of the host's scipy SPD solve; the base agrees to rounding
+    (the reference's own bits come from the host path, the default)."""
     if isinstance(grid, (str, Path)):
         loaded = load_grid(str(grid))
     elif isinstance(grid, dict):
@@ -82,7 +86,9 @@ def session_open(
         raise ValidationError(f"unsupported grid source: {type(grid).__name__}")
     cfg = config if config is not None else SolveConfig()
     cfg.validate()
-    base = prepare_base_ptdf(loaded)
+    if base_setup not in ("host", "gpu"):
+        raise ValidationError(f"unknown base_setup {base_setup!r}")
+    base = prepare_base_ptdf(loaded, device=device if base_setup == "gpu" else None)
     return SolverSession(
         grid=loaded,
         base=base,

@@ -277,6 +277,13 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
         monkeypatch.delenv(env[0])
         assert np.array_equal(warp.best, alt.best), env
         assert np.array_equal(warp.metric, alt.metric, equal_nan=True), env
+    # k_scale_tc with task groups rasterised fastest (the large-grid order): same bounds
+    monkeypatch.setenv("BDC_SCALE_RASTER", "1")
+    ras = eng.solve(*args)
+    monkeypatch.delenv("BDC_SCALE_RASTER")
+    assert np.array_equal(warp.best, ras.best)
+    assert np.array_equal(warp.metric, ras.metric, equal_nan=True)
+    assert warp.n1_pairs == ras.n1_pairs
     monkeypatch.setenv("BDC_RSWEEP_WIDE", "1")  # 160-case sweep tiles (batches >= 1024 tasks)
     wide = eng.solve(*args)
     monkeypatch.delenv("BDC_RSWEEP_WIDE")
