@@ -25,7 +25,9 @@ from .grid import (
     Grid,
     Injection,
     SplittableSubstation,
+    branch_bridges,
     build_grid,
+    replace_stub_branches,
     static_injection_fold,
 )
 from .io import grid_from_dict, grid_to_dict, load_grid, result_to_dict

@@ -317,3 +317,130 @@ def static_injection_fold(grid: Grid, movable: Optional[Iterable[int]] = None) -
     effective = tuple(sorted(required))
     static = tuple(i for i in range(grid.n_nodes) if i not in required)
     return StaticFold(static_nodes=static, effective_nodes=effective, static_power=power)
+
+
+# -- stub-branch replacement ------------------------------------
+def branch_bridges(grid: Grid) -> frozenset[int]:
+    """Branches whose removal disconnects the grid (`Grid.bridges`, grid.py:183-189).
+
+    Tarjan's low-link over branch ids, iteratively: the DFS skips only the branch it
+    arrived by (not every branch back to the parent node), so a node pair joined by
+    parallel branches is never a bridge."""
+    n = grid.n_nodes
+    adj: list[list[tuple[int, int]]] = [[] for _ in range(n)]
+    for k, b in enumerate(grid.branches):
+        adj[b.from_node].append((b.to_node, k))
+        adj[b.to_node].append((b.from_node, k))
+    order = [-1] * n
+    low = [0] * n
+    out: set[int] = set()
+    clock = 0
+    for root in range(n):
+        if order[root] >= 0:
+            continue
+        order[root] = low[root] = clock
+        clock += 1
+        stack = [(root, -1, 0)]  # (node, branch it was entered by, next adjacency index)
+        while stack:
+            v, via, i = stack[-1]
+            if i < len(adj[v]):
+                stack[-1] = (v, via, i + 1)
+                w, k = adj[v][i]
+                if k == via:
+                    continue
+                if order[w] < 0:
+                    order[w] = low[w] = clock
+                    clock += 1
+                    stack.append((w, k, 0))
+                else:
+                    low[v] = min(low[v], order[w])
+            else:
+                stack.pop()
+                if stack:
+                    u = stack[-1][0]
+                    low[u] = min(low[u], low[v])
+                    if low[v] > order[u]:
+                        out.add(via)
+    return frozenset(out)
+
+
+def _find_stub(grid: Grid):
+    """The first removable appendage in (substation, incident branch) order, or None: a
+    bridge at a substation node, not named by a contingency, whose far side holds no
+    slack, no substation node and no contingency branch (grid.py:461-478)."""
+    bridges = branch_bridges(grid)
+    named = {k for c in grid.contingencies for k in c.branches}
+    sub_nodes = {s.node for s in grid.substations}
+    adj: dict[int, list[tuple[int, int]]] = {}
+    for k, b in enumerate(grid.branches):
+        adj.setdefault(b.from_node, []).append((b.to_node, k))
+        adj.setdefault(b.to_node, []).append((b.from_node, k))
+    for si, sub in enumerate(grid.substations):
+        for k, b in enumerate(grid.branches):
+            if sub.node not in (b.from_node, b.to_node) or k not in bridges or k in named:
+                continue
+            far = b.to_node if b.from_node == sub.node else b.from_node
+            nodes, branches = {far}, set()
+            todo = [far]
+            while todo:  # everything reachable from the far end without crossing k
+                v = todo.pop()
+                for w, j in adj.get(v, ()):
+                    if j == k:
+                        continue
+                    branches.add(j)
+                    if w not in nodes:
+                        nodes.add(w)
+                        todo.append(w)
+            if grid.slack in nodes or nodes & sub_nodes or branches & named:
+                continue
+            return si, nodes, branches | {k}
+    return None
+
+
+def _carve_stub(grid: Grid, si: int, dead_nodes: set, dead_branches: set) -> Grid:
+    """The grid without one appendage; its injections move to the substation node and
+    join the substation's reassignable elements (grid.py:500-560)."""
+    from dataclasses import replace
+
+    hub = grid.substations[si].node
+    keep_nodes = [v for v in range(grid.n_nodes) if v not in dead_nodes]
+    nmap = {v: i for i, v in enumerate(keep_nodes)}
+    keep_br = [k for k in range(grid.n_branches) if k not in dead_branches]
+    bmap = {k: i for i, k in enumerate(keep_br)}
+    moved = [j for j, inj in enumerate(grid.injections) if inj.node in dead_nodes]
+    injections = tuple(
+        replace(inj, node=nmap[hub] if inj.node in dead_nodes else nmap[inj.node]) for inj in grid.injections
+    )
+    subs = []
+    for i, s in enumerate(grid.substations):
+        elems = list(s.injection_elements)
+        if i == si:
+            elems += [j for j in moved if j not in elems]
+        subs.append(SplittableSubstation(
+            node=nmap[s.node],
+            branch_elements=tuple(bmap[k] for k in s.branch_elements if k in bmap),
+            injection_elements=tuple(elems),
+        ))
+    return Grid(
+        node_ids=tuple(grid.node_ids[v] for v in keep_nodes),
+        branches=tuple(replace(grid.branches[k], from_node=nmap[grid.branches[k].from_node],
+                               to_node=nmap[grid.branches[k].to_node]) for k in keep_br),
+        injections=injections,
+        slack=nmap[grid.slack],
+        substations=tuple(subs),
+        contingencies=tuple(replace(c, branches=tuple(bmap[k] for k in c.branches)) for c in grid.contingencies),
+    )
+
+
+def replace_stub_branches(grid: Grid) -> Grid:
+    """Remove radial appendages hanging off substation nodes, to convergence
+    (`batchdc.grid.replace_stub_branches`, grid.py:437-458): each one's injections are
+    re-homed to the substation (raising the candidate count |T_i|) and
+    its branches leave the grid, monitored or not.  Returns a new validated Grid."""
+    current = grid
+    while True:
+        stub = _find_stub(current)
+        if stub is None:
+            current.validate()
+            return current
+        current = _carve_stub(current, *stub)
