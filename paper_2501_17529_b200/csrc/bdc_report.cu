@@ -625,8 +625,11 @@ __global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w)
 // top-kc (rel desc, position asc; solver.py:287-299), merged per case into the warp's
 // top-kg by (rel desc, case order, position) (_merge_entries, solver.py:302-318); the
 // CTA merges its warps' lists into one partial slot.
-template <int KC, int CQ, int RPL>  // CQ: cases per warp evaluated together; RPL: rows per lane
-__global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+// NTH threads per CTA: 256, or 128 on one-chunk grids (smaller footprint, twice the tasks
+// in flight per SM: the one-chunk sweep is latency-bound per task).
+template <int KC, int CQ, int RPL, int NTH>  // CQ: cases per warp evaluated together; RPL: rows per lane
+__global__ void __launch_bounds__(NTH, NTH == 128 ? 8 : (CQ == 1 ? 4 : 3)) k_rsweep(DevGrid g, DevCfg cfg, Work w) {
+  constexpr int RT = NTH, RW = NTH / 32;
   constexpr int SRC = 32 * RPL;  // monitored rows per chunk
   const int b = blockIdx.y, tile = blockIdx.x;
   if (w.status[b] != 0) return;
@@ -636,19 +639,23 @@ __global__ void __launch_bounds__(RT, CQ == 1 ? 4 : 3) k_rsweep(DevGrid g, DevCf
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int M = g.M, N1 = g.N1, rs = w.rs, rt = w.rank[b], kc = cfg.kc, kg = cfg.kg;
   const int base = tile * RC, ncs = min(n, base + RC) - base;
+  // one chunk (small grids): a single staging buffer and no per-case lists (each case
+  // merges straight into its warp's list) -- see rsweep_dyn_bytes
+  const bool one1 = M <= SRC;
+  const int nbf = one1 ? 1 : 2, kcl = one1 ? 0 : KC;
   extern __shared__ __align__(16) double rsm[];
-  double* sB = rsm;                  // [2][rt][SRC] B'' on the chunk's monitored rows
-  double* sN = sB + 2 * rs * SRC;    // [2][SRC] N-0 column
-  double* sI = sN + 2 * SRC;         // [2][SRC] 1 / rating
-  double* sWc = sI + 2 * SRC;        // [RC][rs] the cases' W rows
-  double* cRel = sWc + RC * rs;     // [RC][KC] each case's running top-kc
-  double* cFlow = cRel + RC * KC;
-  double* sIdn = cFlow + RC * KC;   // [RC] 1 / den
-  double* sSc = sIdn + RC;          // [RC] N-0 flow of the outaged row
-  int* cPos = (int*)(sSc + RC);     // [RC][KC]
-  int* sC = cPos + RC * KC;         // [RC] case index
-  int* sOwn = sC + RC;              // [RC] monitored position of the outaged row
-  int* cN = sOwn + RC;              // [RC] entries in the case's list
+  double* sB = rsm;                    // [nbf][rt][SRC] B'' on the chunk's monitored rows
+  double* sN = sB + nbf * rs * SRC;    // [nbf][SRC] N-0 column
+  double* sI = sN + nbf * SRC;         // [nbf][SRC] 1 / rating
+  double* sWc = sI + nbf * SRC;        // [RC][rs] the cases' W rows
+  double* cRel = sWc + RC * rs;        // [RC][KC] each case's running top-kc (multi-chunk)
+  double* cFlow = cRel + RC * kcl;
+  double* sIdn = cFlow + RC * kcl;     // [RC] 1 / den
+  double* sSc = sIdn + RC;             // [RC] N-0 flow of the outaged row
+  int* cPos = (int*)(sSc + RC);        // [RC][KC] (multi-chunk)
+  int* sC = cPos + RC * kcl;           // [RC] case index
+  int* sOwn = sC + RC;                 // [RC] monitored position of the outaged row
+  int* cN = sOwn + RC;                 // [RC] entries in the case's list
   __shared__ WarpList wl[RW];
   __shared__ double wmax[RW];
   __shared__ int sdeadp[RMAX];  // monitored positions of the disconnected rows (-1: unmonitored)
@@ -1459,9 +1466,10 @@ __global__ void k_probe(DevGrid g, Work w, double* n0o, double* n1o, uint8_t* ok
 }
 
 namespace {
-size_t rsweep_dyn_bytes(int rs, int kc, int src, int rcw) {
-  return (2 * (size_t)rs * src + 4 * (size_t)src + (size_t)rcw * rs + 2 * (size_t)rcw * kc + 2 * rcw) *
-             sizeof(double) + ((size_t)rcw * kc + 3 * rcw) * sizeof(int);
+size_t rsweep_dyn_bytes(int rs, int kc, int src, int rcw, int M) {
+  const size_t nbf = M <= src ? 1 : 2, kcl = M <= src ? 0 : kc;
+  return (nbf * rs * src + 2 * nbf * src + (size_t)rcw * rs + 2 * (size_t)rcw * kcl + 2 * rcw) * sizeof(double) +
+         ((size_t)rcw * kcl + 3 * rcw) * sizeof(int);
 }
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
@@ -1478,16 +1486,19 @@ void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStrea
     const char* cq_env = getenv("BDC_RSWEEP_CQ");
     const int cq = cq_env ? atoi(cq_env) : (g.M <= 2048 ? 1 : 4);
     const int rpl = cq == 1 && g.M <= 64 ? 2 : cq == 1 && g.M > 128 && g.M <= 192 ? 6 : 4;
-    const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl, w.rcw);
+    const size_t dyn = rsweep_dyn_bytes(w.rs, KC, 32 * rpl, w.rcw, g.M);
     const dim3 grid((g.N1 + w.rcw - 1) / w.rcw, w.Wb);
-    auto go = [&](auto kern) {
+    // one-chunk grids: 128-thread CTAs (test hook BDC_RSWEEP_NT=256 keeps 256)
+    const char* nt_env = getenv("BDC_RSWEEP_NT");
+    const bool small = g.M <= 32 * rpl && cq == 1 && !(nt_env && atoi(nt_env) == 256);
+    auto go = [&](auto kern, int nth) {
       smem_opt_in((const void*)kern, (int)dyn);
-      kern<<<grid, RT, dyn, s>>>(g, c, w);
+      kern<<<grid, nth, dyn, s>>>(g, c, w);
     };
-    if (cq != 1) go(k_rsweep<KC, 4, 4>);
-    else if (rpl == 2) go(k_rsweep<KC, 1, 2>);
-    else if (rpl == 6) go(k_rsweep<KC, 1, 6>);
-    else go(k_rsweep<KC, 1, 4>);
+    if (cq != 1) go(k_rsweep<KC, 4, 4, 256>, 256);
+    else if (rpl == 2) small ? go(k_rsweep<KC, 1, 2, 128>, 128) : go(k_rsweep<KC, 1, 2, 256>, 256);
+    else if (rpl == 6) small ? go(k_rsweep<KC, 1, 6, 128>, 128) : go(k_rsweep<KC, 1, 6, 256>, 256);
+    else small ? go(k_rsweep<KC, 1, 4, 128>, 128) : go(k_rsweep<KC, 1, 4, 256>, 256);
   }
   const long long threads = (long long)w.Wb * 32;
   k_rmerge<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, c, w);

@@ -284,6 +284,11 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     assert np.array_equal(warp.best, ras.best)
     assert np.array_equal(warp.metric, ras.metric, equal_nan=True)
     assert warp.n1_pairs == ras.n1_pairs
+    monkeypatch.setenv("BDC_RSWEEP_NT", "256")  # one-chunk sweep with 256- instead of 128-thread CTAs
+    nt = eng.solve(*args)
+    monkeypatch.delenv("BDC_RSWEEP_NT")
+    assert np.array_equal(warp.metric, nt.metric, equal_nan=True)
+    assert warp.reports() == nt.reports()
     monkeypatch.setenv("BDC_RSWEEP_WIDE", "1")  # 160-case sweep tiles (batches >= 1024 tasks)
     wide = eng.solve(*args)
     monkeypatch.delenv("BDC_RSWEEP_WIDE")
