@@ -471,7 +471,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_n1c = L.add(B * 4), o_n1k = L.add(B * KMAX * 4), o_n1p = L.add(B * KMAX * 4);
   size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
   size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)SB * g.N1 * 4);
-  size_t o_m0b = L.add(B * (size_t)SB * T * 4);
+  size_t o_m0b = L.add(B * (size_t)SB * T * 4), o_m0bx = L.add(B * (size_t)SB * 4);
   const size_t nitems = B * (size_t)((g.N1 + TOPC - 1) / TOPC) * (size_t)((T + top_tile_cands(T) - 1) / top_tile_cands(T));
   size_t o_ll = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_lc = L.add(B * 4);
   size_t o_q = L.add((nitems > 0 ? nitems : 1) * 8);
@@ -526,6 +526,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.top = (int*)(base + o_top); x.done = (uint8_t*)(base + o_done);
   x.ptop = TOPC;
   x.m0b = (float*)(base + o_m0b);
+  x.m0bx = (float*)(base + o_m0bx);
   x.llist = (int*)(base + o_ll); x.lcnt = (int*)(base + o_lc);
   x.queue = (int2*)(base + o_q);
   x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
@@ -765,6 +766,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m32, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0b, 0, (size_t)nb * SB * T * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(x.m0bx, 0, (size_t)nb * SB * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 8, st);  // k_pairs queue, re-score queue
     if (err == cudaSuccess) err = cudaMemsetAsync(x.lcnt, 0, (size_t)nb * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);

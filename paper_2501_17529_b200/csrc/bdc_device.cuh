@@ -129,6 +129,7 @@ struct Work {
   int2* queue;    // (Wb * ceil(N1/TOPC) * candidate tiles)  k_pairs items (task, group<<16 | tile)
   unsigned* qcount;  // items in the queue (device counter, reset per wave)
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
+  float* m0bx;    // (Wb, SB)      max_t m0b (k_n0; the screening key's N-0 term)
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
   float* scale;   // (Wb, SB, N1)  FP32 upper bound of max_{r in block} |LODF(r,c)|/rating_r
   float* B32;     // (Wb, b32_task_floats) FP32 B''/rating on monitored rows, 0 on dead rows,

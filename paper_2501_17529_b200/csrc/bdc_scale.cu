@@ -185,14 +185,10 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
     const int k = i / RMAX, d = i % RMAX;
     if (d < snd[k]) sdead[k][d] = g.row_mon_pos[w.dead[(size_t)(tb0 + k) * RMAX + d]];  // -1: unmonitored
   }
-  // max_t m0_b(t) of each task and block (ranking key)
-  for (int kb = wid; kb < TB * SB; kb += NT / 32) {
-    const int k = kb / SB, blk = kb % SB;
-    float v = 0.f;
-    if (srt[k] >= 0)
-      for (int t = lane; t < T; t += 32) v = fmaxf(v, w.m0b[((size_t)(tb0 + k) * SB + blk) * T + t]);
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sm0[k][blk] = v;
+  // max_t m0_b(t) of each task and block (ranking key; folded by k_n0)
+  if (tid < TB * SB) {
+    const int k = tid / SB, blk = tid % SB;
+    sm0[k][blk] = srt[k] >= 0 ? w.m0bx[(size_t)(tb0 + k) * SB + blk] : 0.f;
   }
   // A operands (warpgroup 0): W(c, j) of every task, TF32 (cvt.rna), zero past the rank
   if (wg == 0) {

@@ -676,25 +676,27 @@ __global__ void __launch_bounds__(NT) k_terms(DevGrid g, Work w) {
 // the reference's dgemm column (f0 + sum_j B''_j y_j), rounded once.
 constexpr int N0_ROWS = 128;
 
-template <int TPL>
+// ROWS emitted rows per CTA: 192 when every row fits one CTA (small grids: one CTA per
+// task instead of a full and a thin one), else 128.
+template <int TPL, int ROWS>
 __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   const int b = blockIdx.y;
   if (w.status[b] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // rows emitted: monitored positions, then (unless s is read from n0s) single cases
   const int R = g.R, T = w.T, M = g.M, N1 = g.N1, NL = g.s_mon ? M : M + N1, rs = w.rs, rt = w.rank[b];
-  const int r0 = blockIdx.x * N0_ROWS, nr = min(NL - r0, N0_ROWS);
+  const int r0 = blockIdx.x * ROWS, nr = min(NL - r0, ROWS);
   const double* Bm = w.Bm + (size_t)b * rs * R;
   const double* Y = w.Y + (size_t)b * rs * T;
   float* n0s = w.n0s + (size_t)b * M * T;
   float* s32 = w.s32 + (size_t)b * N1 * T;
   constexpr int TCH = 32 * TPL, RG = 4;
   extern __shared__ __align__(16) double n0sm[];
-  double* sB = n0sm;                       // [rt][N0_ROWS]  B'' on the CTA's rows
-  double* sY = sB + (size_t)rs * N0_ROWS;  // [rt][TCH]      y_t of the candidate chunk
-  __shared__ double sF0[N0_ROWS], sScl[N0_ROWS];
-  __shared__ int sLive[N0_ROWS];
-  __shared__ float sSmax[N0_ROWS];  // max_t |s(c,t)| of the CTA's single-case rows
+  double* sB = n0sm;                       // [rt][ROWS]  B'' on the CTA's rows
+  double* sY = sB + (size_t)rs * ROWS;  // [rt][TCH]      y_t of the candidate chunk
+  __shared__ double sF0[ROWS], sScl[ROWS];
+  __shared__ int sLive[ROWS];
+  __shared__ float sSmax[ROWS];  // max_t |s(c,t)| of the CTA's single-case rows
   __shared__ int sdead[RMAX];
   __shared__ unsigned tmax[TCH];
   __shared__ unsigned tmaxb[SB][TCH];  // per screening row block
@@ -703,7 +705,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   __syncthreads();
   // the CTA's emitted rows: monitored positions (n0 / rating) then single cases (n0[r_c])
-  for (int i = tid; i < N0_ROWS; i += NT) {
+  for (int i = tid; i < ROWS; i += NT) {
     const int li = r0 + i;
     int row = 0, live = 0;
     double scl = 1.0;
@@ -722,7 +724,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
     sLive[i] = live;
     for (int j = 0; j < rt; ++j) {
       const double bv = i < nr ? Bm[(size_t)j * R + row] : 0.0;
-      sB[j * N0_ROWS + i] = bv;
+      sB[j * ROWS + i] = bv;
       if (li < M) {
         // FP32 B'' on monitored rows and max_r |B''(r,j)|/rating_r for the scale bound
         w.B32[(size_t)b * b32_task_floats(rs, M) + b32_off(rs, li, j)] = live ? (float)(bv * scl) : 0.f;
@@ -753,7 +755,7 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
       for (int j = 0; j < rt; ++j) {
         double bv[RG], yv[TPL];
 #pragma unroll
-        for (int i = 0; i < RG; ++i) bv[i] = sB[j * N0_ROWS + i0 + i];
+        for (int i = 0; i < RG; ++i) bv[i] = sB[j * ROWS + i0 + i];
 #pragma unroll
         for (int k = 0; k < TPL; ++k) yv[k] = sY[j * TCH + lane + 32 * k];
 #pragma unroll
@@ -807,6 +809,14 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
       for (int blk = blo; blk <= bhi; ++blk)
         for (int i = tid; i < min(TCH, T - tc); i += NT)
           atomicMax(reinterpret_cast<unsigned*>(&w.m0b[((size_t)b * SB + blk) * T + tc + i]), tmaxb[blk][i]);
+      // and max_t m0_b(t), the screening key's N-0 term (k_scale_tc): one atomic per block
+      if (wid == 0)
+        for (int blk = blo; blk <= bhi; ++blk) {
+          unsigned v = 0u;
+          for (int i = lane; i < min(TCH, T - tc); i += 32) v = max(v, tmaxb[blk][i]);
+          v = __reduce_max_sync(0xffffffffu, v);
+          if (lane == 0 && v) atomicMax(reinterpret_cast<unsigned*>(&w.m0bx[(size_t)b * SB + blk]), v);
+        }
     }
     __syncthreads();
   }
@@ -896,8 +906,10 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
     k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
   }
   if (w.NTERM > 0 && g.M > 0) {
+    // >= 8 items per thread: small grids take one CTA per task (the per-CTA cost, not
+    // the items, dominated with several thin CTAs per task), large grids up to eight
     const int work = g.M + w.NTERM * w.T;
-    const dim3 grid((unsigned)std::min(8, (work + NT - 1) / NT), w.Wb);
+    const dim3 grid((unsigned)std::max(1, std::min(8, work / (8 * NT))), w.Wb);
     k_terms<<<grid, NT, 0, st>>>(g, w);
   }
 }
@@ -905,16 +917,23 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t st) {
   const int NL = g.s_mon ? g.M : g.M + g.N1;
   if (NL == 0) return;
-  const dim3 grid((NL + N0_ROWS - 1) / N0_ROWS, w.Wb);
+  const int rows = NL <= 192 ? 192 : N0_ROWS;
+  const dim3 grid((NL + rows - 1) / rows, w.Wb);
   const int tpl = w.T > 64 ? 4 : (w.T > 32 ? 2 : 1);
-  const size_t dyn = (size_t)w.rs * (N0_ROWS + 32 * tpl) * sizeof(double);
+  const size_t dyn = (size_t)w.rs * (rows + 32 * tpl) * sizeof(double);
   auto go = [&](auto kern) {
     smem_opt_in((const void*)kern, (int)dyn);
     kern<<<grid, NT, dyn, st>>>(g, w);
   };
-  if (tpl == 4) go(k_n0<4>);
-  else if (tpl == 2) go(k_n0<2>);
-  else go(k_n0<1>);
+  if (rows == 192) {
+    if (tpl == 4) go(k_n0<4, 192>);
+    else if (tpl == 2) go(k_n0<2, 192>);
+    else go(k_n0<1, 192>);
+  } else {
+    if (tpl == 4) go(k_n0<4, N0_ROWS>);
+    else if (tpl == 2) go(k_n0<2, N0_ROWS>);
+    else go(k_n0<1, N0_ROWS>);
+  }
 }
 
 // k_topk for small grids (N1 <= 32 KW): a warp per task, keys in registers, ptop rounds

@@ -8,7 +8,7 @@ TAG=$1
 OUT=gpurun_out; mkdir -p $OUT/tmp
 S=$OUT/summary_${TAG}.md; : > $S
 timeout 400 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for C in g118 g1k g3k g14 g10k; do
+for C in g118 g1k g3k g14 g10k g1k_c; do
   if [ $C = g118 ]; then timeout 900 python bench.py --config $C 2>&1 | tail -1 > $OUT/bench_${C}_${TAG}.json
   else timeout 900 python bench.py --config $C --no-cpu 2>&1 | tail -1 > $OUT/bench_${C}_${TAG}.json; fi
   python -c "
@@ -32,7 +32,7 @@ cap() {  # cap <kernel regex> <config>
   python profiles/summarize.py --source $R.ncu-rep >> $S 2>&1
 }
 for CFG in g118 g1k g3k; do
-  for K in "k_update" "k_terms" "k_n0" "k_scale_tc" "^k_top$" "k_live" "k_pairs" "k_other" "k_rsel" "k_rsweep"; do
+  for K in "k_update" "k_terms" "k_n0" "k_scale_tc" "^k_top$" "k_live" "k_pairs" "k_other" "k_rescore" "k_rsel" "k_rsweep"; do
     cap "$K" $CFG
   done
 done
