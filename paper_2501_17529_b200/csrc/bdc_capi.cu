@@ -472,6 +472,8 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_n1f = L.add(B * KMAX * 8), o_n1r = L.add(B * KMAX * 8);
   size_t o_m0 = L.add(B * T * 4), o_sc = L.add(B * (size_t)SB * g.N1 * 4);
   size_t o_m0b = L.add(B * (size_t)SB * T * 4), o_m0bx = L.add(B * (size_t)SB * 4);
+  const size_t nqa = (size_t)std::max(1, g.NM + g.NI);
+  size_t o_osk = L.add(B * nqa), o_ol = L.add(B * nqa * 4), o_oc = L.add(B * 4);
   const size_t nitems = B * (size_t)((g.N1 + TOPC - 1) / TOPC) * (size_t)((T + top_tile_cands(T) - 1) / top_tile_cands(T));
   size_t o_ll = L.add(B * (size_t)(g.N1 > 0 ? g.N1 : 1) * 4), o_lc = L.add(B * 4);
   size_t o_q = L.add((nitems > 0 ? nitems : 1) * 8);
@@ -527,6 +529,7 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.ptop = TOPC;
   x.m0b = (float*)(base + o_m0b);
   x.m0bx = (float*)(base + o_m0bx);
+  x.oskip = (uint8_t*)(base + o_osk); x.olist = (int*)(base + o_ol); x.ocnt = (int*)(base + o_oc);
   x.llist = (int*)(base + o_ll); x.lcnt = (int*)(base + o_lc);
   x.queue = (int2*)(base + o_q);
   x.B32 = (float*)(base + o_b32); x.bmax = (float*)(base + o_bmx); x.smax = (float*)(base + o_smx);
@@ -633,6 +636,7 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     w.rsel_cta = (rc && rc[0] == '1') ? 1 : 0;
   }
   w.ranked = (w.screen && g.N1 > w.ptop) ? 1 : 0;
+  w.oscr = other_screened(g, w) ? 1 : 0;
   CK(cudaMemsetAsync(w.lf, 0, 64, st));
 
   const int nwaves = (int)((B + Wb - 1) / Wb);
@@ -774,16 +778,25 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.B32, 0, (size_t)nb * b32_task_floats(rs, g.M) * 4, st);
     if (err != cudaSuccess) break;
     cudaEventRecord(E[1], st);
-    // stage_ms (bdc.h BDC_STAGE_*): 0 h2d, 1 update, 2 N-0, 3 multi/injection N-1,
-    // 4 screening scales (tcgen05), 5 top-k, 6 TOP tile, 7 screen + live cases,
-    // 8 select, 9 winner report, 10 d2h, 11 unused
+    // events in execution order; stage_ms (bdc.h BDC_STAGE_*: 0 h2d, 1 update, 2 N-0,
+    // 3 multi/injection N-1, 4 screening scales (tcgen05), 5 top-k, 6 TOP tile, 7 screen +
+    // live cases, 8 select, 9 winner report, 10 d2h) from kExecStage below.  The
+    // multi/injection cases run after the TOP tile so that their own dominance screen
+    // (k_oscreen) sees the TOP cases' maxima.
     launch_update(g, s->cfg, x, st);
     cudaEventRecord(E[2], st);
     launch_n0(g, x, st);
     cudaEventRecord(E[3], st);
-    launch_other(g, x, st);
-    cudaEventRecord(E[4], st);
-    launch_single(g, s->cfg, x, st, &E[4]);  // records E[5], E[6], E[7]
+    if (x.oscr) {
+      launch_single_top(g, s->cfg, x, st, &E[4]);  // records E[4], E[5], E[6]
+      launch_other(g, s->cfg, x, st);
+      cudaEventRecord(E[7], st);
+    } else {  // unscreened: the multi/injection stream first (the order measured faster)
+      launch_other(g, s->cfg, x, st);
+      cudaEventRecord(E[4], st);
+      launch_single_top(g, s->cfg, x, st, &E[5]);  // records E[5], E[6], E[7]
+    }
+    launch_single_screen(g, s->cfg, x, st);
     cudaEventRecord(E[8], st);
     launch_select(g, s->cfg, x, st);
     cudaEventRecord(E[9], st);
@@ -872,10 +885,14 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   if (err == cudaSuccess) {
     for (int wv = 0; wv < nwaves; ++wv) {
       cudaEvent_t* E = &ev[(size_t)wv * NE];
+      // interval k (E[k] -> E[k+1], execution order) belongs to stage kExecStage[k]
+      static constexpr int kScreened[BDC_STAGES] = {0, 1, 2, 4, 5, 6, 3, 7, 8, 9, 10, 11};
+      static constexpr int kInOrder[BDC_STAGES] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11};
+      const int* kExecStage = w.oscr ? kScreened : kInOrder;
       for (int k = 0; k < BDC_STAGES; ++k) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, E[k], E[k + 1]) == cudaSuccess) {
-          bt->stage_ms[k] += ms;
+          bt->stage_ms[kExecStage[k]] += ms;
         }
       }
     }

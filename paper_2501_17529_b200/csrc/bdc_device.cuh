@@ -130,6 +130,11 @@ struct Work {
   unsigned* qcount;  // items in the queue (device counter, reset per wave)
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0bx;    // (Wb, SB)      max_t m0b (k_n0; the screening key's N-0 term)
+  uint8_t* oskip; // (Wb, NQ)      multi/injection case skipped by k_oscreen (cmax holds a bound)
+  int* olist;     // (Wb, NQ)      the cases k_other evaluates, ascending
+  int* ocnt;      // (Wb)
+  int oscr;       // 1: k_oscreen runs (many cases over many candidates), else every case is
+                  //    evaluated (oskip / olist unused)
   float* m0;      // (Wb, T)       FP32 N-0 max |n0|/rating (dominance-screen bound)
   float* scale;   // (Wb, SB, N1)  FP32 upper bound of max_{r in block} |LODF(r,c)|/rating_r
   float* B32;     // (Wb, b32_task_floats) FP32 B''/rating on monitored rows, 0 on dead rows,
@@ -291,6 +296,11 @@ __device__ __forceinline__ float s_at(const DevGrid& g, const Work& w, int b, in
   if (g.s_mon) return w.n0s[((size_t)b * g.M + g.sc_pos[c]) * w.T + t] * g.sc_rat[c];
   return w.s32[((size_t)b * g.N1 + c) * w.T + t];
 }
+// Is the multi/injection case q's cmax the exact FP32 maximum (k_other evaluated it), or the
+// dominance bound k_oscreen left when it skipped the case?
+__device__ __forceinline__ bool other_exact(const DevGrid& g, const Work& w, int b, int q) {
+  return !w.oscr || !w.oskip[(size_t)b * (g.NM + g.NI) + q];
+}
 __device__ __forceinline__ float smax_at(const DevGrid& g, const Work& w, int b, int c) {
   if (g.s_mon) return w.rmax[(size_t)b * g.M + g.sc_pos[c]] * g.sc_rat[c];
   return w.smax[(size_t)b * g.N1 + c];
@@ -330,10 +340,15 @@ int smem_opt_in_max(const void* fn);
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
-void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s, cudaEvent_t* ev = nullptr);
+// the single-branch N-1 stage in two parts: scales, top-k and the TOP tile (records ev[0..2]),
+// then the exact screen's live cases (k_live, k_queue, k_pairs)
+void launch_single_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s, cudaEvent_t* ev = nullptr);
+void launch_single_screen(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_topk(const DevGrid& g, const Work& w, cudaStream_t s);
 void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s);
-void launch_other(const DevGrid& g, const Work& w, cudaStream_t s);
+void launch_other(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+bool other_screened(const DevGrid& g, const Work& w);  // does k_oscreen run (Work::oscr)?
+void launch_oexact(const DevGrid& g, const Work& w, cudaStream_t s);  // report prologue
 void launch_select(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_report(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
 void launch_rescore(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);

@@ -11,6 +11,8 @@
 // is fused into the update kernel (bdc_update.cu).
 #include "bdc_device.cuh"
 
+#include <cstdlib>
+
 namespace bdc {
 
 // ---------------------------------------------------------------------------- k_other
@@ -29,7 +31,7 @@ constexpr int OW = OT / 32;    // warps (row groups)
 constexpr int ORC = 64;        // monitored rows per chunk
 }  // namespace
 
-template <int MT, int QC, int TPT>
+template <int MT, int QC, int TPT, bool LIST>  // LIST: the cases k_oscreen left, else all
 __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
   constexpr int TT = 32 * TPT, LQ = QC * MT;  // candidates per CTA, Lo floats per row
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -45,11 +47,14 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
   const float* n0s = w.n0s + (size_t)b * M * T;
   const float* So = w.So + (size_t)b * NQ * MT * T;
   float* cm = w.cmax + (size_t)b * (g.N1 + NQ) * T;
+  // the cases k_oscreen left (ascending), or all of them
+  const int* ol = w.olist + (size_t)b * NQ;
+  const int nq = LIST ? w.ocnt[b] : NQ;
   const bool vecN = (T % 4) == 0;
   for (int i = tid; i < TT; i += OT) sMax[i] = 0.f;
 
-  for (int qb = 0; qb < NQ; qb += QC) {
-    const int nqb = min(QC, NQ - qb), LW = nqb * MT;  // cases / Lo floats of this batch
+  for (int qb = 0; qb < nq; qb += QC) {
+    const int nqb = min(QC, nq - qb), LW = nqb * MT;  // cases / Lo floats of this batch
     float sv[QC][MT][TPT], acc[QC][TPT];
 #pragma unroll
     for (int k = 0; k < QC; ++k) {
@@ -58,7 +63,7 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
 #pragma unroll
         for (int i = 0; i < TPT; ++i) {
           const int t = t0 + lane * TPT + i;
-          sv[k][j][i] = (k < nqb && t < T) ? So[((size_t)(qb + k) * MT + j) * T + t] : 0.f;
+          sv[k][j][i] = (k < nqb && t < T) ? So[((size_t)(LIST ? ol[qb + k] : qb + k) * MT + j) * T + t] : 0.f;
         }
 #pragma unroll
       for (int i = 0; i < TPT; ++i) acc[k][i] = 0.f;
@@ -82,7 +87,8 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
       for (int idx = tid; idx < ORC * (LW / 2); idx += OT) {
         const int rr = idx / (LW / 2), u = 2 * (idx % (LW / 2)), m = m0 + rr;
         const bool ok = m < M;
-        cp8(&sL[(buf * ORC + rr) * LQ + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
+        const int q = LIST ? ol[qb + u / MT] : qb + u / MT;
+        cp8(&sL[(buf * ORC + rr) * LQ + u], ok ? &Lo[((size_t)m * NQ + q) * MT + (u % MT)] : Lo, ok);
       }
       cp_commit();
     };
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(OT) k_other(DevGrid g, Work w) {
     }
     __syncthreads();
     for (int idx = tid; idx < nqb * TT; idx += OT) {
-      const int k = idx / TT, u = idx % TT, q = qb + k, t = t0 + u;
+      const int k = idx / TT, u = idx % TT, q = LIST ? ol[qb + k] : qb + k, t = t0 + u;
       const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
       const float v = ok ? __uint_as_float(sAcc[k][u]) : 0.f;
       if (t < T) {
@@ -167,7 +173,7 @@ namespace {
 constexpr int ORC_W = 32;      // monitored rows per chunk (k_other_w)
 }  // namespace
 
-template <int MT, int QW, int TPT>
+template <int MT, int QW, int TPT, bool LIST>
 __global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
   constexpr int TT = 32 * TPT, QB = OW * QW;  // candidates per CTA, cases per batch
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -182,21 +188,24 @@ __global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
   const float* n0s = w.n0s + (size_t)b * M * T;
   const float* So = w.So + (size_t)b * NQ * MT * T;
   float* cm = w.cmax + (size_t)b * (g.N1 + NQ) * T;
+  // the cases k_oscreen left (ascending), or all of them
+  const int* ol = w.olist + (size_t)b * NQ;
+  const int nq = LIST ? w.ocnt[b] : NQ;
   const bool vecN = (T % 4) == 0;
   for (int i = tid; i < TT; i += OT) sMax[i] = 0.f;
 
-  for (int qb = 0; qb < NQ; qb += QB) {
-    const int nqb = min(QB, NQ - qb), LW = nqb * MT;  // cases / Lo floats of this batch
+  for (int qb = 0; qb < nq; qb += QB) {
+    const int nqb = min(QB, nq - qb), LW = nqb * MT;  // cases / Lo floats of this batch
     float sv[QW][MT][TPT], acc[QW][TPT];
 #pragma unroll
     for (int k = 0; k < QW; ++k) {
-      const int q = qb + wid + OW * k;
+      const int qi = qb + wid + OW * k;
 #pragma unroll
       for (int j = 0; j < MT; ++j)
 #pragma unroll
         for (int i = 0; i < TPT; ++i) {
           const int t = t0 + lane * TPT + i;
-          sv[k][j][i] = (q < NQ && t < T) ? So[((size_t)q * MT + j) * T + t] : 0.f;
+          sv[k][j][i] = (qi < nq && t < T) ? So[((size_t)(LIST ? ol[qi] : qi) * MT + j) * T + t] : 0.f;
         }
 #pragma unroll
       for (int i = 0; i < TPT; ++i) acc[k][i] = 0.f;
@@ -219,7 +228,8 @@ __global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
       for (int idx = tid; idx < ORC_W * (LW / 2); idx += OT) {
         const int rr = idx / (LW / 2), u = 2 * (idx % (LW / 2)), m = m0 + rr;
         const bool ok = m < M;
-        cp8(&sL[(buf * ORC_W + rr) * QB * MT + u], ok ? &Lo[((size_t)m * NQ + qb) * MT + u] : Lo, ok);
+        const int q = LIST ? ol[qb + u / MT] : qb + u / MT;
+        cp8(&sL[(buf * ORC_W + rr) * QB * MT + u], ok ? &Lo[((size_t)m * NQ + q) * MT + (u % MT)] : Lo, ok);
       }
       cp_commit();
     };
@@ -265,8 +275,9 @@ __global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
     // per-(case, candidate) maxima (islanded multi cases contribute 0), candidate max
 #pragma unroll
     for (int k = 0; k < QW; ++k) {
-      const int q = qb + wid + OW * k;
-      if (q >= NQ) break;
+      const int qi = qb + wid + OW * k;
+      if (qi >= nq) break;
+      const int q = LIST ? ol[qi] : qi;
       const bool ok = q >= g.NM || w.mc_ok[(size_t)b * g.NM + q];
 #pragma unroll
       for (int i = 0; i < TPT; ++i) {
@@ -282,6 +293,134 @@ __global__ void __launch_bounds__(OT) k_other_w(DevGrid g, Work w) {
   __syncthreads();
   for (int u = tid; u < TT; u += OT)
     if (t0 + u < T) atomic_max_pos(&w.m32[(size_t)b * T + t0 + u], sMax[u]);
+}
+
+// -------------------------------------------------------------------------- k_oscreen
+// The exact dominance screen for the multi-branch and injection cases (the reference
+// evaluates every one, solver.py:608-622; skipping a dominated one leaves every metric
+// bit-identical).  Runs after the TOP tile, so lb(t) = m32(t) already holds the N-0 and
+// TOP-case maxima (and the islanding penalty floors it).  Per case q (a warp each):
+//   |F'(r, t)| = |n0'(r, t) + sum_j Lo(r, q, j) So(q, j, t)|
+//              <= m0(t) + sum_j max_r |Lo(r, q, j)| |So(q, j, t)|   (FFMA chain: x (1 + 1e-5))
+// and a case whose bound stays <= lb(t) for every candidate cannot raise a metric: it is
+// skipped (its bound goes to cmax as the report's / re-score's upper bound, oskip marks
+// it inexact).  Islanded multi cases (mc_ok = 0) contribute 0 and are skipped too.  The
+// remaining cases are listed, ascending, for k_other.
+__global__ void __launch_bounds__(256) k_oscreen(DevGrid g, DevCfg cfg, Work w) {
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int NQ = g.NM + g.NI, M = g.M, T = w.T, MT = g.MT;
+  if (w.status[b] != 0) {
+    if (tid == 0) w.ocnt[b] = 0;
+    return;
+  }
+  const float* Lo = w.Lo + (size_t)b * M * NQ * MT;
+  const float* So = w.So + (size_t)b * NQ * MT * T;
+  const float* m0 = w.m0 + (size_t)b * T;
+  const float* m32 = reinterpret_cast<const float*>(w.m32) + (size_t)b * T;
+  float* cm = w.cmax + (size_t)b * (g.N1 + NQ) * T;
+  const bool pen = w.nisl[b] > 0;
+  const float penf = (float)cfg.penalty;
+  for (int q = wid; q < NQ; q += 8) {
+    const bool dead = q < g.NM && !w.mc_ok[(size_t)b * g.NM + q];
+    bool skip = dead;
+    float lm[8];
+    if (!dead && w.screen) {
+      for (int j = 0; j < MT; ++j) {
+        float v = 0.f;
+        for (int r = lane; r < M; r += 32) v = fmaxf(v, fabsf(Lo[((size_t)r * NQ + q) * MT + j]));
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        lm[j] = v;
+      }
+      bool dom = true;
+      for (int t = lane; t < T; t += 32) {
+        float ub = m0[t];
+        for (int j = 0; j < MT; ++j) ub = fmaf(lm[j], fabsf(So[((size_t)q * MT + j) * T + t]), ub);
+        const float lb = pen ? fmaxf(m32[t], penf) : m32[t];
+        dom &= ub * (1.f + 1e-5f) <= lb;
+      }
+      skip = __all_sync(0xffffffffu, dom);
+      if (skip)  // the report's and the re-score's upper bound of the skipped pairs
+        for (int t = lane; t < T; t += 32) {
+          float ub = m0[t];
+          for (int j = 0; j < MT; ++j) ub = fmaf(lm[j], fabsf(So[((size_t)q * MT + j) * T + t]), ub);
+          cm[(size_t)(g.N1 + q) * T + t] = ub * (1.f + 1e-5f);
+        }
+    }
+    if (dead)
+      for (int t = lane; t < T; t += 32) cm[(size_t)(g.N1 + q) * T + t] = 0.f;
+    if (lane == 0) w.oskip[(size_t)b * NQ + q] = skip;
+  }
+  __syncthreads();  // the block's oskip writes are visible to warp 0
+  if (wid == 0) {  // the kept cases, ascending
+    int off = 0;
+    for (int q0 = 0; q0 < NQ; q0 += 32) {
+      const bool keep = q0 + lane < NQ && !w.oskip[(size_t)b * NQ + q0 + lane];
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) w.olist[(size_t)b * NQ + off + __popc(bal & ((1u << lane) - 1u))] = q0 + lane;
+      off += __popc(bal);
+    }
+    if (lane == 0) w.ocnt[b] = off;
+  }
+}
+
+// --------------------------------------------------------------------------- k_oexact
+// The winner's exact FP32 maximum of every feasible multi/injection case k_oscreen skipped:
+// the report's kg-th case value (k_rsel) is taken over exact maxima, so the skipped cases
+// get k_other's expression (n0' + sum_j Lo_j So_j by fmaf in j order, the scalar form of
+// its FFMA2) at the winning candidate and are marked exact again.
+__global__ void __launch_bounds__(256) k_oexact(DevGrid g, Work w) {
+  constexpr int QP = 64;  // skipped cases per pass
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  if (w.status[b] != 0) return;
+  const int NQ = g.NM + g.NI, M = g.M, T = w.T, MT = g.MT, t = (int)w.best[b];
+  const float* Lo = w.Lo + (size_t)b * M * NQ * MT;
+  const float* So = w.So + (size_t)b * NQ * MT * T;
+  const float* n0s = w.n0s + (size_t)b * M * T;
+  __shared__ int sq[QP];
+  __shared__ float ss[QP][8];
+  __shared__ unsigned smx[QP];
+  __shared__ int nsq;
+  for (int q0 = 0; q0 < NQ; q0 += QP) {
+    if (tid == 0) nsq = 0;
+    __syncthreads();
+    if (tid < QP && q0 + tid < NQ) {
+      const int q = q0 + tid;
+      if (w.oskip[(size_t)b * NQ + q] && (q >= g.NM || w.mc_ok[(size_t)b * g.NM + q])) {
+        const int k = atomicAdd(&nsq, 1);
+        sq[k] = q;
+        smx[k] = 0u;
+      }
+    }
+    __syncthreads();
+    const int n = nsq;
+    if (n == 0) continue;
+    for (int i = tid; i < n * MT; i += 256) ss[i / MT][i % MT] = So[((size_t)sq[i / MT] * MT + i % MT) * T + t];
+    __syncthreads();
+    // rows over the block: each row's n0 once for every skipped case; per-case maxima by
+    // warp reduction, one shared-memory atomic per warp and case
+    for (int r0 = 0; r0 < M; r0 += 256) {
+      const int r = r0 + tid;
+      const float nv = r < M ? n0s[(size_t)r * T + t] : 0.f;
+      for (int k = 0; k < n; ++k) {
+        float f = nv;
+        if (r < M)
+          for (int j = 0; j < MT; ++j) f = fmaf(Lo[((size_t)r * NQ + sq[k]) * MT + j], ss[k][j], f);
+        unsigned v = __float_as_uint(fabsf(f));
+        v = __reduce_max_sync(0xffffffffu, v);
+        if (lane == 0) atomicMax(&smx[k], v);
+      }
+    }
+    __syncthreads();
+    if (tid < n) {
+      w.cmax[((size_t)b * (g.N1 + NQ) + g.N1 + sq[tid]) * T + t] = __uint_as_float(smx[tid]);
+      w.oskip[(size_t)b * NQ + sq[tid]] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_oexact(const DevGrid& g, const Work& w, cudaStream_t s) {
+  if (w.oscr && g.NM + g.NI > 0 && g.M > 0) k_oexact<<<w.Wb, 256, 0, s>>>(g, w);
 }
 
 // --------------------------------------------------------------------------- k_select
@@ -342,9 +481,13 @@ template <int MT, int QC, int TPT>
 void launch_other_t(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int TT = 32 * TPT;
   const size_t dyn = (2 * (size_t)ORC * TT + 2 * (size_t)ORC * QC * MT) * sizeof(float);
-  smem_opt_in((const void*)k_other<MT, QC, TPT>, (int)dyn);
   dim3 grid((w.T + TT - 1) / TT, w.Wb);
-  k_other<MT, QC, TPT><<<grid, OT, dyn, s>>>(g, w);
+  auto go = [&](auto kern) {
+    smem_opt_in((const void*)kern, (int)dyn);
+    kern<<<grid, OT, dyn, s>>>(g, w);
+  };
+  if (w.oscr) go(k_other<MT, QC, TPT, true>);
+  else go(k_other<MT, QC, TPT, false>);
 }
 template <int MT, int QC>
 void launch_other_m(const DevGrid& g, const Work& w, cudaStream_t s) {
@@ -355,9 +498,13 @@ template <int MT, int QW, int TPT>
 void launch_other_w(const DevGrid& g, const Work& w, cudaStream_t s) {
   constexpr int TT = 32 * TPT;
   const size_t dyn = (2 * (size_t)ORC_W * TT + 2 * (size_t)ORC_W * OW * QW * MT) * sizeof(float);
-  smem_opt_in((const void*)k_other_w<MT, QW, TPT>, (int)dyn);
   dim3 grid((w.T + TT - 1) / TT, w.Wb);
-  k_other_w<MT, QW, TPT><<<grid, OT, dyn, s>>>(g, w);
+  auto go = [&](auto kern) {
+    smem_opt_in((const void*)kern, (int)dyn);
+    kern<<<grid, OT, dyn, s>>>(g, w);
+  };
+  if (w.oscr) go(k_other_w<MT, QW, TPT, true>);
+  else go(k_other_w<MT, QW, TPT, false>);
 }
 template <int MT, int QW>
 void launch_other_wm(const DevGrid& g, const Work& w, cudaStream_t s) {
@@ -365,9 +512,19 @@ void launch_other_wm(const DevGrid& g, const Work& w, cudaStream_t s) {
 }
 }  // namespace
 
-void launch_other(const DevGrid& g, const Work& w, cudaStream_t s) {
+// The multi/injection screen pays where the stream is long (many cases over many
+// candidates: G1k 4.98 -> 1.46 ms per step); on small grids its per-task pass costs more than
+// it skips (G118 +0.7 ms).  Tests force it either way (BDC_OSCREEN=0/1).
+bool other_screened(const DevGrid& g, const Work& w) {
+  const int nq = g.NM + g.NI;
+  const char* e = getenv("BDC_OSCREEN");
+  if (e) return w.screen && e[0] == '1';
+  return w.screen && nq > 8 && w.T > 64;
+}
+void launch_other(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   const int nq = g.NM + g.NI;
   if (nq == 0 || g.M == 0) return;
+  if (w.oscr) k_oscreen<<<w.Wb, 256, 0, s>>>(g, c, w);
   // every lane carries a batch of cases and the warps split the rows; many cases over
   // more than 64 candidates: a warp per case, one pass over n0 (measured faster there)
   if (nq > 8 && w.T > 64) {

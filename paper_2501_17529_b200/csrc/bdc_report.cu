@@ -348,7 +348,11 @@ __global__ void __launch_bounds__(RT, 3) k_rsel(DevGrid g, DevCfg cfg, Work w) {
   };
   // exact FP32 maximum (>= 0), or -1 with the dominance bound in `ub`
   auto case_value = [&](int ci, float& ub) -> float {
-    if (ci >= N1 || pair_evaluated(g, w, b, ci, best)) {
+    if (ci >= N1) {  // multi/injection: exact unless k_oscreen skipped it (cmax = bound)
+      ub = cm[(size_t)ci * T];
+      return other_exact(g, w, b, ci - N1) ? ub : -1.f;
+    }
+    if (pair_evaluated(g, w, b, ci, best)) {
       ub = cm[(size_t)ci * T];
       return ub;
     }
@@ -546,7 +550,10 @@ __global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w)
     else if (ci < N1 + g.NM) feas = w.mc_ok[(size_t)b * g.NM + (ci - N1)] != 0;
     else feas = true;
     if (!feas) continue;
-    if (ci >= N1 || pair_evaluated(g, w, b, ci, best)) {
+    if (ci >= N1) {  // multi/injection: exact unless k_oscreen skipped it (cmax = bound)
+      cub[k] = cm[(size_t)ci * T];
+      cv[k] = other_exact(g, w, b, ci - N1) ? cub[k] : -1.f;
+    } else if (pair_evaluated(g, w, b, ci, best)) {
       cv[k] = cm[(size_t)ci * T];
       cub[k] = cv[k];
     } else {
@@ -1474,6 +1481,7 @@ size_t rsweep_dyn_bytes(int rs, int kc, int src, int rcw, int M) {
 template <int KC>
 void launch_report_t(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
   const int nc = g.N1 + g.NM + g.NI;
+  launch_oexact(g, w, s);  // exact winner maxima of the screened-out multi/injection cases
   if (!w.rsel_cta && g.M <= 32 * 8 && nc <= 32 * 8)
     k_rsel_w<KC, 8><<<(w.Wb + RW - 1) / RW, RT, 0, s>>>(g, c, w);
   else if (!w.rsel_cta && g.M <= 32 * 16 && nc <= 32 * 16)
@@ -1543,7 +1551,7 @@ int kernels_per_wave(const DevGrid& g, const Work& w) {
   const bool single = g.N1 > 0 && g.M > 0;
   // update, N-0, select + FP64 re-score, report select + merge (+ single: the N-1 stage's
   // launches and the report sweep) (+ multi/injection: the correction terms and k_other)
-  return 6 + (single ? single_launches(g, w) + 1 : 0) + 2 * (g.NM + g.NI > 0 && g.M > 0);
+  return 6 + (single ? single_launches(g, w) + 1 : 0) + (2 + 2 * w.oscr) * (g.NM + g.NI > 0 && g.M > 0);
 }
 
 }  // namespace bdc

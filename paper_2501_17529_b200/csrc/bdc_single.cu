@@ -467,19 +467,23 @@ void launch_pairs(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t
 
 // ev (optional): ev[1], ev[2], ev[3] are recorded after the scales, the top-k and the
 // TOP tile (stage boundaries of bdc_solve's timing).
-void launch_single(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s, cudaEvent_t* ev) {
+void launch_single_top(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s, cudaEvent_t* ev) {
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
   if (g.N1 == 0 || g.M == 0) {
-    mark(1); mark(2); mark(3);
+    mark(0); mark(1); mark(2);
     return;
   }
   // per-case block scales and ranking key, then the TOP tile by key
   if (w.ranked) launch_scale(g, w, s);
-  mark(1);
+  mark(0);
   if (w.ranked) launch_topk(g, w, s);
-  mark(2);
+  mark(1);
   launch_top(g, c, w, s);
-  mark(3);
+  mark(2);
+}
+
+void launch_single_screen(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s) {
+  if (g.N1 == 0 || g.M == 0) return;
   if (g.N1 > w.ptop) {
     k_live<<<dim3((g.N1 + LC - 1) / LC, w.Wb), LC, 0, s>>>(g, c, w);
     k_queue<<<(w.Wb + 255) / 256, 256, 0, s>>>(g, w);

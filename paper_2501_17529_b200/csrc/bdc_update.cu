@@ -704,35 +704,41 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
   const int nd = w.ndead[b];
   if (tid < nd) sdead[tid] = w.dead[(size_t)b * RMAX + tid];
   __syncthreads();
-  // the CTA's emitted rows: monitored positions (n0 / rating) then single cases (n0[r_c])
-  for (int i = tid; i < ROWS; i += NT) {
-    const int li = r0 + i;
+  // the CTA's emitted rows: monitored positions (n0 / rating) then single cases (n0[r_c]);
+  // a thread per row (ROWS <= NT)
+  static_assert(ROWS <= NT, "one emitted row per thread");
+  {
+    const int i = tid, li = r0 + i;
     int row = 0, live = 0;
     double scl = 1.0;
-    if (li < M) {
-      row = g.mon_row[li];
-      scl = g.inv_rating[li];
-      live = !is_dead(sdead, nd, row);
-    } else if (li < NL) {
-      const int c = li - M;
-      row = g.sc_row[c];
-      live = w.sc_ok[(size_t)b * N1 + c] && !is_dead(sdead, nd, row);
+    if (i < ROWS) {
+      if (li < M) {
+        row = g.mon_row[li];
+        scl = g.inv_rating[li];
+        live = !is_dead(sdead, nd, row);
+      } else if (li < NL) {
+        const int c = li - M;
+        row = g.sc_row[c];
+        live = w.sc_ok[(size_t)b * N1 + c] && !is_dead(sdead, nd, row);
+      }
+      sF0[i] = live ? g.f0[row] : 0.0;
+      sScl[i] = scl;
+      sSmax[i] = 0.f;
+      sLive[i] = live;
     }
-    sF0[i] = live ? g.f0[row] : 0.0;
-    sScl[i] = scl;
-    sSmax[i] = 0.f;
-    sLive[i] = live;
     for (int j = 0; j < rt; ++j) {
       const double bv = i < nr ? Bm[(size_t)j * R + row] : 0.0;
-      sB[j * ROWS + i] = bv;
-      if (li < M) {
+      if (i < ROWS) sB[j * ROWS + i] = bv;
+      unsigned bm = 0u;
+      if (i < ROWS && li < M) {
         // FP32 B'' on monitored rows and max_r |B''(r,j)|/rating_r for the scale bound
         w.B32[(size_t)b * b32_task_floats(rs, M) + b32_off(rs, li, j)] = live ? (float)(bv * scl) : 0.f;
         w.Bmon[((size_t)b * rs + j) * M + li] = bv;
-        if (live)
-          atomicMax(reinterpret_cast<unsigned*>(&w.bmax[(size_t)b * rs + j]),
-                    __float_as_uint((float)(fabs(bv) * scl) * (1.f + 1e-6f)));
+        if (live) bm = __float_as_uint((float)(fabs(bv) * scl) * (1.f + 1e-6f));
       }
+      // one atomic per warp and rank term (same-address atomics from every row are slow)
+      bm = __reduce_max_sync(0xffffffffu, bm);
+      if (lane == 0 && bm) atomicMax(reinterpret_cast<unsigned*>(&w.bmax[(size_t)b * rs + j]), bm);
     }
   }
   for (int tc = 0; tc < T; tc += TCH) {

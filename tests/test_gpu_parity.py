@@ -284,6 +284,13 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     assert np.array_equal(warp.best, ras.best)
     assert np.array_equal(warp.metric, ras.metric, equal_nan=True)
     assert warp.n1_pairs == ras.n1_pairs
+    # the multi/injection dominance screen (k_oscreen + k_oexact) forced on
+    monkeypatch.setenv("BDC_OSCREEN", "1")
+    osc = eng.solve(*args)
+    monkeypatch.delenv("BDC_OSCREEN")
+    assert np.array_equal(warp.best, osc.best)
+    assert np.array_equal(warp.metric, osc.metric, equal_nan=True)
+    assert warp.reports() == osc.reports()
     monkeypatch.setenv("BDC_RSWEEP_NT", "256")  # one-chunk sweep with 256- instead of 128-thread CTAs
     nt = eng.solve(*args)
     monkeypatch.delenv("BDC_RSWEEP_NT")
