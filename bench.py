@@ -488,6 +488,7 @@ def run_ours(args):
     pairs_eval = 0
     report_cases = 0
     rescore = [0, 0, 0]
+    split_shared = 0
     lf_total = 0
     stage = [0.0] * len(STAGES)
     launches = 0
@@ -509,6 +510,7 @@ def run_ours(args):
         pairs_eval += eng.last_pairs
         report_cases += eng.last_report_cases
         rescore = [a + b for a, b in zip(rescore, eng.last_rescore)]
+        split_shared += eng.last_split_shared
     torch.cuda.synchronize()
     clk = clocks.stop()
     if ws > 1:
@@ -656,6 +658,12 @@ def run_ours(args):
         },
         "tasks": {"generated_on": "device (taskgen.random_tasks_device, bdc_draw_tasks)" if device_tasks else
                   "host (synth.random_task_arrays)", "generate_s": gen_s},
+        "split_chain": {
+            "applications_per_step": float(((np.asarray(splits).reshape(B, -1, splits.shape[-1]).any(axis=2)).sum())),
+            "shared_per_step": split_shared / args.steps,
+            "note": "split applications copied from another task of the wave with the same canonical prefix "
+            "(k_update prefix memo, levels < 2; tree.py:50-113) instead of computed",
+        },
         "gpu_launches": int(launches),
         "clocks": clk,
         "loadflows_per_step": lf_all / args.steps,

@@ -178,6 +178,9 @@ typedef struct {
                                 coefficients y_t) re-scored in FP64 (the winner's near-tie band,
                                 solver.py:804-823), [1] tasks whose FP32 argmin the FP64
                                 re-score replaced, [2] tasks with a band of > 1 */
+  int64_t* split_shared;     /* (1) optional: split applications copied from another task of
+                                the wave with the same split prefix (k_update's prefix memo,
+                                tree.py:50-113) instead of computed */
 } BdcBatch;
 
 int bdc_device_count(int* count);

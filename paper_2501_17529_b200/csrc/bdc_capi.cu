@@ -487,6 +487,17 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   size_t o_b32 = L.add(B * b32_task_floats(rs, g.M) * 4), o_bmx = L.add(B * (size_t)rs * 4);
   size_t o_smx = L.add(B * (size_t)g.N1 * 4);
   size_t o_lf = L.add(64), o_bs = L.add(16), o_rsq = L.add(B * 4);
+  // prefix memo of the split chain (k_update): up to PFX_LEVELS entries per task.  Opt-in
+  // (BDC_PREFIX=1): bit-identical and it shares 58 % of the split applications at G118, but
+  // the probe / wait / copy costs more than the split it saves (G118 update 2.92 -> 3.62 ms,
+  // G1k 3.44 -> 3.54 ms), so the flat chain is the default
+  const char* pe = std::getenv("BDC_PREFIX");
+  const bool pfx_on = pe && pe[0] == '1';
+  size_t pcap = 0;
+  if (pfx_on) { pcap = 1; while (pcap < (size_t)B * PFX_LEVELS) pcap <<= 1; }
+  const size_t pc1 = pcap > 0 ? pcap : 1;
+  size_t o_pk = L.add(pc1 * 8), o_pst = L.add(pc1 * 4), o_pfl = L.add(pc1 * 4), o_pid = L.add(pc1 * 2 * PFX_LEVELS * 4);
+  size_t o_pB = L.add(pcap * (size_t)g.R * 8), o_pC = L.add(pcap * (size_t)Cs * 8);
   if (!base) return L.total;
   Work& x = *w;
   x.Wb = Wb; x.T = T; x.D = D; x.Ein = Ein; x.rs = rs; x.Cs = Cs; x.NCw = NCw;
@@ -529,6 +540,10 @@ size_t carve(const DevGrid& g, int Wb, int T, int D, int Ein, int rs, char* base
   x.ptop = TOPC;
   x.m0b = (float*)(base + o_m0b);
   x.m0bx = (float*)(base + o_m0bx);
+  x.pfx_cap = (int)pcap;
+  x.pfx_key = (unsigned long long*)(base + o_pk); x.pfx_state = (int*)(base + o_pst);
+  x.pfx_fail = (int*)(base + o_pfl); x.pfx_id = (int*)(base + o_pid);
+  x.pfx_B = (double*)(base + o_pB); x.pfx_C = (double*)(base + o_pC);
   x.oskip = (uint8_t*)(base + o_osk); x.olist = (int*)(base + o_ol); x.ocnt = (int*)(base + o_oc);
   x.llist = (int*)(base + o_ll); x.lcnt = (int*)(base + o_lc);
   x.queue = (int2*)(base + o_q);
@@ -771,6 +786,10 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0, 0, (size_t)nb * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0b, 0, (size_t)nb * SB * T * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.m0bx, 0, (size_t)nb * SB * 4, st);
+    if (err == cudaSuccess && x.pfx_cap) {  // an empty prefix table per wave
+      err = cudaMemsetAsync(x.pfx_key, 0, (size_t)x.pfx_cap * 8, st);
+      if (err == cudaSuccess) err = cudaMemsetAsync(x.pfx_state, 0, (size_t)x.pfx_cap * 4, st);
+    }
     if (err == cudaSuccess) err = cudaMemsetAsync(x.qcount, 0, 8, st);  // k_pairs queue, re-score queue
     if (err == cudaSuccess) err = cudaMemsetAsync(x.lcnt, 0, (size_t)nb * 4, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(x.bmax, 0, (size_t)nb * rs * 4, st);
@@ -907,6 +926,9 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     bt->rescore_stats[0] = (int64_t)counters[4];
     bt->rescore_stats[1] = (int64_t)counters[5];
     bt->rescore_stats[2] = (int64_t)counters[6];
+  }
+  if (bt->split_shared) {
+    bt->split_shared[0] = (int64_t)counters[7];
   }
   bt->waves = nwaves;
   bt->kernel_launches = launches;

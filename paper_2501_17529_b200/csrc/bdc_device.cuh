@@ -16,6 +16,7 @@ constexpr int MMAX = BDC_MAX_MULTI;       // branches per multi-branch case
 constexpr int KMAX = BDC_MAX_TOPK;        // top-k limits
 constexpr int ACTMAX = 64;                // active slots (slots at split substations) per task
 constexpr int RHMAX = RMAX * EMAX;        // re-homed branch ends per task
+constexpr int PFX_LEVELS = 2;             // split-prefix levels shared through k_update's memo
 constexpr double ISL_TOL = 1e-8;          // ISLANDING_TOL == SPLIT_TOL (factors.py:48-49)
 // Absolute margin (in units of relative loading) on the FP32 screening values
 // used to decide which cases the FP64 winner report must revisit.  The FP32
@@ -130,6 +131,14 @@ struct Work {
   unsigned* qcount;  // items in the queue (device counter, reset per wave)
   float* m0b;     // (Wb, SB, T)   FP32 max |n0|/rating per screening row block
   float* m0bx;    // (Wb, SB)      max_t m0b (k_n0; the screening key's N-0 term)
+  // prefix-shared split chains (k_update): hash table of split prefixes, per wave
+  int pfx_cap;                    // slots (power of two), 0 = off
+  unsigned long long* pfx_key;    // (cap) prefix hash, 0 = empty
+  int* pfx_state;                 // (cap) 0 free, 1 claimed, 2 published
+  int* pfx_fail;                  // (cap) BDC_TASK_* of the split (0 ok)
+  int* pfx_id;                    // (cap, 2 PFX_LEVELS) the prefix (substation, bits) per level
+  double* pfx_B;                  // (cap, R)  B_j
+  double* pfx_C;                  // (cap, Cs) C_j over columns 0..C0+j
   uint8_t* oskip; // (Wb, NQ)      multi/injection case skipped by k_oscreen (cmax holds a bound)
   int* olist;     // (Wb, NQ)      the cases k_other evaluates, ascending
   int* ocnt;      // (Wb)

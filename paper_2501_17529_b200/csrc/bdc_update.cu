@@ -33,6 +33,7 @@ struct UpdShared {
   int sub[RMAX];
   unsigned bits[RMAX];
   int k, d, nd, fail, farg, nrh, nact;
+  int pmode, pslot;    // prefix memo of the current split (PFX_*) and its table slot
   int wcnt[UWMAX];
   int dead[RMAX];
   int orow[RMAX];      // outage rows in task order
@@ -98,6 +99,56 @@ __device__ void set_island(const Work& w, int b, int order) {
 }
 
 }  // namespace
+
+// ---- prefix-shared split chains (tree.py:50-113 on the device).  Split j's factors
+// (B_j over the rows, the coupler row C_j over columns 0..C0+j, and whether it is singular)
+// depend only on the canonical prefix (sub_0, bits_0, ..., sub_j, bits_j).  The first task
+// of a wave to reach a prefix claims its slot in a hash table, computes the split and
+// publishes it; every other task with the same prefix waits for it and copies, so each
+// shared tree edge is computed once per wave (levels < PFX_LEVELS, not the last split of a
+// task).  Copies are the producer's bits, so results do not depend on who computed.
+constexpr int PFX_OFF = 0, PFX_PUBLISH = 1, PFX_WAIT = 2;
+
+__device__ __forceinline__ unsigned long long pfx_hash(const UpdShared& s, int j) {
+  unsigned long long h = 0x9e3779b97f4a7c15ull ^ (unsigned long long)(j + 1);
+  for (int i = 0; i <= j; ++i) {
+    h ^= (unsigned long long)s.sub[i] * 0xbf58476d1ce4e5b9ull + s.bits[i];
+    h = (h ^ (h >> 31)) * 0x94d049bb133111ebull;
+  }
+  return h | 1ull;  // 0 marks an empty slot
+}
+
+// thread 0: find or claim the slot of prefix j (PFX_PUBLISH: ours to compute, PFX_WAIT:
+// someone else's, PFX_OFF: table full around the home slot -- compute locally)
+__device__ int pfx_lookup(const Work& w, const UpdShared& s, int j, int& slot) {
+  const unsigned long long h = pfx_hash(s, j);
+  const unsigned cap = (unsigned)w.pfx_cap;
+  unsigned sl = (unsigned)(h ^ (h >> 32)) & (cap - 1u);
+  for (int probe = 0; probe < 32; ++probe, sl = (sl + 1u) & (cap - 1u)) {
+    const unsigned long long key = atomicCAS(&w.pfx_key[sl], 0ull, h);
+    int* id = w.pfx_id + (size_t)sl * 2 * PFX_LEVELS;
+    if (key == 0ull) {  // claimed: record the prefix, then announce it
+      for (int i = 0; i <= j; ++i) { id[2 * i] = s.sub[i]; id[2 * i + 1] = (int)s.bits[i]; }
+      for (int i = j + 1; i < PFX_LEVELS; ++i) { id[2 * i] = -1; id[2 * i + 1] = 0; }
+      __threadfence();
+      atomicExch(&w.pfx_state[sl], 1);
+      slot = (int)sl;
+      return PFX_PUBLISH;
+    }
+    if (key != h) continue;
+    while (atomicAdd(&w.pfx_state[sl], 0) == 0) __nanosleep(64);  // the claimer writes id first
+    bool same = true;
+    for (int i = 0; i < PFX_LEVELS && same; ++i) {
+      const int vs = __ldcg(&id[2 * i]), vb = __ldcg(&id[2 * i + 1]);
+      same = i <= j ? (vs == s.sub[i] && vb == (int)s.bits[i]) : vs == -1;
+    }
+    if (same) {
+      slot = (int)sl;
+      return PFX_WAIT;
+    }
+  }
+  return PFX_OFF;
+}
 
 // UT threads per task: 128 for small grids (many tasks in flight), more for large grids,
 // whose row and column loops need the memory parallelism (few tasks per SM).
@@ -210,6 +261,36 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
     __syncthreads();
     if (s.fail) goto done;
     const int a = s.a, nm = s.nm, nst = s.nst;
+    if (tid == 0) {
+      s.pmode = PFX_OFF;
+      if (w.pfx_cap > 0 && j < PFX_LEVELS && j + 1 < k) s.pmode = pfx_lookup(w, s, j, s.pslot);
+    }
+    __syncthreads();
+    if (s.pmode == PFX_WAIT) {
+      // another task computed this prefix: copy its split (B_j, C_j[0..C0+j]) or failure
+      const int sl = s.pslot;
+      if (tid == 0) {
+        while (atomicAdd(&w.pfx_state[sl], 0) != 2) __nanosleep(128);
+        __threadfence();
+        const int f = __ldcg(&w.pfx_fail[sl]);
+        if (f) { s.fail = f; s.farg = j; }
+      }
+      __syncthreads();
+      if (s.fail) goto done;
+      for (int r = tid; r < R; r += UT) Bm[(size_t)j * R + r] = __ldcg(&w.pfx_B[(size_t)sl * R + r]);
+      for (int col = tid; col <= C0 + j; col += UT) Cm[(size_t)j * Cs + col] = __ldcg(&w.pfx_C[(size_t)sl * Cs + col]);
+      for (int i = tid; i < j; i += UT) Cm[(size_t)i * Cs + C0 + j] = Cm[(size_t)i * Cs + a];
+      if (tid == 0) {
+        for (int m = 0; m < nm; ++m) {
+          rh_key[s.nrh] = s.mrow[m] * 2 + s.mend[m];
+          rh_col[s.nrh] = C0 + j;
+          ++s.nrh;
+        }
+        atomicAdd(w.lf + 7, 1ull);  // split applications shared (copied)
+      }
+      __syncthreads();
+      continue;
+    }
     for (int idx = tid; idx < nm * j; idx += UT) {
       int m = idx / j, i = idx % j;
       MB(m, i) = Bm[(size_t)i * R + s.mrow[m]];
@@ -242,6 +323,11 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
       for (int st = 0; st < nst; ++st) den -= s.sw[st] * Cm[(size_t)j * Cs + s.sfar[st]];
       if (fabs(den) < ISL_TOL) { s.fail = BDC_TASK_SINGULAR_SPLIT; s.farg = j; }
       s.den = den;
+      if (s.pmode == PFX_PUBLISH && s.fail) {  // waiters learn the failure
+        w.pfx_fail[s.pslot] = s.fail;
+        __threadfence();
+        atomicExch(&w.pfx_state[s.pslot], 2);
+      }
     }
     for (int idx = tid; idx < (nst + 1) * j; idx += UT) {
       int st = idx / j, i = idx % j;
@@ -271,6 +357,18 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
         }
         for (int i = 0; i < j; ++i) num = fma(Bm[(size_t)i * R + r], s.coefB[i], num);
         Bm[(size_t)j * R + r] = num / den;
+      }
+    }
+    if (s.pmode == PFX_PUBLISH) {  // the split for every task sharing this prefix
+      const int sl = s.pslot;
+      for (int r = tid; r < R; r += UT) w.pfx_B[(size_t)sl * R + r] = Bm[(size_t)j * R + r];
+      for (int col = tid; col <= C0 + j; col += UT) w.pfx_C[(size_t)sl * Cs + col] = Cm[(size_t)j * Cs + col];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        w.pfx_fail[sl] = 0;
+        __threadfence();
+        atomicExch(&w.pfx_state[sl], 2);
       }
     }
     if (tid == 0) {

@@ -111,6 +111,7 @@ class _Batch(ctypes.Structure):
         ("waves", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
         ("rescore_stats", _P),
+        ("split_shared", _P),
     ]
 
 
@@ -436,6 +437,8 @@ class Engine:
         bt.report_cases = _ptr(rcases)
         rstats = np.zeros(3, dtype=np.int64)
         bt.rescore_stats = _ptr(rstats)
+        sshared = np.zeros(1, dtype=np.int64)
+        bt.split_shared = _ptr(sshared)
         bt.screen = int(self.screen)
         rc = self.lib.bdc_solve(self.handle, ctypes.byref(bt))
         if rc != 0:
@@ -443,6 +446,7 @@ class Engine:
         self.last_pairs = int(pairs[0])
         self.last_report_cases = int(rcases[0])
         self.last_rescore = [int(x) for x in rstats]
+        self.last_split_shared = int(sshared[0])
         return [float(x) for x in bt.stage_ms], int(bt.waves), int(bt.kernel_launches), int(lf[0])
 
     def probe_flows(self, splits_row: np.ndarray, discos_row: np.ndarray, inj_rows: np.ndarray):
@@ -530,6 +534,7 @@ class BatchOutput:
         # [0] y-classes re-scored in FP64, [1] winners the re-score replaced,
         # [2] tasks with more than one candidate in the near-tie band
         self.rescore_stats = np.zeros(3, dtype=np.int64)
+        self.split_shared = np.zeros(1, dtype=np.int64)  # split applications copied (prefix memo)
         self.stage_ms = [0.0] * N_STAGES
         self.waves = 0
         self.kernel_launches = 0
@@ -546,6 +551,7 @@ class BatchOutput:
         bt.bsdf_applications = _ptr(self._bsdf)
         bt.n1_pairs = _ptr(self._pairs)
         bt.rescore_stats = _ptr(self.rescore_stats)
+        bt.split_shared = _ptr(self.split_shared)
         bt.screen = int(self.engine.screen)
 
     def finish(self, bt: _Batch) -> None:

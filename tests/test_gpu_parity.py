@@ -284,6 +284,13 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     assert np.array_equal(warp.best, ras.best)
     assert np.array_equal(warp.metric, ras.metric, equal_nan=True)
     assert warp.n1_pairs == ras.n1_pairs
+    # prefix-shared split chains (k_update's memo) forced on: copied splits, same bits
+    monkeypatch.setenv("BDC_PREFIX", "1")
+    pfx = eng.solve(*args)
+    monkeypatch.delenv("BDC_PREFIX")
+    assert np.array_equal(warp.best, pfx.best)
+    assert np.array_equal(warp.metric, pfx.metric, equal_nan=True)
+    assert warp.reports() == pfx.reports()
     # the multi/injection dominance screen (k_oscreen + k_oexact) forced on
     monkeypatch.setenv("BDC_OSCREEN", "1")
     osc = eng.solve(*args)
