@@ -358,9 +358,19 @@ int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, 
       const uint8_t* sp = splits + (size_t)b * S * E;
       for (int si = 0; si < S; ++si) {
         const uint8_t* e = sp + (size_t)si * E;
-        bool any = false;
-        for (int j = 0; j < E; ++j) any |= e[j] != 0;
-        if (any) { ++k; act += s->slots_per_sub[si]; }
+        uint64_t acc = 0;  // any nonzero byte, eight at a time
+        int j = 0;
+        for (; j + 8 <= E; j += 8) {
+          uint64_t v;
+          std::memcpy(&v, e + j, 8);
+          acc |= v;
+        }
+        if (j < E) {
+          uint64_t v = 0;
+          std::memcpy(&v, e + j, (size_t)(E - j));
+          acc |= v;
+        }
+        if (acc) { ++k; act += s->slots_per_sub[si]; }
       }
       for (int i = 0; i < D; ++i) d += discos[(size_t)b * D + i] >= 0;
       mr = std::max(mr, k + d);
@@ -370,7 +380,7 @@ int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, 
     out[0] = mr; out[1] = md; out[2] = ma;
   };
   const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(hw, B / 8192));
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(hw, B / 2048));
   std::vector<int32_t> res((size_t)nt * 3, 0);
   std::vector<std::thread> th;
   const int64_t per = (B + nt - 1) / nt;

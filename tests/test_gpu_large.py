@@ -27,6 +27,8 @@ pytestmark = pytest.mark.gpu
 
 with open(golden_path("manifest_large.json")) as _fh:
     LARGE = json.load(_fh)["cases"]
+with open(golden_path("manifest_edges.json")) as _fh:
+    LARGE += json.load(_fh)["cases"]  # edge cases: ragged / 8 outages / duplicates / T=1 / top-k 32
 
 
 def _grid_source(case):
@@ -253,3 +255,17 @@ def test_folded_endpoint_disconnection_raises():
     seq = session_open(grid, replace(sess.config, multi_outage_method="sequential"))
     with pytest.raises(ValidationError, match="endpoint column folded, cannot outage"):
         solve_batch(seq, splits, discos, inj)
+
+
+def test_empty_batch():
+    """B = 0 returns empty arrays and an empty report list, as the reference's session does."""
+    from paper_2501_17529_b200.session import session_open, solve_batch
+
+    sess = session_open(golden_path("grids", "fixture_b.json"))
+    S, E = sess.split_shape
+    out = solve_batch(sess, np.zeros((0, S, E), bool), np.zeros((0, 0), np.int64),
+                      np.zeros((0, 3, sess.n_slots), bool))
+    assert out["metrics"].shape == (0,) and out["metrics"].dtype == np.float64
+    assert out["best_injection"].shape == (0,) and out["best_injection"].dtype == np.int64
+    assert out["feasible"].shape == (0,) and out["feasible"].dtype == bool
+    assert out["reports"] == []

@@ -20,13 +20,15 @@ from paper_2501_17529_b200.ptdf import prepare_base_ptdf
 from paper_2501_17529_b200.solver import SolveConfig
 
 CASES = load_manifest()
+with open(golden_path("manifest_edges.json")) as _fh:
+    EDGES = json.load(_fh)["cases"]  # reference-run edge cases (make_edge_golden.py)
 
 
 def _grid(case):
     return bio.load_grid(golden_path("grids", case["grid"]))
 
 
-@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+@pytest.mark.parametrize("case", CASES + EDGES, ids=[c["name"] for c in CASES + EDGES])
 def test_port_reproduces_reference_documents(case):
     grid = _grid(case)
     base = prepare_base_ptdf(grid)
