@@ -20,6 +20,7 @@
 #include "bdc_device.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace bdc {
 
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
 
   if (tid == 0) {
     s.k = 0; s.d = 0; s.nd = 0; s.fail = 0; s.farg = 0; s.nrh = 0; s.nact = 0; s.nisl = 0;
+    s.pmode = PFX_OFF;
   }
   for (int i = tid; i < w.NCw; i += UT) w.isl[(size_t)b * w.NCw + i] = 0u;
   __syncthreads();
@@ -261,11 +263,13 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
     __syncthreads();
     if (s.fail) goto done;
     const int a = s.a, nm = s.nm, nst = s.nst;
-    if (tid == 0) {
-      s.pmode = PFX_OFF;
-      if (w.pfx_cap > 0 && j < PFX_LEVELS && j + 1 < k) s.pmode = pfx_lookup(w, s, j, s.pslot);
+    if (w.pfx_cap > 0) {  // uniform: no extra barrier on the default (flat) chain
+      if (tid == 0) {
+        s.pmode = PFX_OFF;
+        if (j < PFX_LEVELS && j + 1 < k) s.pmode = pfx_lookup(w, s, j, s.pslot);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (s.pmode == PFX_WAIT) {
       // another task computed this prefix: copy its split (B_j, C_j[0..C0+j]) or failure
       const int sl = s.pslot;
