@@ -14,6 +14,12 @@ for C in g118 g1k g3k g14 g10k g1k_c; do
   python -c "
 import json; d=json.load(open('$OUT/bench_${C}_${TAG}.json')); print('$C', '%.3e'%d['value'], 'e2e %.3e'%d['e2e']['value'], round(d['ms_per_step'],2), d['roofline']['kernel'][:20], round(d['roofline']['frac'],4), d.get('cpu_baseline',{}).get('value'))"
 done
+# brute force (every (case, candidate) pair; BASELINE.md 3 / VERDICT r1 item 3)
+for C in g118 g1k; do
+  timeout 900 python bench.py --config $C --no-cpu --no-screen --check 8 2>&1 | tail -1 > $OUT/bench_${C}_noscreen_${TAG}.json
+  python -c "
+import json; d=json.load(open('$OUT/bench_${C}_noscreen_${TAG}.json')); print('$C no-screen', '%.3e'%d['value'], round(d['ms_per_step'],2))"
+done
 declare -A TASKS=([g14]=1024 [g118]=16384 [g1k]=2048 [g3k]=512)
 for CFG in g14 g118 g1k g3k; do
   N=${TASKS[$CFG]}
@@ -32,7 +38,7 @@ cap() {  # cap <kernel regex> <config>
   python profiles/summarize.py --source $R.ncu-rep >> $S 2>&1
 }
 for CFG in g118 g1k g3k; do
-  for K in "k_update" "k_terms" "k_n0" "k_scale_tc" "^k_top$" "k_live" "k_pairs" "k_other" "k_rescore" "k_rsel" "k_rsweep"; do
+  for K in "k_update" "k_terms" "k_n0" "k_scale_tc" "^k_top$" "k_live" "k_pairs" "k_oscreen" "k_other" "k_rescore" "k_oexact" "k_rsel" "k_rsweep"; do
     cap "$K" $CFG
   done
 done
