@@ -1285,8 +1285,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 12 : 3) k_rescore(DevGrid g, De
             if (h < RHOT) { sHotC[h] = -1; sHotP[h] = p; }
           }
         }
-        // single cases, a warp each
-        for (int kk = wid; kk < sNRel2; kk += NW) {
+        // single cases: (case, row) pairs over the whole CTA (few cases, long rows on
+        // large grids; many cases, short rows on small ones)
+        const int nr2 = sNRel2;
+        for (int e = tid; e < nr2 * M; e += NT) {
+          const int kk = e / M, p = e - kk * M;
           const int c = sRel2[kk];
           const int rowc = g.sc_row[c], ownp = g.row_mon_pos[rowc];
           const double idn = 1.0 / w.den[(size_t)b * N1 + c];
@@ -1294,7 +1297,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 12 : 3) k_rescore(DevGrid g, De
           if (!is_dead(sdead, nd, rowc))
             for (int j = 0; j < rt; ++j) ms = fma(fabs(Bm[(size_t)j * g.R + rowc]), dy[j], ms);
           const double* Wc = w.Wsc + ((size_t)b * N1 + c) * rs;
-          for (int p = lane; p < M; p += 32) {
+          {
             if (is_dead(sdeadp, nd, p) || p == ownp) continue;  // the own row's flow is exactly 0
             double mv = 0.0, dv = g.DM64[(size_t)c * M + p];
             for (int j = 0; j < rt; ++j) {
