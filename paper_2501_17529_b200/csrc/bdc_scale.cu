@@ -384,8 +384,9 @@ void launch_scale_tc_t(const DevGrid& g, const Work& w, cudaStream_t s) {
 }  // namespace
 
 void launch_scale(const DevGrid& g, const Work& w, cudaStream_t s) {
-  // four tasks per CTA, two CTAs per SM (eight tasks per CTA -- one CTA per SM for its 512
-  // TMEM columns -- measured 2.44 -> 4.22 ms at G118)
+  // four tasks per CTA, two CTAs per SM.  Measured and not kept: eight tasks per CTA (one
+  // CTA per SM for its 512 TMEM columns; G118 2.44 -> 4.22 ms) and two (four CTAs per SM,
+  // each D' tile shared by half as many tasks; G118 2.64, G1k 3.69 -> 4.63, G3k 3.37 -> 4.31 ms)
   if (w.rs <= 8) launch_scale_tc_t<4, 1>(g, w, s);
   else if (w.rs <= 16) launch_scale_tc_t<2, 2>(g, w, s);
   else launch_scale_tc_t<1, 4>(g, w, s);
