@@ -110,6 +110,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def ready(self, timeout: float = 3.0) -> None:
+        """Wait until nvidia-smi streams (its start-up takes a while), then drop what came
+        before, so the samples cover the timed region."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.lines.clear()
+
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -484,6 +492,7 @@ def run_ours(args):
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.ready()
     elapsed_ms = 0.0
     pairs_eval = 0
     report_cases = 0
