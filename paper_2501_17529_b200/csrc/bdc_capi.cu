@@ -733,8 +733,8 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
       rel(bt->n0_rel, O.n0pos, O.n0flow);
       rel(bt->n1_rel, O.n1pos, O.n1flow);
     };
-    const unsigned hw = std::max(1u, std::min(4u, std::thread::hardware_concurrency()));
-    const size_t nt = std::max<size_t>(1, std::min<size_t>(hw, nb / 4096));
+    const unsigned hw = std::max(1u, std::min(12u, std::thread::hardware_concurrency()));
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(hw, nb / 2048));
     const size_t per = (nb + nt - 1) / nt;
     std::vector<std::thread> th;
     for (size_t i = 1; i < nt; ++i) th.emplace_back(part, i * per, std::min(nb, (i + 1) * per));
