@@ -141,6 +141,40 @@ def solve_sharded(
     return solve_shard(splits[a:b], discos[a:b], inj[a:b], B, solver, group=group, device=device)
 
 
+def global_topk(metric, k: int, offset: int, group=None):
+    """The k best topologies of the whole sharded batch (optional): each rank
+    takes its shard's k smallest metrics (infeasible tasks, NaN, last), all-gathers the
+    (metric, global task index) pairs and merges them -- ascending metric, lower task index
+    first on ties, the reference's task order.  ``metric`` is this rank's (B,) tensor (CUDA
+    with NCCL, CPU with gloo), ``offset`` the global index of its first task.  Returns the
+    (k,) metrics and (k,) int64 task indices on every rank (fewer if the batch is smaller)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = metric.device
+    m = torch.nan_to_num(metric.to(torch.float64), nan=float("inf"))
+    idx = torch.arange(m.numel(), device=dev, dtype=torch.int64) + int(offset)
+    kk = min(int(k), m.numel())
+    # (metric, index) lexicographic: a stable sort by metric keeps the lower index first
+    order = torch.sort(m, stable=True).indices[:kk]
+    loc_m = torch.full((int(k),), float("inf"), dtype=torch.float64, device=dev)
+    loc_i = torch.full((int(k),), -1, dtype=torch.int64, device=dev)
+    loc_m[:kk] = m[order]
+    loc_i[:kk] = idx[order]
+    all_m = torch.empty((world * int(k),), dtype=torch.float64, device=dev)
+    all_i = torch.empty((world * int(k),), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(all_m, loc_m, group=group)
+    dist.all_gather_into_tensor(all_i, loc_i, group=group)
+    valid = all_i >= 0
+    all_m, all_i = all_m[valid], all_i[valid]
+    # ascending metric, then ascending global index
+    o1 = torch.sort(all_i, stable=True).indices
+    o2 = torch.sort(all_m[o1], stable=True).indices
+    sel = o1[o2][: int(k)]
+    return all_m[sel], all_i[sel]
+
+
 def engine_solver(session) -> Callable:
     """Adapter: the session's GPU engine as a ``solve_sharded`` solver."""
 

@@ -77,6 +77,14 @@ def _worker(rank, port, out_path):
     g = all_gather_device(loc)
     assert g["metric"].tolist() == [0.0] * 3 + [1.0] * 3
     assert g["n1_case"][3:].tolist() == (torch.arange(6, dtype=torch.int32).reshape(3, 2) + 100).tolist()
+    # optional global top-k topologies: shards of a known metric vector
+    from paper_2501_17529_b200.parallel import global_topk
+
+    full_metric = torch.tensor([3.0, float("nan"), 1.0, 2.0, 1.0, 0.5, float("nan"), 2.0, 0.5, 4.0], dtype=torch.float64)
+    a, b = (0, 5) if rank == 0 else (5, 10)
+    tm, ti = global_topk(full_metric[a:b], 4, a)
+    assert ti.tolist() == [5, 8, 2, 4], ti.tolist()
+    assert tm.tolist() == [0.5, 0.5, 1.0, 1.0]
     if rank == 0:
         np.savez(out_path, **{k: v for k, v in full.items() if k != "loadflows"}, loadflows=full["loadflows"])
     dist.barrier()
