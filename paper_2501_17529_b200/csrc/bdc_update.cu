@@ -50,7 +50,6 @@ struct UpdShared {
   double coefC[RMAX];        // sum_m sign_m B_i[row_m]            (coupler row of split j)
   double coefB[RMAX];        // sum_st w_st (C_i[far_st] - C_i[a]) (numerator of split j)
   double inner[MMAX * MMAX];
-  double mA[UWMAX][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
   double inv[MMAX * MMAX];   // MODF inverse (d <= MMAX outages)
   double ybase[RMAX];
   int act_slot[ACTMAX], act_ca[ACTMAX], act_cb[ACTMAX];
@@ -157,6 +156,7 @@ template <int UT, int MINB>
 __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work w) {
   constexpr int UW = UT / 32;
   __shared__ UpdShared s;
+  __shared__ double mA[UW][MMAX * MMAX];  // per-warp m x m inner system of a multi-branch case
   const int b = blockIdx.x, tid = threadIdx.x;
   const int R = g.R, C0 = g.C0, rs = w.rs, Cs = w.Cs;
   const int E = g.E > 0 ? g.E : 1, E2 = E > 2 ? E : 2;
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(UT, MINB) k_update(DevGrid g, DevCfg cfg, Work
         w.Wm[((size_t)b * g.NMB + st + i) * rs + j] = Cm[(size_t)j * Cs + fc] - Cm[(size_t)j * Cs + tc];
       }
       __syncwarp();
-      double* A = s.mA[wid];
+      double* A = mA[wid];
       for (int idx = lane; idx < m * m; idx += 32) {
         const int aa = idx / m, bb = idx % m;
         const int ra = g.mb_row[st + aa];
@@ -1009,9 +1009,13 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
   } else if (g.R > 512) {
     smem_opt_in((const void*)k_update<256, 4>, (int)dyn);
     k_update<256, 4><<<w.Wb, 256, dyn, st>>>(g, c, w);
-  } else {
+  } else if (g.R > 256 || (getenv("BDC_UPDATE_NT") && atoi(getenv("BDC_UPDATE_NT")) == 128)) {
     smem_opt_in((const void*)k_update<128, 8>, (int)dyn);
     k_update<128, 8><<<w.Wb, 128, dyn, st>>>(g, c, w);
+  } else {
+    // small grids: a warp per task -- no cross-warp barrier waits on the serial split setup
+    smem_opt_in((const void*)k_update<32, 32>, (int)dyn);
+    k_update<32, 32><<<w.Wb, 32, dyn, st>>>(g, c, w);
   }
   if (w.NTERM > 0 && g.M > 0) {
     // >= 8 items per thread: small grids take one CTA per task (the per-CTA cost, not
