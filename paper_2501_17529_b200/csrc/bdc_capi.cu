@@ -358,18 +358,8 @@ int bdc_scan_tasks(BdcSession* s, const uint8_t* splits, const int64_t* discos, 
       const uint8_t* sp = splits + (size_t)b * S * E;
       for (int si = 0; si < S; ++si) {
         const uint8_t* e = sp + (size_t)si * E;
-        uint64_t acc = 0;  // any nonzero byte, eight at a time
-        int j = 0;
-        for (; j + 8 <= E; j += 8) {
-          uint64_t v;
-          std::memcpy(&v, e + j, 8);
-          acc |= v;
-        }
-        if (j < E) {
-          uint64_t v = 0;
-          std::memcpy(&v, e + j, (size_t)(E - j));
-          acc |= v;
-        }
+        unsigned acc = 0;
+        for (int j = 0; j < E; ++j) acc |= e[j];
         if (acc) { ++k; act += s->slots_per_sub[si]; }
       }
       for (int i = 0; i < D; ++i) d += discos[(size_t)b * D + i] >= 0;
