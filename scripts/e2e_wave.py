@@ -2,10 +2,11 @@ import sys, time, numpy as np, torch
 sys.path.insert(0, ".")
 import bench
 from paper_2501_17529_b200.session import session_open, solve_batch_output
-grid, s, d, i = bench.make_workload("g118", 0)
+cfg = sys.argv[1] if len(sys.argv) > 1 else "g118"
+grid, s, d, i = bench.make_workload(cfg, 0)
 sess = session_open(grid)
 ps = torch.from_numpy(s).pin_memory().numpy(); pd = torch.from_numpy(d).pin_memory().numpy(); pi = torch.from_numpy(i).pin_memory().numpy()
-for cap in (0, 16384, 8192, 0):
+for cap in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "16384", "8192", "0"])]:
     sess.engine.set_wave(cap)
     solve_batch_output(sess, ps, pd, pi)
     ts = []
