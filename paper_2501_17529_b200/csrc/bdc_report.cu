@@ -31,6 +31,10 @@ __device__ __forceinline__ bool better3(double r1, int c1, int p1, double r2, in
   return r1 > r2 || (r1 == r2 && (c1 < c2 || (c1 == c2 && p1 < p2)));
 }
 
+// max of two loadings (>= 0): one compare and select, where fmax also handles NaN operands
+// (the running value never is one; a NaN loading is dropped by both)
+__device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
+
 template <int KC>
 struct LaneTop {
   double rel[KC], flow[KC];
@@ -265,7 +269,7 @@ __device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q,
       int own;
       const double f = multi_flow(g, w, b, st, m, row, n0b[row], sv, sMinv, Bm, rt, own);
       const double rel = fabs(f) * g.inv_rating[p];
-      mymax = fmax(mymax, rel);
+      mymax = dmax(mymax, rel);
       if (own < 0 && rel >= thresh) lt.insert(rel, p, f);
     }
   } else {
@@ -279,7 +283,7 @@ __device__ void other_case_report(const DevGrid& g, const Work& w, int b, int q,
       if (is_dead(sdead, nd, row)) continue;
       const double f = inj_flow(g, ca, coef, sp, row, n0b[row], Bm, rt);
       const double rel = fabs(f) * g.inv_rating[p];
-      mymax = fmax(mymax, rel);
+      mymax = dmax(mymax, rel);
       if (rel >= thresh) lt.insert(rel, p, f);
     }
   }
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(RT, 3) k_rsel(DevGrid g, DevCfg cfg, Work w) {
     return -1.f;
   };
   double mymax = 0.0;
-  for (int p = tid; p < M; p += RT) mymax = fmax(mymax, fabs(n0b[g.mon_row[p]]) * g.inv_rating[p]);
+  for (int p = tid; p < M; p += RT) mymax = dmax(mymax, fabs(n0b[g.mon_row[p]]) * g.inv_rating[p]);
   {
     const int n = warp_topk(M, kg, [&](int p) -> double {
       const int row = g.mon_row[p];
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(RT, 3) k_rsel_w(DevGrid g, DevCfg cfg, Work w)
     nv[k] = -1.0;
     if (p < M) {
       const double v = fabs(n0m[p]) * g.inv_rating[p];
-      mymax = fmax(mymax, v);
+      mymax = dmax(mymax, v);
       if (!is_dead(sdead[wid], nd, g.mon_row[p])) nv[k] = v;
     }
   }
@@ -728,6 +732,8 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? 8 : (CQ == 1 ? 4 : 3)) k_rsw
       if (p >= M || is_dead(sdeadp, nd, p)) skip |= 1u << u;
     }
     const double* cB = sB + bf * rs * SRC + lane;
+    const double* cNv = sN + bf * SRC + lane;  // this lane's rows: N-0 flow, 1 / rating
+    const double* cIv = sI + bf * SRC + lane;
     for (int i0 = wid * CQ; i0 < ncs; i0 += RW * CQ) {
       double dv[CQ][RPL];
 #pragma unroll
@@ -761,15 +767,20 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? 8 : (CQ == 1 ? 4 : 3)) k_rsw
         const double thresh = one ? fmax(floor_rel, warp_thresh(wl[wid], kg))
                                   : fmax(floor_rel, cN[i] == kc ? cRel[i * KC + kc - 1] : -1.0);
         lt.clear();
+        // the outaged row (flow exactly 0: never reported, 0 in the metric) joins the
+        // skipped rows, so the row loop is single_flow's regular branch only
+        unsigned skq = skip;
+        {
+          const int ou = ownp - m0 - lane;
+          if (ownp >= 0 && ou >= 0 && (ou & 31) == 0 && (ou >> 5) < RPL) skq |= 1u << (ou >> 5);
+        }
 #pragma unroll
         for (int u = 0; u < RPL; ++u) {
-          if (skip & (1u << u)) continue;
-          const int r = lane + 32 * u, p = m0 + r;
-          const double nv = sN[bf * SRC + r];
-          const double f = single_flow(nv, dv[q][u], idn, sc, p == ownp);
-          const double rel = fabs(f) * sI[bf * SRC + r];
-          mymax = fmax(mymax, rel);
-          if (p != ownp && rel >= thresh) lt.insert(rel, p, f);
+          if (skq & (1u << u)) continue;
+          const double f = fma(dv[q][u] * idn, sc, cNv[32 * u]);  // single_flow, not the own row
+          const double rel = fabs(f) * cIv[32 * u];
+          mymax = dmax(mymax, rel);
+          if (rel >= thresh) lt.insert(rel, m0 + lane + 32 * u, f);
         }
         if (!__any_sync(0xffffffffu, lt.rel[0] >= 0.0)) continue;
         if (one) {
@@ -1009,7 +1020,7 @@ __device__ double warp_multi_max(const DevGrid& g, const Work& w, const RsTask& 
       if (is_dead(k.sdead, nd, row)) continue;
       int own;
       const double f = multi_flow(g, w, b, st, m, row, n0_at(g, k.Bm, y, rt, k.sdead, nd, row), sv, sMinv, k.Bm, rt, own);
-      mx = fmax(mx, fabs(f) * g.inv_rating[p]);
+      mx = dmax(mx, fabs(f) * g.inv_rating[p]);
     }
     __syncwarp();
   }
@@ -1025,7 +1036,7 @@ __device__ double warp_class_max(const DevGrid& g, const Work& w, const RsTask& 
   const int M = g.M, N1 = g.N1, nd = k.nd, b = k.b, T = k.T;
   double mx = 0.0;
   for (int p = lane; p < M; p += 32)
-    if (!is_dead(k.sdeadp, nd, p)) mx = fmax(mx, elem_value(g, w, k, y, -1, p));
+    if (!is_dead(k.sdeadp, nd, p)) mx = dmax(mx, elem_value(g, w, k, y, -1, p));
   const int ncand = rel_all ? N1 : nrel;
   for (int k0 = 0; k0 < ncand; k0 += 32) {
     const int kk = k0 + lane;
@@ -1044,7 +1055,7 @@ __device__ double warp_class_max(const DevGrid& g, const Work& w, const RsTask& 
       todo &= todo - 1;
       const int cc = __shfl_sync(0xffffffffu, c, src);
       for (int p = lane; p < M; p += 32)
-        if (!is_dead(k.sdeadp, nd, p)) mx = fmax(mx, elem_value(g, w, k, y, cc, p));
+        if (!is_dead(k.sdeadp, nd, p)) mx = dmax(mx, elem_value(g, w, k, y, cc, p));
     }
   }
   return fmax(warp_max(mx), warp_multi_max(g, w, k, t, y, sMinv));
@@ -1062,7 +1073,7 @@ __device__ double warp_inj_max(const DevGrid& g, const Work& w, const RsTask& k,
     const int row = g.mon_row[p];
     if (is_dead(k.sdead, k.nd, row)) continue;
     const double f = inj_flow(g, ca, coef, sp, row, n0_at(g, k.Bm, y, k.rt, k.sdead, k.nd, row), k.Bm, k.rt);
-    iv = fmax(iv, fabs(f) * g.inv_rating[p]);
+    iv = dmax(iv, fabs(f) * g.inv_rating[p]);
   }
   return warp_max(iv);
 }
@@ -1326,7 +1337,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 12 : 3) k_rescore(DevGrid g, De
         double mx;
         if (hot_ok) {
           mx = 0.0;
-          for (int h = lane; h < nhot; h += 32) mx = fmax(mx, elem_value(g, w, tk, y, sHotC[h], sHotP[h]));
+          for (int h = lane; h < nhot; h += 32) mx = dmax(mx, elem_value(g, w, tk, y, sHotC[h], sHotP[h]));
           mx = warp_max(mx);
           if (sNeedM[i]) mx = fmax(mx, warp_multi_max(g, w, tk, t, y, sMinv[wid], sNeedM[i]));
         } else {
