@@ -108,7 +108,7 @@ enum {
   BDC_STAGE_H2D = 0,      /* input copies + per-wave resets */
   BDC_STAGE_UPDATE = 1,   /* k_update: split chain, outages, case factors */
   BDC_STAGE_N0 = 2,       /* k_n0: N-0 contraction, screening data */
-  BDC_STAGE_OTHER = 3,    /* k_other: multi-branch / injection cases */
+  BDC_STAGE_OTHER = 3,    /* k_terms + k_other (+ k_oscreen): multi-branch / injection cases */
   BDC_STAGE_SCALE = 4,    /* k_scale_tc: screening scales (tcgen05) */
   BDC_STAGE_TOPK = 5,     /* k_topk */
   BDC_STAGE_TOP = 6,      /* k_top: the TOP tile */

@@ -658,6 +658,27 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
   constexpr int NE = BDC_STAGES + 1;  // events per wave
   std::vector<cudaEvent_t> ev((size_t)nwaves * NE);
   for (auto& e : ev) CK(cudaEventCreate(&e));
+  // side stream: the multi/injection correction terms (k_terms) next to the N-0 contraction,
+  // and -- unscreened -- the multi/injection N-1 stream (k_other) next to the single-branch
+  // scales / top-k / TOP tile; joined before the exact screen reads the candidates' lower
+  // bounds.  Only on waves too small to fill the GPU (G10k, 64 topologies: 7.2 -> 6.6 ms);
+  // on full waves the overlapped kernels slow each other down as much as they gain (G118
+  // 20.0 -> 20.1 ms, G3k 17.8 -> 18.0).  Test knob BDC_SIDE=0/1 forces it.
+  const char* side_env = std::getenv("BDC_SIDE");
+  const bool side = (side_env ? side_env[0] == '1' : Wb < 512) && g.NM + g.NI > 0 && g.M > 0;
+  constexpr int NS = 4;  // side events per wave: terms start/end, other start/end
+  const bool terms = g.NM + g.NI > 0 && g.M > 0;  // k_terms timed apart (multi/injection stage)
+  std::vector<cudaEvent_t> sev(terms ? (size_t)nwaves * NS : 0);
+  for (auto& e : sev) CK(cudaEventCreate(&e));
+  struct EvVecGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvVecGuard() { for (auto& e : v) cudaEventDestroy(e); }
+  } sevg{sev};
+  StreamGuard ss;
+  if (side) {
+    CK(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    ss.own = true;
+  }
   const bool ondev_in = bt->inputs_on_device != 0, ondev_out = bt->outputs_on_device != 0;
   const int kg = s->cfg.kg, NCw = w.NCw;
   // pinned staging for host outputs: two wave-sized buffers, unpacked by the host while
@@ -804,12 +825,32 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     // (k_oscreen) sees the TOP cases' maxima.
     launch_update(g, s->cfg, x, st);
     cudaEventRecord(E[2], st);
+    cudaEvent_t* S = terms ? &sev[(size_t)wv * NS] : nullptr;
+    if (side) {  // S[0] follows k_update on the solve stream
+      cudaEventRecord(S[0], st);
+      cudaStreamWaitEvent(ss.s, S[0], 0);
+      launch_terms(g, x, ss.s);
+      cudaEventRecord(S[1], ss.s);
+    } else if (terms) {  // inside the N-0 interval on the solve stream; moved to its stage below
+      cudaEventRecord(S[0], st);
+      launch_terms(g, x, st);
+      cudaEventRecord(S[1], st);
+    }
     launch_n0(g, x, st);
     cudaEventRecord(E[3], st);
     if (x.oscr) {
       launch_single_top(g, s->cfg, x, st, &E[4]);  // records E[4], E[5], E[6]
-      launch_other(g, s->cfg, x, st);
+      if (side) cudaStreamWaitEvent(st, S[1], 0);
+      launch_other(g, s->cfg, x, st);  // its screen reads the TOP tile's maxima
       cudaEventRecord(E[7], st);
+    } else if (side) {  // the multi/injection stream next to the single-branch TOP path
+      cudaStreamWaitEvent(ss.s, E[3], 0);  // reads the N-0 table
+      cudaEventRecord(S[2], ss.s);
+      launch_other(g, s->cfg, x, ss.s);
+      cudaEventRecord(S[3], ss.s);
+      cudaEventRecord(E[4], st);
+      launch_single_top(g, s->cfg, x, st, &E[5]);  // records E[5], E[6], E[7]
+      cudaStreamWaitEvent(st, S[3], 0);  // the screen's lower bounds include those cases
     } else {  // unscreened: the multi/injection stream first (the order measured faster)
       launch_other(g, s->cfg, x, st);
       cudaEventRecord(E[4], st);
@@ -901,6 +942,10 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
     es = cudaStreamSynchronize(cs.s);
     if (err == cudaSuccess) err = es;
   }
+  if (side) {  // likewise the side stream's kernels (an error break can leave them queued)
+    es = cudaStreamSynchronize(ss.s);
+    if (err == cudaSuccess) err = es;
+  }
   if (err == cudaSuccess) {
     for (int wv = 0; wv < nwaves; ++wv) {
       cudaEvent_t* E = &ev[(size_t)wv * NE];
@@ -913,6 +958,16 @@ extern "C" int bdc_solve(BdcSession* s, BdcBatch* bt) {
         if (cudaEventElapsedTime(&ms, E[k], E[k + 1]) == cudaSuccess) {
           bt->stage_ms[kExecStage[k]] += ms;
         }
+      }
+      if (terms) {  // k_terms (and, on the side stream, k_other) belong to the multi/injection stage
+        const cudaEvent_t* S = &sev[(size_t)wv * NS];
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, S[0], S[1]) == cudaSuccess) {
+          bt->stage_ms[BDC_STAGE_OTHER] += ms;
+          if (!side) bt->stage_ms[BDC_STAGE_N0] -= ms;  // it ran inside the N-0 interval
+        }
+        if (side && !w.oscr && cudaEventElapsedTime(&ms, S[2], S[3]) == cudaSuccess)
+          bt->stage_ms[BDC_STAGE_OTHER] += ms;
       }
     }
   }

@@ -348,6 +348,7 @@ int smem_opt_in_max(const void* fn);
 
 // Kernel launchers.
 void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_t s);
+void launch_terms(const DevGrid& g, const Work& w, cudaStream_t s);  // multi/injection terms (k_terms)
 void launch_n0(const DevGrid& g, const Work& w, cudaStream_t s);
 // the single-branch N-1 stage in two parts: scales, top-k and the TOP tile (records ev[0..2]),
 // then the exact screen's live cases (k_live, k_queue, k_pairs)

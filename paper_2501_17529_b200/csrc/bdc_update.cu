@@ -894,8 +894,9 @@ __global__ void __launch_bounds__(NT) k_n0(DevGrid g, Work w) {
           }
           rmax = fmaxf(rmax, fabsf(v));
         }
-        {  // warp-uniform: the row's max over this candidate chunk
-          for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        {  // warp-uniform: the row's max over this candidate chunk (non-negative floats
+           // order as their bit patterns: one redux instead of five shuffle + max steps)
+          rmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(rmax)));
           if (lane == 0) sSmax[i0 + i] = fmaxf(sSmax[i0 + i], rmax);
         }
       }
@@ -1017,6 +1018,11 @@ void launch_update(const DevGrid& g, const DevCfg& c, const Work& w, cudaStream_
     smem_opt_in((const void*)k_update<32, 32>, (int)dyn);
     k_update<32, 32><<<w.Wb, 32, dyn, st>>>(g, c, w);
   }
+}
+
+// The multi/injection correction terms (after k_update; independent of k_n0, so bdc_solve
+// runs them on a side stream next to it).
+void launch_terms(const DevGrid& g, const Work& w, cudaStream_t st) {
   if (w.NTERM > 0 && g.M > 0) {
     // >= 8 items per thread: small grids take one CTA per task (the per-CTA cost, not
     // the items, dominated with several thin CTAs per task), large grids up to eight

@@ -294,10 +294,31 @@ def test_report_select_variants_agree(name, sessions, monkeypatch):
     # the multi/injection dominance screen (k_oscreen + k_oexact) forced on
     monkeypatch.setenv("BDC_OSCREEN", "1")
     osc = eng.solve(*args)
+    # ... with the side stream forced on and off (k_terms, k_other next to / on the solve stream)
+    monkeypatch.setenv("BDC_SIDE", "1")
+    osc2 = eng.solve(*args)
+    monkeypatch.setenv("BDC_SIDE", "0")
+    osc1 = eng.solve(*args)
     monkeypatch.delenv("BDC_OSCREEN")
     assert np.array_equal(warp.best, osc.best)
     assert np.array_equal(warp.metric, osc.metric, equal_nan=True)
     assert warp.reports() == osc.reports()
+    assert np.array_equal(osc1.metric, osc.metric, equal_nan=True)
+    assert osc1.reports() == osc.reports() and osc1.n1_pairs == osc.n1_pairs
+    assert np.array_equal(osc2.metric, osc.metric, equal_nan=True)
+    assert osc2.reports() == osc.reports() and osc2.n1_pairs == osc.n1_pairs
+    # one stream for everything, and the side stream next to the N-0 contraction / TOP path
+    ser = eng.solve(*args)
+    monkeypatch.setenv("BDC_SIDE", "1")
+    sid = eng.solve(*args)
+    monkeypatch.delenv("BDC_SIDE")
+    assert np.array_equal(warp.metric, sid.metric, equal_nan=True)
+    assert warp.reports() == sid.reports()
+    assert warp.n1_pairs == sid.n1_pairs and warp.loadflows == sid.loadflows
+    assert np.array_equal(warp.best, ser.best)
+    assert np.array_equal(warp.metric, ser.metric, equal_nan=True)
+    assert warp.reports() == ser.reports()
+    assert warp.n1_pairs == ser.n1_pairs and warp.loadflows == ser.loadflows
     monkeypatch.setenv("BDC_RSWEEP_NT", "256")  # one-chunk sweep with 256- instead of 128-thread CTAs
     nt = eng.solve(*args)
     monkeypatch.delenv("BDC_RSWEEP_NT")
