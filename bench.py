@@ -601,19 +601,20 @@ def run_ours(args):
     roof = stage_rooflines(tb, splits, discos, fe, T, evaluated, stage_ms, report_cases / args.steps,
                            rescore[0] / args.steps)
     dom = max(roof, key=lambda r: r["kernel_ms_per_step"])  # the longest stage with a roofline
-    traffic = None
+    # DRAM bytes per launch (ncu --set full, per task, scaled to this launch size) of every
+    # stage's kernels, where profiles/kernel_traffic.json has them for this config
+    tj = {}
     tp = os.path.join(REPO, "profiles", "kernel_traffic.json")
     if os.path.exists(tp):
         try:
             with open(tp) as fh:
-                tj = json.load(fh)
-            per_task = tj.get(args.config, {}).get(dom["kernel"].split()[0])
-            if per_task:
-                traffic = per_task * B / max(1, waves)  # DRAM bytes per launch (ncu --set full)
+                tj = json.load(fh).get(args.config, {})
         except (OSError, ValueError):
-            traffic = None
+            tj = {}
+    for r in roof:
+        per_task = tj.get(r["kernel"].split()[0])
+        r["traffic"] = per_task * B / max(1, waves) if per_task else None
     roofline = dict(dom)
-    roofline["traffic"] = traffic
     step_ms = elapsed_max / args.steps
     line = {
         "metric": "DC loadflows/sec (topo x inj x N-1)",

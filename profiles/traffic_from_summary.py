@@ -8,7 +8,7 @@ import re
 import sys
 
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-GROUPS = {"k_update": ["k_update", "k_terms"], "k_n0": ["k_n0"], "k_scale_tc": ["k_scale_tc"],
+GROUPS = {"k_update": ["k_update"], "k_n0": ["k_n0"], "k_scale_tc": ["k_scale_tc"],
           "k_top": ["^k_top$", "k_live", "k_pairs"], "k_rsel": ["k_oexact", "k_rsel", "k_rsweep"],
           "k_select": ["k_rescore"]}
 
@@ -31,7 +31,7 @@ def main(path, tag):
     out = {"note": "DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) per task of the "
                    "kernels behind each bench roofline stage, from the --set full captures in "
                    f"profiles/{tag}/ (one launch each); bench.py scales them to its own launch size. "
-                   "k_update = k_update + k_terms, k_top = k_top + k_live + k_pairs, k_rsel = the winner report "
+                   "k_update = k_update (k_terms is timed in the multi/injection stage), k_top = k_top + k_live + k_pairs, k_rsel = the winner report "
                    "(k_oexact + k_rsel + k_rsweep), k_select = k_rescore."}
     for cfg in sorted({c for _, c in caps}):
         out[cfg] = {g: sum(caps.get((k, cfg), 0.0) for k in ks) for g, ks in GROUPS.items()}
