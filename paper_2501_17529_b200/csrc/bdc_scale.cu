@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(2 * SM_CASES, 1) k_scale_tc(DevGrid g, Work w,
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     // epilogue: this warpgroup's 32-row half (a screening block holds whole halves)
     const int r0 = ch * SM_ROWS + wg * 32;
-    if (r0 < M) {
+    // warps whose 32 cases all lie past N1 (the last case tile of G118: 24 of 128) skip
+    // the epilogue: their accumulators are never read
+    if (r0 < M && c0 + (wid & 3) * 32 < N1) {
       const int blk = r0 / MB;
       if (blk != curblk) {
         flush();
