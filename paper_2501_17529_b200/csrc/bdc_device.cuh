@@ -319,18 +319,21 @@ __device__ __forceinline__ float smax_at(const DevGrid& g, const Work& w, int b,
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
-// 4-byte async copy global->shared; src_bytes = 0 zero-fills.
+// Async copies global->shared; !ok stores zeros instead.  The zeros are a plain shared
+// store rather than cp.async's src-size zero-fill: a runtime source size costs ~15 extra
+// SASS instructions per copy (address re-alignment arithmetic), a predicated store one.
+// Readers wait for the copy group and a barrier either way, so both are visible to them.
 __device__ __forceinline__ void cp4(void* dst, const void* src, bool ok) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(ok ? 4 : 0));
+  if (ok) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src));
+  else *reinterpret_cast<uint32_t*>(dst) = 0u;
 }
 __device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(ok ? 8 : 0));
+  if (ok) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+  else *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
 }
 __device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(ok ? 16 : 0));
+  if (ok) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+  else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
