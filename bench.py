@@ -121,6 +121,12 @@ class ClockSampler:
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # a timed region shorter than the sampling period: the first sample right after it
+        after = False
+        t0 = time.perf_counter()
+        while not self.lines and time.perf_counter() - t0 < 0.5:
+            after = True
+            time.sleep(0.005)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -141,13 +147,16 @@ class ClockSampler:
             for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {
+        out = {
             "sm_mhz": statistics.median(sm) if sm else None,
             "sm_max_mhz": max(smax) if smax else None,
             "reasons": sorted(reasons),
             "samples": len(sm),
             "power_w_max": max(power) if power else None,
         }
+        if after and sm:
+            out["note"] = "timed region shorter than the 50 ms sampling period: first sample right after it"
+        return out
 
 
 def make_workload(name, rank, n_tasks=None, n_cand=None):
