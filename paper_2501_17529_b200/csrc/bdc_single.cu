@@ -374,31 +374,54 @@ __global__ void __launch_bounds__(LC) k_live(DevGrid g, DevCfg cfg, Work w) {
   }
   bool mylive = cand && !w.screen;
   unsigned todo = __ballot_sync(0xffffffffu, cand && w.screen);
+  // two cases per pass: their s rows are loaded together, so each pass waits on one memory
+  // latency for two cases (the loop is latency-bound); a case's verdict is the same --
+  // "live" once any candidate's bound exceeds the lower bound, extra chunks cannot undo it
   while (todo) {
-    const int k = __ffs(todo) - 1;
+    const int k1 = __ffs(todo) - 1;
     todo &= todo - 1;
-    const int c = blockIdx.x * LC + wid * 32 + k;
-    float sk[SB];
-#pragma unroll
-    for (int blk = 0; blk < SB; ++blk) sk[blk] = __shfl_sync(0xffffffffu, scl[blk], k);
-    // s(c, .): a row of s32, or the N-0 row of the outaged branch times its rating
-    const float* sc = g.s_mon ? w.n0s + ((size_t)b * g.M + g.sc_pos[c]) * T : w.s32 + ((size_t)b * N1 + c) * T;
-    const float srat = g.s_mon ? g.sc_rat[c] : 1.f;
-    bool live = false;
-    for (int t0 = 0; t0 < T && !live; t0 += 32) {
-      const int t = t0 + lane;
-      bool lt = false;
-      if (t < T) {
-        const float as = g.s_mon ? fabsf(sc[t] * srat) : fabsf(sc[t]);
-        float bound = 0.f;
-#pragma unroll
-        for (int blk = 0; blk < SB; ++blk)
-          bound = fmaxf(bound, (staged ? sM0[blk][t] : m0b[(size_t)blk * T + t]) + sk[blk] * as);
-        lt = bound > (staged ? sLb[t] : fmaxf(m32[t], pen));
-      }
-      live = __any_sync(0xffffffffu, lt);
+    int k2 = -1;
+    if (todo) {
+      k2 = __ffs(todo) - 1;
+      todo &= todo - 1;
     }
-    if (lane == k) mylive = live;
+    const int c1 = blockIdx.x * LC + wid * 32 + k1;
+    const int c2 = k2 >= 0 ? blockIdx.x * LC + wid * 32 + k2 : c1;
+    float sk1[SB], sk2[SB];
+#pragma unroll
+    for (int blk = 0; blk < SB; ++blk) {
+      sk1[blk] = __shfl_sync(0xffffffffu, scl[blk], k1);
+      sk2[blk] = __shfl_sync(0xffffffffu, scl[blk], k2 >= 0 ? k2 : k1);
+    }
+    // s(c, .): a row of s32, or the N-0 row of the outaged branch times its rating
+    const float* sc1 = g.s_mon ? w.n0s + ((size_t)b * g.M + g.sc_pos[c1]) * T : w.s32 + ((size_t)b * N1 + c1) * T;
+    const float* sc2 = g.s_mon ? w.n0s + ((size_t)b * g.M + g.sc_pos[c2]) * T : w.s32 + ((size_t)b * N1 + c2) * T;
+    const float srat1 = g.s_mon ? g.sc_rat[c1] : 1.f;
+    const float srat2 = g.s_mon ? g.sc_rat[c2] : 1.f;
+    bool live1 = false, live2 = k2 < 0;
+    for (int t0 = 0; t0 < T && !(live1 && live2); t0 += 32) {
+      const int t = t0 + lane;
+      bool lt1 = false, lt2 = false;
+      if (t < T) {
+        const float v1 = sc1[t], v2 = sc2[t];
+        const float as1 = g.s_mon ? fabsf(v1 * srat1) : fabsf(v1);
+        const float as2 = g.s_mon ? fabsf(v2 * srat2) : fabsf(v2);
+        float b1 = 0.f, b2 = 0.f;
+#pragma unroll
+        for (int blk = 0; blk < SB; ++blk) {
+          const float m0v = staged ? sM0[blk][t] : m0b[(size_t)blk * T + t];
+          b1 = fmaxf(b1, m0v + sk1[blk] * as1);
+          b2 = fmaxf(b2, m0v + sk2[blk] * as2);
+        }
+        const float lbt = staged ? sLb[t] : fmaxf(m32[t], pen);
+        lt1 = b1 > lbt;
+        lt2 = k2 >= 0 && b2 > lbt;
+      }
+      live1 = live1 || __any_sync(0xffffffffu, lt1);
+      live2 = live2 || __any_sync(0xffffffffu, lt2);
+    }
+    if (lane == k1) mylive = live1;
+    if (k2 >= 0 && lane == k2) mylive = live2;
   }
   if (cl < N1 && (cand || !w.ranked)) {
     // TOP cases keep done = 1 (k_topk); unranked tasks have no k_topk pass
